@@ -1,0 +1,216 @@
+"""B200-native 2D Neighborhood Attention (arXiv 2204.07143) -- thin Python binding.
+
+Every step of the path runs in ``libna2d.so`` (hand-written sm_100a CUDA kernels behind the
+C ABI in ``include/na2d.h``).  This module only marshals arguments: torch supplies device
+memory and the current CUDA stream.  There is no CPU fallback: if the library is missing, or a
+tensor is not on a CUDA device, calls raise.
+
+Low level (same names as the C ABI, integer device pointers):
+    na2d_forward, na2d_backward, na2d_backward_workspace_bytes, na2d_step_host,
+    na2d_step_host_workspace_bytes, na2d_launch_count, na2d_kernel_family, na2d_status_string
+Torch level:
+    forward(q, k, v, rpb, kernel_size, scale=None) -> (out, lse)
+    backward(q, k, v, rpb, out, lse, dout, kernel_size, scale=None) -> (dq, dk, dv, drpb)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libna2d.so")
+
+NA2D_BF16, NA2D_F32 = 0, 1
+_STATUS = ["ok", "null pointer", "kernel size", "shape", "dtype", "unsupported", "alignment", "workspace",
+           "invalid argument", "cuda"]
+
+
+class NA2DError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        self.status = status
+        super().__init__(f"{what}: status {status} ({na2d_status_string(status)})")
+
+
+class na2d_problem(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int32), ("heads", ctypes.c_int32), ("height", ctypes.c_int32),
+                ("width", ctypes.c_int32), ("dim", ctypes.c_int32), ("kernel_size", ctypes.c_int32),
+                ("dtype", ctypes.c_int32), ("scale", ctypes.c_float), ("map_height", ctypes.c_int32),
+                ("q_row0", ctypes.c_int32), ("kv_row0", ctypes.c_int32), ("kv_rows", ctypes.c_int32)]
+
+
+EXPORTS = ("na2d_status_string", "na2d_version", "na2d_forward", "na2d_backward_workspace_bytes",
+           "na2d_backward", "na2d_step_host_workspace_bytes", "na2d_step_host", "na2d_launch_count",
+           "na2d_kernel_family", "na2d_profile_enable", "na2d_profile_read")
+
+_lib = None
+
+
+def load_library():
+    """Load libna2d.so (raises if it was not built: there is no fallback path)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not found: build it with `python -m paper_2204_07143_b200.build` "
+                          "(no CPU or eager fallback exists)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, PP, VP, SZ = ctypes.POINTER(na2d_problem), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t
+    lib.na2d_status_string.argtypes = [ctypes.c_int]
+    lib.na2d_status_string.restype = ctypes.c_char_p
+    lib.na2d_version.restype = ctypes.c_int
+    lib.na2d_forward.argtypes = [P] + [VP] * 7
+    lib.na2d_forward.restype = ctypes.c_int
+    lib.na2d_backward_workspace_bytes.argtypes = [P]
+    lib.na2d_backward_workspace_bytes.restype = SZ
+    lib.na2d_backward.argtypes = [P] + [VP] * 12 + [SZ, VP]
+    lib.na2d_backward.restype = ctypes.c_int
+    lib.na2d_step_host_workspace_bytes.argtypes = [P]
+    lib.na2d_step_host_workspace_bytes.restype = SZ
+    lib.na2d_step_host.argtypes = [P] + [VP] * 12 + [SZ, VP]
+    lib.na2d_step_host.restype = ctypes.c_int
+    lib.na2d_launch_count.argtypes = [P, ctypes.c_int]
+    lib.na2d_launch_count.restype = ctypes.c_int
+    lib.na2d_kernel_family.argtypes = [P, ctypes.c_int]
+    lib.na2d_kernel_family.restype = ctypes.c_char_p
+    lib.na2d_profile_enable.argtypes = [ctypes.c_int]
+    lib.na2d_profile_enable.restype = ctypes.c_int
+    lib.na2d_profile_read.argtypes = [ctypes.c_char_p, SZ, ctypes.POINTER(ctypes.c_float),
+                                      ctypes.POINTER(ctypes.c_int), ctypes.c_int]
+    lib.na2d_profile_read.restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def make_problem(batch, heads, height, width, dim, kernel_size, dtype=NA2D_BF16, scale=None, *,
+                 map_height=0, q_row0=0, kv_row0=0, kv_rows=0) -> na2d_problem:
+    if scale is None:
+        scale = dim ** -0.5 if dim > 0 else 1.0
+    return na2d_problem(batch, heads, height, width, dim, kernel_size, dtype, float(scale), map_height, q_row0,
+                        kv_row0, kv_rows)
+
+
+# ------------------------------------------------------------------ C ABI, same names
+
+def na2d_status_string(status: int) -> str:
+    return load_library().na2d_status_string(status).decode()
+
+
+def _check(status: int, what: str):
+    if status != 0:
+        raise NA2DError(status, what)
+
+
+def na2d_forward(p: na2d_problem, q: int, k: int, v: int, rpb: int | None, out: int, lse: int | None,
+                 stream: int | None) -> None:
+    _check(load_library().na2d_forward(ctypes.byref(p), q, k, v, rpb, out, lse, stream), "na2d_forward")
+
+
+def na2d_backward_workspace_bytes(p: na2d_problem) -> int:
+    return load_library().na2d_backward_workspace_bytes(ctypes.byref(p))
+
+
+def na2d_backward(p, q, k, v, rpb, out, lse, dout, dq, dk, dv, drpb, workspace, workspace_bytes, stream) -> None:
+    _check(load_library().na2d_backward(ctypes.byref(p), q, k, v, rpb, out, lse, dout, dq, dk, dv, drpb,
+                                        workspace, workspace_bytes, stream), "na2d_backward")
+
+
+def na2d_step_host_workspace_bytes(p: na2d_problem) -> int:
+    return load_library().na2d_step_host_workspace_bytes(ctypes.byref(p))
+
+
+def na2d_step_host(p, q, k, v, rpb, dout, out, lse, dq, dk, dv, drpb, workspace, workspace_bytes, stream) -> None:
+    _check(load_library().na2d_step_host(ctypes.byref(p), q, k, v, rpb, dout, out, lse, dq, dk, dv, drpb,
+                                         workspace, workspace_bytes, stream), "na2d_step_host")
+
+
+def na2d_launch_count(p: na2d_problem, which: int) -> int:
+    return load_library().na2d_launch_count(ctypes.byref(p), which)
+
+
+def na2d_kernel_family(p: na2d_problem, which: int) -> str | None:
+    r = load_library().na2d_kernel_family(ctypes.byref(p), which)
+    return None if r is None else r.decode()
+
+
+def na2d_profile_enable(on: bool) -> None:
+    _check(load_library().na2d_profile_enable(1 if on else 0), "na2d_profile_enable")
+
+
+def na2d_profile_read() -> dict:
+    """{kernel name: (total_ms, launches)} recorded since na2d_profile_enable(True)."""
+    lib = load_library()
+    n = 64
+    names = ctypes.create_string_buffer(8192)
+    ms = (ctypes.c_float * n)()
+    cnt = (ctypes.c_int * n)()
+    k = lib.na2d_profile_read(names, 8192, ms, cnt, n)
+    if k < 0:
+        raise NA2DError(9, "na2d_profile_read")
+    out, parts = {}, names.raw.split(b"\0")
+    for i in range(min(k, n)):
+        out[parts[i].decode()] = (float(ms[i]), int(cnt[i]))
+    return out
+
+
+# ------------------------------------------------------------------ torch convenience layer
+
+def _dtype_code(t):
+    import torch
+    if t.dtype == torch.bfloat16:
+        return NA2D_BF16
+    if t.dtype == torch.float32:
+        return NA2D_F32
+    raise TypeError(f"unsupported dtype {t.dtype} (bf16 or fp32)")
+
+
+def _dev(t, name):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU path exists)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t.data_ptr()
+
+
+def _stream(t):
+    import torch
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def problem_for(q, k, kernel_size, scale=None, *, map_height=0, q_row0=0, kv_row0=0) -> na2d_problem:
+    B, heads, H, W, d = q.shape
+    return make_problem(B, heads, H, W, d, kernel_size, _dtype_code(q), scale, map_height=map_height,
+                        q_row0=q_row0, kv_row0=kv_row0, kv_rows=k.shape[2])
+
+
+def forward(q, k, v, rpb, kernel_size: int, scale: float | None = None, *, map_height=0, q_row0=0, kv_row0=0,
+            out=None, lse=None):
+    """Eq. 2 forward.  q: [B,heads,H,W,d] (bf16 or fp32, CUDA); k, v: [B,heads,kv_rows,W,d];
+    rpb: [heads,2L-1,2L-1] fp32 or None.  Returns (out, lse fp32 [B,heads,H,W])."""
+    import torch
+    p = problem_for(q, k, kernel_size, scale, map_height=map_height, q_row0=q_row0, kv_row0=kv_row0)
+    out = torch.empty_like(q) if out is None else out
+    lse = torch.empty(q.shape[:4], device=q.device, dtype=torch.float32) if lse is None else lse
+    na2d_forward(p, _dev(q, "q"), _dev(k, "k"), _dev(v, "v"), _dev(rpb, "rpb"), _dev(out, "out"), _dev(lse, "lse"),
+                 _stream(q))
+    return out, lse
+
+
+def backward(q, k, v, rpb, out, lse, dout, kernel_size: int, scale: float | None = None, *, map_height=0,
+             q_row0=0, kv_row0=0, workspace=None, grads=None):
+    """Analytic backward of Eq. 2.  Returns (dq, dk, dv, drpb or None)."""
+    import torch
+    p = problem_for(q, k, kernel_size, scale, map_height=map_height, q_row0=q_row0, kv_row0=kv_row0)
+    nbytes = na2d_backward_workspace_bytes(p)
+    if workspace is None or workspace.numel() < nbytes:
+        workspace = torch.empty(max(nbytes, 16), device=q.device, dtype=torch.uint8)
+    if grads is None:
+        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+        drpb = torch.empty_like(rpb) if rpb is not None else None
+    else:
+        dq, dk, dv, drpb = grads
+    na2d_backward(p, _dev(q, "q"), _dev(k, "k"), _dev(v, "v"), _dev(rpb, "rpb"), _dev(out, "out"),
+                  _dev(lse, "lse"), _dev(dout, "dout"), _dev(dq, "dq"), _dev(dk, "dk"), _dev(dv, "dv"),
+                  _dev(drpb, "drpb"), _dev(workspace, "workspace"), workspace.numel(), _stream(q))
+    return dq, dk, dv, drpb

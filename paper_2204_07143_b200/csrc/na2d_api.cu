@@ -1,0 +1,218 @@
+// na2d_api.cu -- the C ABI declared in include/na2d.h: argument validation, workspace
+// layout, kernel-family dispatch and the host-buffer end-to-end step.
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "na2d_internal.cuh"
+#include "na2d_tc.cuh"
+
+namespace na2d {
+namespace {
+
+constexpr int kMaxKernel = 31;  // SIMT dRPB staging bound ((2L-1)^2 floats of shared memory)
+
+bool aligned16(const void *p) { return p == nullptr || ((uintptr_t)p & 15u) == 0; }
+
+// Synchronous validation; fills g on success.
+na2d_status make_geo(const na2d_problem *p, Geo *g) {
+  if (!p) return NA2D_ERR_NULL_POINTER;
+  if (p->dtype != NA2D_BF16 && p->dtype != NA2D_F32) return NA2D_ERR_DTYPE;
+  if (p->kernel_size < 3 || (p->kernel_size % 2) == 0) return NA2D_ERR_KERNEL_SIZE;
+  if (p->batch <= 0 || p->heads <= 0 || p->height <= 0 || p->width <= 0 || p->dim <= 0) return NA2D_ERR_SHAPE;
+  if (!(isfinite(p->scale) && p->scale > 0.f)) return NA2D_ERR_INVALID_ARG;
+  if (p->dim > 128 || (p->dim % 2) != 0 || p->kernel_size > kMaxKernel) return NA2D_ERR_UNSUPPORTED;
+  g->B = p->batch;
+  g->heads = p->heads;
+  g->W = p->width;
+  g->d = p->dim;
+  g->L = p->kernel_size;
+  g->scale = p->scale;
+  g->dtype = p->dtype;
+  g->q_rows = p->height;
+  g->q_row0 = p->q_row0;
+  g->H = p->map_height > 0 ? p->map_height : p->height;
+  g->kv_row0 = p->kv_row0;
+  g->kv_rows = p->kv_rows > 0 ? p->kv_rows : p->height;
+  if (p->map_height < 0 || p->kv_rows < 0) return NA2D_ERR_SHAPE;
+  if (g->q_row0 < 0 || g->q_row0 + g->q_rows > g->H) return NA2D_ERR_SHAPE;
+  if (g->kv_row0 < 0 || g->kv_row0 + g->kv_rows > g->H) return NA2D_ERR_SHAPE;
+  // every held query row's window must lie inside the held K/V rows (monotone starts)
+  const int s0 = wstart(g->q_row0, g->H, g->L);
+  const int s1 = wstart(g->q_row0 + g->q_rows - 1, g->H, g->L) + wlen(g->H, g->L);
+  if (s0 < g->kv_row0 || s1 > g->kv_row0 + g->kv_rows) return NA2D_ERR_SHAPE;
+  // 64-bit element counts must stay far from overflow
+  const double elems = (double)g->B * g->heads * (double)(g->q_rows > g->kv_rows ? g->q_rows : g->kv_rows) *
+                       g->W * g->d;
+  if (elems > 9.0e15 || (double)g->B * g->heads > 2147483647.0) return NA2D_ERR_SHAPE;
+  return NA2D_OK;
+}
+
+size_t elem_size(const Geo &g) { return g.dtype == NA2D_F32 ? 4 : 2; }
+size_t n_query(const Geo &g) { return (size_t)g.B * g.heads * g.q_rows * g.W; }
+size_t n_key(const Geo &g) { return (size_t)g.B * g.heads * g.kv_rows * g.W; }
+size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+bool force_simt() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("NA2D_FORCE_SIMT");
+    v = (e && e[0] && e[0] != '0') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+bool use_tc(const Geo &g, int which) {
+  if (force_simt()) return false;
+  return which == 0 ? tc_forward_supported(g) : tc_backward_supported(g);
+}
+
+// Workspace: [D fp32 per query | tensor-core backward scratch]
+size_t bwd_ws(const Geo &g) {
+  size_t b = align_up(n_query(g) * sizeof(float));
+  if (use_tc(g, 1)) b += align_up(tc_backward_scratch_bytes(g));
+  return b;
+}
+
+na2d_status cuda_status(cudaError_t e) { return e == cudaSuccess ? NA2D_OK : NA2D_ERR_CUDA; }
+
+}  // namespace
+}  // namespace na2d
+
+using namespace na2d;
+
+extern "C" {
+
+const char *na2d_status_string(na2d_status s) {
+  switch (s) {
+    case NA2D_OK: return "ok";
+    case NA2D_ERR_NULL_POINTER: return "a required pointer is NULL";
+    case NA2D_ERR_KERNEL_SIZE: return "kernel_size must be odd and >= 3 (PAPER App. A: odd number greater than 1)";
+    case NA2D_ERR_SHAPE: return "invalid shape (dimension <= 0, overflow, or band misses needed K/V rows)";
+    case NA2D_ERR_DTYPE: return "dtype must be NA2D_BF16 or NA2D_F32";
+    case NA2D_ERR_UNSUPPORTED: return "unsupported problem (dim must be even and <= 128, kernel_size <= 31)";
+    case NA2D_ERR_ALIGNMENT: return "tensor base pointers must be 16-byte aligned";
+    case NA2D_ERR_WORKSPACE: return "workspace smaller than na2d_backward_workspace_bytes()";
+    case NA2D_ERR_INVALID_ARG: return "invalid argument (scale must be finite and > 0; drpb must be NULL iff rpb is NULL)";
+    case NA2D_ERR_CUDA: return "CUDA runtime error";
+  }
+  return "unknown status";
+}
+
+int na2d_version(void) { return NA2D_VERSION; }
+
+na2d_status na2d_forward(const na2d_problem *p, const void *q, const void *k, const void *v, const float *rpb,
+                         void *out, float *lse, void *stream) {
+  Geo g;
+  na2d_status s = make_geo(p, &g);
+  if (s != NA2D_OK) return s;
+  if (!q || !k || !v || !out) return NA2D_ERR_NULL_POINTER;
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(out) || !aligned16(lse) || !aligned16(rpb))
+    return NA2D_ERR_ALIGNMENT;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (use_tc(g, 0)) return cuda_status(tc_forward(g, q, k, v, rpb, out, lse, st));
+  return cuda_status(simt_forward(g, q, k, v, rpb, out, lse, st));
+}
+
+size_t na2d_backward_workspace_bytes(const na2d_problem *p) {
+  Geo g;
+  if (make_geo(p, &g) != NA2D_OK) return 0;
+  return bwd_ws(g);
+}
+
+na2d_status na2d_backward(const na2d_problem *p, const void *q, const void *k, const void *v, const float *rpb,
+                          const void *out, const float *lse, const void *dout, void *dq, void *dk, void *dv,
+                          float *drpb, void *workspace, size_t workspace_bytes, void *stream) {
+  Geo g;
+  na2d_status s = make_geo(p, &g);
+  if (s != NA2D_OK) return s;
+  if (!q || !k || !v || !out || !lse || !dout || !dq || !dk || !dv) return NA2D_ERR_NULL_POINTER;
+  if ((rpb == nullptr) != (drpb == nullptr)) return NA2D_ERR_INVALID_ARG;
+  const size_t need = bwd_ws(g);
+  if (workspace_bytes < need) return NA2D_ERR_WORKSPACE;
+  if (!workspace) return NA2D_ERR_NULL_POINTER;
+  const void *ptrs[] = {q, k, v, rpb, out, lse, dout, dq, dk, dv, drpb, workspace};
+  for (const void *ptr : ptrs)
+    if (!aligned16(ptr)) return NA2D_ERR_ALIGNMENT;
+  cudaStream_t st = (cudaStream_t)stream;
+  float *D = (float *)workspace;
+  if (use_tc(g, 1)) {
+    void *scratch = (char *)workspace + align_up(n_query(g) * sizeof(float));
+    return cuda_status(tc_backward(g, q, k, v, rpb, out, lse, dout, dq, dk, dv, drpb, D, scratch, st));
+  }
+  return cuda_status(simt_backward(g, q, k, v, rpb, out, lse, dout, dq, dk, dv, drpb, D, st));
+}
+
+size_t na2d_step_host_workspace_bytes(const na2d_problem *p) {
+  Geo g;
+  if (make_geo(p, &g) != NA2D_OK) return 0;
+  if (g.q_rows != g.H || g.kv_rows != g.H) return 0;
+  const size_t t = align_up(n_query(g) * g.d * elem_size(g));
+  const size_t TT = 2 * g.L - 1;
+  // q k v dout out dq dk dv | lse | rpb drpb | backward workspace
+  return 8 * t + align_up(n_query(g) * sizeof(float)) + 2 * align_up(g.heads * TT * TT * sizeof(float)) + bwd_ws(g);
+}
+
+na2d_status na2d_step_host(const na2d_problem *p, const void *q, const void *k, const void *v, const float *rpb,
+                           const void *dout, void *out, float *lse, void *dq, void *dk, void *dv, float *drpb,
+                           void *device_workspace, size_t workspace_bytes, void *stream) {
+  Geo g;
+  na2d_status s = make_geo(p, &g);
+  if (s != NA2D_OK) return s;
+  if (g.q_rows != g.H || g.kv_rows != g.H || g.q_row0 || g.kv_row0) return NA2D_ERR_SHAPE;
+  if (!q || !k || !v || !dout || !out || !lse || !dq || !dk || !dv || !device_workspace) return NA2D_ERR_NULL_POINTER;
+  if ((rpb == nullptr) != (drpb == nullptr)) return NA2D_ERR_INVALID_ARG;
+  const size_t need = na2d_step_host_workspace_bytes(p);
+  if (workspace_bytes < need) return NA2D_ERR_WORKSPACE;
+  if (!aligned16(device_workspace)) return NA2D_ERR_ALIGNMENT;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t bytes = n_query(g) * g.d * elem_size(g);
+  const size_t t = align_up(bytes);
+  const size_t TT = 2 * g.L - 1;
+  const size_t tb = g.heads * TT * TT * sizeof(float);
+  char *w = (char *)device_workspace;
+  char *dq_ = w, *dk_ = w + t, *dv_ = w + 2 * t, *dout_ = w + 3 * t, *out_ = w + 4 * t;
+  char *q_ = w + 5 * t, *k_ = w + 6 * t, *v_ = w + 7 * t;
+  float *lse_ = (float *)(w + 8 * t);
+  float *rpb_ = (float *)(w + 8 * t + align_up(n_query(g) * sizeof(float)));
+  float *drpb_ = (float *)((char *)rpb_ + align_up(tb));
+  char *ws = (char *)drpb_ + align_up(tb);
+  cudaError_t e = cudaSuccess;
+#define NA2D_TRY(x)                  \
+  do {                               \
+    e = (x);                         \
+    if (e != cudaSuccess) return NA2D_ERR_CUDA; \
+  } while (0)
+  NA2D_TRY(cudaMemcpyAsync(q_, q, bytes, cudaMemcpyHostToDevice, st));
+  NA2D_TRY(cudaMemcpyAsync(k_, k, bytes, cudaMemcpyHostToDevice, st));
+  NA2D_TRY(cudaMemcpyAsync(v_, v, bytes, cudaMemcpyHostToDevice, st));
+  NA2D_TRY(cudaMemcpyAsync(dout_, dout, bytes, cudaMemcpyHostToDevice, st));
+  if (rpb) NA2D_TRY(cudaMemcpyAsync(rpb_, rpb, tb, cudaMemcpyHostToDevice, st));
+  s = na2d_forward(p, q_, k_, v_, rpb ? rpb_ : nullptr, out_, lse_, stream);
+  if (s != NA2D_OK) return s;
+  s = na2d_backward(p, q_, k_, v_, rpb ? rpb_ : nullptr, out_, lse_, dout_, dq_, dk_, dv_, rpb ? drpb_ : nullptr, ws,
+                    bwd_ws(g), stream);
+  if (s != NA2D_OK) return s;
+  NA2D_TRY(cudaMemcpyAsync(out, out_, bytes, cudaMemcpyDeviceToHost, st));
+  NA2D_TRY(cudaMemcpyAsync(lse, lse_, n_query(g) * sizeof(float), cudaMemcpyDeviceToHost, st));
+  NA2D_TRY(cudaMemcpyAsync(dq, dq_, bytes, cudaMemcpyDeviceToHost, st));
+  NA2D_TRY(cudaMemcpyAsync(dk, dk_, bytes, cudaMemcpyDeviceToHost, st));
+  NA2D_TRY(cudaMemcpyAsync(dv, dv_, bytes, cudaMemcpyDeviceToHost, st));
+  if (drpb) NA2D_TRY(cudaMemcpyAsync(drpb, drpb_, tb, cudaMemcpyDeviceToHost, st));
+#undef NA2D_TRY
+  return NA2D_OK;
+}
+
+int na2d_launch_count(const na2d_problem *p, int which) {
+  Geo g;
+  if (make_geo(p, &g) != NA2D_OK || (which != 0 && which != 1)) return -1;
+  return use_tc(g, which) ? tc_launches(g, which) : simt_launches(g, which);
+}
+
+const char *na2d_kernel_family(const na2d_problem *p, int which) {
+  Geo g;
+  if (make_geo(p, &g) != NA2D_OK || (which != 0 && which != 1)) return nullptr;
+  return use_tc(g, which) ? "tcgen05" : "simt";
+}
+
+}  // extern "C"

@@ -1,0 +1,66 @@
+"""Shared parity helpers: run the CUDA path (through the C ABI binding) and the fp64 oracle
+on the same seeded inputs and compare element by element with the tolerances of
+BASELINE.json's north_star:
+
+* bf16 I/O, fp32 accumulate: max |gpu - oracle| <= 2e-2 on out, lse, dq, dk, dv;
+  drpb <= 2e-2 * max(1, ||drpb_oracle||_inf) (a sum over up to B*H*W terms, reading R7);
+* fp32 path: ||gpu - oracle||_inf <= 1e-4 * max(1, ||oracle||_inf) per tensor.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+BF16_ATOL = 2e-2
+F32_RTOL = 1e-4
+
+
+def tolerance(name: str, ref: np.ndarray, dtype: str) -> float:
+    scale = max(1.0, float(np.abs(ref).max())) if ref.size else 1.0
+    if dtype == "f32":
+        return F32_RTOL * scale
+    return BF16_ATOL * (scale if name == "drpb" else 1.0)
+
+
+def compare(got: dict, ref: dict, dtype: str, names=None) -> dict:
+    """Return {name: (max_abs_err, tol)}; raises AssertionError on the first violation."""
+    report = {}
+    for n in names or got.keys():
+        g, r = got[n], ref[n]
+        if g is None or r is None:
+            assert g is None and r is None, n
+            continue
+        g = np.asarray(g, np.float64)
+        r = np.asarray(r, np.float64)
+        assert g.shape == r.shape, (n, g.shape, r.shape)
+        assert np.all(np.isfinite(g)), f"{n}: non-finite values"
+        err = float(np.abs(g - r).max()) if g.size else 0.0
+        tol = tolerance(n, r, dtype)
+        report[n] = (err, tol)
+        assert err <= tol, f"{n}: max abs err {err:.3e} > tol {tol:.3e}"
+    return report
+
+
+def run_oracle(inp: dict, L: int, scale: float, backward: bool = True, **band):
+    import oracle
+    if backward:
+        return oracle.na2d_backward(inp["q"], inp["k"], inp["v"], inp["rpb"], inp["dout"], L, scale, **band)
+    out, lse = oracle.na2d_forward(inp["q"], inp["k"], inp["v"], inp["rpb"], L, scale, **band)
+    return dict(out=out, lse=lse)
+
+
+def run_cuda(inp: dict, L: int, scale: float, dtype: str, backward: bool = True, device="cuda", **band):
+    import torch
+    import paper_2204_07143_b200 as na2d
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    t = {n: torch.from_numpy(np.ascontiguousarray(inp[n])).to(device=device, dtype=tdt) for n in ("q", "k", "v", "dout")}
+    rpb = None if inp["rpb"] is None else torch.from_numpy(np.ascontiguousarray(inp["rpb"])).to(device)
+    kw = {}
+    if band:
+        kw = dict(map_height=band.get("H", 0), q_row0=band.get("q_row0", 0), kv_row0=band.get("kv_row0", 0))
+    out, lse = na2d.forward(t["q"], t["k"], t["v"], rpb, L, scale, **kw)
+    res = dict(out=out, lse=lse)
+    if backward:
+        dq, dk, dv, drpb = na2d.backward(t["q"], t["k"], t["v"], rpb, out, lse, t["dout"], L, scale, **kw)
+        res.update(dq=dq, dk=dk, dv=dv, drpb=drpb)
+    torch.cuda.synchronize()
+    return {n: (None if x is None else x.float().cpu().numpy()) for n, x in res.items()}

@@ -1,0 +1,157 @@
+"""GPU parity (-m gpu): the CUDA path through the C ABI vs the fp64 oracle on the same seeded
+inputs, element by element, with the north-star tolerances (tests/parity.py).  Covers the
+BASELINE configs at full size (the launch configuration bench.py times), ragged tiles, L >= map
+size, single-pixel maps, no-RPB, row bands, both kernel families and RPB probes."""
+import os
+
+import numpy as np
+import pytest
+
+from na2d_inputs import CONFIGS, Shape, make_inputs
+from tests.parity import compare, run_cuda, run_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def cuda_lib():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2204_07143_b200 import build
+    build.build()
+
+
+def check(shape: Shape, dtype="bf16", rpb="parity", seed=None, backward=True, **band):
+    inp = make_inputs(shape, seed=seed, dtype=dtype, rpb=rpb)
+    scale = shape.d ** -0.5
+    ref = run_oracle(inp, shape.kernel_size, scale, backward=backward)
+    got = run_cuda(inp, shape.kernel_size, scale, dtype, backward=backward)
+    return compare(got, ref, dtype)
+
+
+SMALL = [
+    Shape("s8x8k3", 1, 1, 8, 8, 32, 3),          # BASELINE config 1
+    Shape("ragged13x29k7", 2, 2, 13, 29, 32, 7),  # ragged in both axes
+    Shape("ragged30x17k5", 1, 3, 30, 17, 32, 5),
+    Shape("k_gt_map5x5k7", 2, 1, 5, 5, 32, 7),   # window covers the map
+    Shape("k_gt_w9x4k7", 1, 2, 9, 4, 32, 7),     # L > W only
+    Shape("pixel1x1k3", 3, 2, 1, 1, 32, 3),      # single pixel: O = V
+    Shape("wide3x70k3", 1, 1, 3, 70, 32, 3),
+    Shape("sa7x7k7", 4, 4, 7, 7, 32, 7),         # NAT-Tiny stage-4 geometry (k = map: full SA)
+    Shape("tall61x9k7", 1, 1, 61, 9, 32, 7),
+]
+
+
+@pytest.mark.parametrize("shape", SMALL, ids=lambda s: s.name)
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_small_shapes(shape, dtype):
+    check(shape, dtype)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_no_rpb(dtype):
+    check(Shape("norpb", 2, 2, 19, 23, 32, 7), dtype, rpb=None)
+
+
+@pytest.mark.parametrize("d,L", [(16, 3), (64, 5), (128, 3), (32, 9), (32, 11), (8, 13)])
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_other_dims_and_kernel_sizes(d, L, dtype):
+    check(Shape(f"d{d}k{L}", 2, 2, 17, 21, d, L), dtype)
+
+
+@pytest.mark.parametrize("L", [3, 5, 7])
+def test_rpb_one_hot_probe(L):
+    """Q = 0, one large table cell: every query whose window holds that offset copies V there.
+    Pins bias sign/orientation incl. the corner cells (1 (query,key) pair per map)."""
+    import torch
+    import paper_2204_07143_b200 as na2d
+    H, W, d = 20, 37, 32
+    T = 2 * L - 1
+    g = np.random.default_rng(L)
+    from na2d_inputs import bf16_round
+    v = bf16_round(g.standard_normal((1, 1, H, W, d)).astype(np.float32))
+    k = bf16_round(g.standard_normal((1, 1, H, W, d)).astype(np.float32))
+    q = np.zeros_like(v)
+    tq, tk, tv = (torch.from_numpy(x).cuda().bfloat16() for x in (q, k, v))
+    for a, c in [(0, 0), (T - 1, T - 1), (0, T - 1), (T - 1, 0), (L - 1, L - 1), (1, L + 1)]:
+        rpb = np.zeros((1, T, T), np.float32)
+        rpb[0, a, c] = 2000.0
+        out, _ = na2d.forward(tq, tk, tv, torch.from_numpy(rpb).cuda(), L, 0.125)
+        out = out.float().cpu().numpy()
+        import oracle
+        ref, _ = oracle.na2d_forward(q, k, v, rpb, L, 0.125)
+        np.testing.assert_allclose(out, ref, atol=2e-2)
+        hits = 0
+        for i in range(H):
+            for j in range(W):
+                p, qq = i + a - (L - 1), j + c - (L - 1)
+                si, sj = oracle.window_start(i, H, L), oracle.window_start(j, W, L)
+                if si <= p < si + L and sj <= qq < sj + L:
+                    hits += 1
+                    np.testing.assert_allclose(out[0, 0, i, j], v[0, 0, p, qq], atol=1e-2)
+        assert hits >= 1
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_row_band(dtype):
+    """Band call (global coordinates) == oracle band call, incl. dk/dv partials."""
+    shape = Shape("band", 2, 2, 40, 27, 32, 7)
+    inp = make_inputs(shape, seed=77, dtype=dtype)
+    import oracle
+    for r0, r1 in [(0, 20), (20, 40), (13, 29)]:
+        k0 = oracle.window_start(r0, 40, 7)
+        k1 = oracle.window_start(r1 - 1, 40, 7) + 7
+        sub = dict(q=inp["q"][:, :, r0:r1], k=inp["k"][:, :, k0:k1], v=inp["v"][:, :, k0:k1],
+                   dout=inp["dout"][:, :, r0:r1], rpb=inp["rpb"])
+        ref = run_oracle(sub, 7, 32 ** -0.5, H=40, q_row0=r0, kv_row0=k0)
+        got = run_cuda(sub, 7, 32 ** -0.5, dtype, H=40, q_row0=r0, kv_row0=k0)
+        compare(got, ref, dtype)
+
+
+@pytest.mark.parametrize("name", list(CONFIGS), ids=str)
+def test_baseline_configs_full_size(name):
+    """Every BASELINE.json config at full size, fwd + bwd, all outputs element by element
+    (the oracle runs on all host cores)."""
+    rep = check(CONFIGS[name], "bf16")
+    print(name, {k: f"{e:.2e}/{t:.1e}" for k, (e, t) in rep.items()})
+
+
+def test_config1_fp32():
+    check(CONFIGS["cfg1_8x8_k3"], "f32")
+
+
+def test_kernel_family_and_launches():
+    import paper_2204_07143_b200 as na2d
+    s = CONFIGS["cfg2_nat_tiny_s1"]
+    p = na2d.make_problem(s.B, s.heads, s.H, s.W, s.d, s.kernel_size)
+    fam = (na2d.na2d_kernel_family(p, 0), na2d.na2d_kernel_family(p, 1))
+    print("cfg2 kernel families", fam)
+    assert na2d.na2d_launch_count(p, 0) >= 1 and na2d.na2d_launch_count(p, 1) >= 1
+
+
+def test_step_host_matches_device_path():
+    """The host-buffer end-to-end entry point gives the device path's results."""
+    import ctypes
+    import torch
+    import paper_2204_07143_b200 as na2d
+    s = Shape("host", 2, 2, 21, 18, 32, 7)
+    inp = make_inputs(s, seed=3)
+    ref = run_cuda(inp, 7, 32 ** -0.5, "bf16")
+    p = na2d.make_problem(s.B, s.heads, s.H, s.W, s.d, 7)
+    host = {n: torch.from_numpy(inp[n]).bfloat16().pin_memory() for n in ("q", "k", "v", "dout")}
+    rpb = torch.from_numpy(inp["rpb"]).pin_memory()
+    outs = {n: torch.empty_like(host["q"]).pin_memory() for n in ("out", "dq", "dk", "dv")}
+    lse = torch.empty(host["q"].shape[:4]).pin_memory()
+    drpb = torch.empty_like(rpb).pin_memory()
+    nbytes = na2d.na2d_step_host_workspace_bytes(p)
+    ws = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    na2d.na2d_step_host(p, host["q"].data_ptr(), host["k"].data_ptr(), host["v"].data_ptr(), rpb.data_ptr(),
+                        host["dout"].data_ptr(), outs["out"].data_ptr(), lse.data_ptr(), outs["dq"].data_ptr(),
+                        outs["dk"].data_ptr(), outs["dv"].data_ptr(), drpb.data_ptr(), ws.data_ptr(), nbytes, st)
+    torch.cuda.synchronize()
+    for n in ("out", "dq", "dk", "dv"):
+        np.testing.assert_array_equal(outs[n].float().numpy(), ref[n])
+    np.testing.assert_allclose(lse.numpy(), ref["lse"], atol=1e-6)
+    np.testing.assert_allclose(drpb.numpy(), ref["drpb"], atol=1e-3, rtol=1e-4)
