@@ -50,7 +50,6 @@ na2d_status make_geo(const na2d_problem *p, Geo *g) {
 
 size_t elem_size(const Geo &g) { return g.dtype == NA2D_F32 ? 4 : 2; }
 size_t n_query(const Geo &g) { return (size_t)g.B * g.heads * g.q_rows * g.W; }
-size_t n_key(const Geo &g) { return (size_t)g.B * g.heads * g.kv_rows * g.W; }
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 bool force_simt() {

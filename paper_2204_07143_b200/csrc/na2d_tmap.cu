@@ -1,0 +1,45 @@
+// na2d_tmap.cu -- see na2d_tmap.cuh.
+#include <cuda_runtime.h>
+
+#include <mutex>
+
+#include "na2d_tmap.cuh"
+
+namespace na2d {
+namespace {
+
+using EncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                              const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeFn)p;
+  });
+  return fn;
+}
+
+}  // namespace
+
+bool tmap_available() { return encode_fn() != nullptr; }
+
+bool make_tmap_bf16_4d(CUtensorMap *m, const void *base, int dim, int W, int rows, int outer, int box_w, int box_h) {
+  EncodeFn fn = encode_fn();
+  if (!fn || dim * 2 != 64) return false;
+  const cuuint64_t gdim[4] = {(cuuint64_t)dim, (cuuint64_t)W, (cuuint64_t)rows, (cuuint64_t)outer};
+  const cuuint64_t gstride[3] = {(cuuint64_t)dim * 2, (cuuint64_t)W * dim * 2, (cuuint64_t)rows * W * dim * 2};
+  const cuuint32_t box[4] = {(cuuint32_t)dim, (cuuint32_t)box_w, (cuuint32_t)box_h, 1};
+  const cuuint32_t estride[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(base), gdim, gstride, box, estride,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace na2d

@@ -1,0 +1,17 @@
+// na2d_tmap.cuh -- TMA tensor-map construction (cuTensorMapEncodeTiled through the runtime's
+// driver entry point, so libna2d needs no link-time libcuda).
+#pragma once
+
+#include <cuda.h>
+
+namespace na2d {
+
+// True if the driver exposes cuTensorMapEncodeTiled.
+bool tmap_available();
+
+// 4-D bf16 tensor [outer][rows][W][dim] (dim innermost, contiguous) with a box of
+// {dim, box_w, box_h, 1} elements and 64-byte swizzle (dim * 2 must be 64).  Out-of-bounds box
+// elements are zero-filled by the hardware.  Returns false on failure.
+bool make_tmap_bf16_4d(CUtensorMap *m, const void *base, int dim, int W, int rows, int outer, int box_w, int box_h);
+
+}  // namespace na2d
