@@ -1,22 +1,28 @@
 // na2d_fwd_tc.cu -- NA2D forward on 5th-generation tensor cores (tcgen05 + TMEM + TMA), sm_100a.
 //
-// Eq. 2 for bf16 Q/K/V, head dim 32, L in {3,5,7}:
-//   one CTA tile = 8 x 16 queries (M = 128 TMEM lanes).  Their neighbourhoods rho (P:150,
-//   P:163-164) all lie inside the halo rows [wstart(i0), +8+L-1) x cols [wstart(j0), +16+L-1)
-//   (global clamped coordinates), which TMA stages into shared memory (zero-filled outside the
-//   tensor).  The tile x halo products are dense contractions:
-//     S = Q K_halo^T      (M=128, N=halo, K=32)   tcgen05.mma SS -> TMEM columns [0, NS)
-//     O = P V_halo        (M=128, N=32, K=halo)   tcgen05.mma TS (P from TMEM) -> TMEM
-//   Between them four softmax warps (one TMEM lane quarter each, 32 queries = a 4 x 8 query
-//   block) read only their block's union of windows (<= (4+L-1) rows x 16 columns of S), add
-//   the relative positional bias B[h][p-i+L-1][q-j+L-1] from shared memory, mask the
-//   keys outside each query's own window, and compute the exact single-pass softmax (the whole
-//   window is in one tile, so no online rescaling): max, exp2, sum, P (bf16) -> TMEM.
-//   LSE (natural log) and O / sum are written by the same warps.
-// Warp roles (persistent CTAs, one per SM): warp 0 TMA producer (3-stage ring), warp 1 MMA
-// issuer, warps 2-5 softmax + epilogue.
+// Eq. 2 for bf16 Q/K/V, head dim 32, L in {3,5,7}.
+//
+// Tiling.  A CTA tile is 8 x 16 queries, split into two sub-tiles of 4 x 16 (rows 0-3, 4-7),
+// each a tcgen05 M=64 MMA whose accumulator rows land in TMEM lanes 0-15 (sub-tile 0) or 16-31
+// (sub-tile 1) of every 32-lane quarter.  All neighbourhoods rho of the tile
+// lie in the halo rows [wstart(i0), +8+L-1) x cols [wstart(j0), +24) (global clamped
+// coordinates, row pitch padded to 24), which TMA stages in shared memory (zero fill outside the
+// tensor).  Sub-tile s only needs the 4+L-1 halo rows starting at rb_s = wstart(i0+4s) -
+// wstart(i0), i.e. a contiguous, 512-byte aligned run of NSUB = (4+L-1)*24 keys:
+//     S_s = Q_s K[rb_s..]^T   (M=64, N=NSUB, K=32)   tcgen05.mma SS -> TMEM [0, NSUB)
+//     O_s = P_s V[rb_s..]     (M=64, N=32, K=NSUB)   tcgen05.mma TS (P from TMEM)
+// Softmax.  TMEM lane quarter q holds the 4 x 4 query block at tile columns [4q, 4q+4) of both
+// sub-tiles; the union of its windows is (4+L-1) rows x (4+L-1) columns of S (loaded as L+5
+// even-aligned columns).  Per element: x = s*scale*log2e + T[cell] where T is a shared-memory
+// table of the head's relative positional bias B[h][p-i+L-1][q-j+L-1] pre-multiplied by
+// scale*log2e, with -inf outside the query's own window (one table per column-clamp class, plus
+// an all -inf row for rows outside the window).  Exact single-pass softmax (the whole window
+// sits in one tile): pass 1 max (x written back in place), pass 2 P = exp2(x - max) packed to
+// bf16 into TMEM, aliased over S columns already consumed.  O lands in dead S columns.
+// Pipeline.  Persistent CTAs (one per SM), contiguous tile ranges.  Warp 0: TMA (3-stage ring);
+// warp 1: MMA issue, software-pipelined one tile ahead; warps 2-5 and 6-9: two softmax +
+// epilogue groups that ping-pong between two TMEM slots of 256 columns.
 #include <math.h>
-#include <stdio.h>
 
 #include <mutex>
 
@@ -31,33 +37,37 @@ namespace {
 
 using namespace sm100;
 
-constexpr int kTQH = 8, kTQW = 16, kM = 128, kD = 32;
+constexpr int kTQH = 8, kTQW = 16, kD = 32;
+constexpr int kHCP = 24;           // halo row pitch (keys)
 constexpr int kStages = 3;
-constexpr int kThreads = 192;  // 6 warps
+constexpr int kThreads = 320;      // 10 warps
 constexpr int kRowBytes = kD * 2;  // 64-byte rows (32 bf16)
+constexpr int kTblStride = 40;     // floats per table row (8 mod 32: conflict-free 4x4 blocks)
+constexpr int kTblOff = 8;         // column offset for negative bias columns
 
 template <int L>
 struct Cfg {
-  static constexpr int HR = kTQH + L - 1, HC = kTQW + L - 1;  // halo extent
-  static constexpr int NKEYS = HR * HC;
-  static constexpr int NS = (NKEYS + 31) / 32 * 32;          // padded key count (S columns)
-  static constexpr int UR = 4 + L - 1;                       // union rows per 4x8 query block
-  static constexpr int S_COL = 0, P_COL = NS, O_COL = NS + NS / 2;
-  static_assert(O_COL + kD <= 512, "TMEM budget");
-  static constexpr int N_HALF = NS > 256 ? NS / 2 : NS;      // MMA N per instruction (<= 256)
-  static constexpr int N_PARTS = NS / N_HALF;
-  static constexpr int Q_BYTES = kM * kRowBytes;             // 8 KB
-  static constexpr int KV_BYTES = NS * kRowBytes;            // padded tile
-  static constexpr int KV_TX = NKEYS * kRowBytes;            // bytes TMA delivers
+  static constexpr int HR = kTQH + L - 1;      // halo rows
+  static constexpr int UR = 4 + L - 1;         // union rows per sub-tile
+  static constexpr int NSUB = UR * kHCP;       // S columns per sub-tile (keys)
+  static constexpr int UCW = L + 5;            // union columns loaded (even)
+  static constexpr int P_COL = 0;              // P (bf16 pairs) aliased over consumed S
+  static constexpr int O_COL = NSUB / 2;       // O in dead S columns
+  static_assert(O_COL + kD <= 256, "slot budget");
+  static constexpr int KV_ROWS = HR * kHCP;
+  static constexpr int Q_BYTES = 128 * kRowBytes;
+  static constexpr int KV_BYTES = KV_ROWS * kRowBytes;
   static constexpr int STAGE_BYTES = Q_BYTES + 2 * KV_BYTES;
   static constexpr int TT = 2 * L - 1;
-  // >= 116 KB so that exactly one CTA (owning all 512 TMEM columns) is resident per SM
-  static constexpr int SMEM_NEED = kStages * STAGE_BYTES + 1024 /*align*/ + 4096 /*table+bars*/;
-  static constexpr int SMEM = SMEM_NEED > 120 * 1024 ? SMEM_NEED : 120 * 1024;
+  static constexpr int TROWS = TT + 1;                             // + all -inf row
+  static constexpr int TBL_FLOATS = L * TROWS * kTblStride;        // one table set (per group)
+  static constexpr int TBL_OFF = kStages * STAGE_BYTES;
+  static constexpr int BAR_OFF = TBL_OFF + 2 * TBL_FLOATS * 4;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;
 };
 
 struct FwdParams {
-  int B, heads, H, W, L, q_rows, q_row0, kv_rows, kv_row0;
+  int heads, H, W, q_rows, q_row0, kv_row0;
   int tiles_h, tiles_w, num_tiles;
   float scale_log2;  // scale * log2(e)
   const float *rpb;  // [heads][TT][TT] or null
@@ -65,41 +75,56 @@ struct FwdParams {
   float *lse;
 };
 
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+
+struct TileGeo {
+  int bh, i0, j0, hr0, hc0;
+};
+__device__ __forceinline__ TileGeo tile_geo(const FwdParams &p, int t, int L) {
+  TileGeo g;
+  const int per = p.tiles_h * p.tiles_w;
+  g.bh = t / per;
+  const int rem = t - g.bh * per;
+  g.i0 = p.q_row0 + (rem / p.tiles_w) * kTQH;
+  g.j0 = (rem % p.tiles_w) * kTQW;
+  g.hr0 = wstart(g.i0, p.H, L);
+  g.hc0 = wstart(g.j0, p.W, L);
+  return g;
+}
+
 template <int L>
 __global__ void __launch_bounds__(kThreads, 1)
     na2d_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                        const __grid_constant__ CUtensorMap tm_v, const FwdParams p) {
   using C = Cfg<L>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t *stage_base = smem;
-  float *s_table = (float *)(smem + kStages * C::STAGE_BYTES);                 // [TT*TT]
-  uint64_t *bars = (uint64_t *)(smem + kStages * C::STAGE_BYTES + 2048);
+  uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  float *tables = (float *)(smem + C::TBL_OFF);
+  uint64_t *bars = (uint64_t *)(smem + C::BAR_OFF);
   uint64_t *full = bars, *empty = bars + kStages;
-  uint64_t *s_full = bars + 2 * kStages, *p_full = s_full + 1, *o_full = s_full + 2, *tmem_free = s_full + 3;
-  uint32_t *tmem_slot = (uint32_t *)(bars + 2 * kStages + 4);
+  uint64_t *s_full = bars + 2 * kStages, *p_full = s_full + 2, *o_full = s_full + 4, *tmem_free = s_full + 6;
+  uint32_t *tmem_slot = (uint32_t *)(bars + 2 * kStages + 8);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int t_begin = (int)((long)p.num_tiles * blockIdx.x / gridDim.x);
+  const int t_end = (int)((long)p.num_tiles * (blockIdx.x + 1) / gridDim.x);
+  const int q_end = p.q_row0 + p.q_rows;
 
-  // zero the padded key rows of every K/V stage once (TMA never writes them; V pad rows are
-  // multiplied by P = 0 and must not hold NaN/Inf garbage)
-  for (int s = 0; s < kStages; ++s) {
-    uint8_t *kt = stage_base + s * C::STAGE_BYTES + C::Q_BYTES;
-    for (int off = C::KV_TX + threadIdx.x * 16; off < C::KV_BYTES; off += kThreads * 16) {
-      *(uint4 *)(kt + off) = make_uint4(0, 0, 0, 0);
-      *(uint4 *)(kt + C::KV_BYTES + off) = make_uint4(0, 0, 0, 0);
-    }
-  }
-  fence_proxy_async_smem();
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(s_full, 1);
-    mbar_init(p_full, 4);
-    mbar_init(o_full, 1);
-    mbar_init(tmem_free, 4);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&p_full[s], 4);
+      mbar_init(&o_full[s], 1);
+      mbar_init(&tmem_free[s], 4);
+    }
     fence_barrier_init();
     tma_prefetch(&tm_q);
     tma_prefetch(&tm_k);
@@ -111,164 +136,236 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const int tiles_per_map = p.tiles_h * p.tiles_w;
-
   if (warp == 0) {
     // ================= TMA producer
     if (elect_one()) {
       int it = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+      for (int t = t_begin; t < t_end; ++t, ++it) {
         const int s = it % kStages;
         mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
-        const int bh = t / tiles_per_map, rem = t % tiles_per_map;
-        const int i0 = p.q_row0 + (rem / p.tiles_w) * kTQH, j0 = (rem % p.tiles_w) * kTQW;
-        const int hr0 = wstart(i0, p.H, L), hc0 = wstart(j0, p.W, L);
-        uint8_t *st = stage_base + s * C::STAGE_BYTES;
-        mbar_expect_tx(&full[s], C::Q_BYTES + 2 * C::KV_TX);
-        // Q as four 4x8 query blocks (TMEM lane quarter b <- block b)
+        const TileGeo g = tile_geo(p, t, L);
+        uint8_t *st = smem + s * C::STAGE_BYTES;
+        mbar_expect_tx(&full[s], C::STAGE_BYTES);
+        // Q: sub-tile sb, quarter qb -> 16 rows = 4x4 block (rows i0+4sb.., cols j0+4qb..)
 #pragma unroll
-        for (int b = 0; b < 4; ++b)
-          tma_load_4d(st + b * 32 * kRowBytes, &tm_q, &full[s], 0, j0 + 8 * (b & 1), i0 - p.q_row0 + 4 * (b >> 1), bh);
-        tma_load_4d(st + C::Q_BYTES, &tm_k, &full[s], 0, hc0, hr0 - p.kv_row0, bh);
-        tma_load_4d(st + C::Q_BYTES + C::KV_BYTES, &tm_v, &full[s], 0, hc0, hr0 - p.kv_row0, bh);
+        for (int sb = 0; sb < 2; ++sb)
+#pragma unroll
+          for (int qb = 0; qb < 4; ++qb)
+            tma_load_4d(st + (64 * sb + 16 * qb) * kRowBytes, &tm_q, &full[s], 0, g.j0 + 4 * qb,
+                        g.i0 - p.q_row0 + 4 * sb, g.bh);
+        tma_load_4d(st + C::Q_BYTES, &tm_k, &full[s], 0, g.hc0, g.hr0 - p.kv_row0, g.bh);
+        tma_load_4d(st + C::Q_BYTES + C::KV_BYTES, &tm_v, &full[s], 0, g.hc0, g.hr0 - p.kv_row0, g.bh);
       }
     }
   } else if (warp == 1) {
-    // ================= MMA issuer
-    constexpr uint32_t idesc_qk = idesc_bf16(kM, C::N_HALF, false);
-    constexpr uint32_t idesc_pv = idesc_bf16(kM, kD, true);
-    int it = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
-      const int s = it % kStages;
-      const uint32_t ph = it & 1;
-      mbar_wait(&full[s], (it / kStages) & 1);
-      mbar_wait(tmem_free, ph ^ 1);
-      tc_fence_after();
-      const uint32_t q_addr = smem_u32(stage_base + s * C::STAGE_BYTES);
-      const uint32_t k_addr = q_addr + C::Q_BYTES;
-      const uint32_t v_addr = k_addr + C::KV_BYTES;
-      if (elect_one()) {
+    // ================= MMA issuer (QK of tile it, then PV of tile it-1)
+    constexpr uint32_t idesc_qk = idesc_bf16(64, C::NSUB, false);
+    constexpr uint32_t idesc_pv = idesc_bf16(64, kD, true);
+    const int n = t_end - t_begin;
+    for (int it = 0; it <= n; ++it) {
+      if (it < n) {
+        const int s = it % kStages, slot = it & 1;
+        const TileGeo g = tile_geo(p, t_begin + it, L);
+        mbar_wait(&full[s], (it / kStages) & 1);
+        mbar_wait(&tmem_free[slot], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t q_addr = smem_u32(smem + s * C::STAGE_BYTES);
+        const uint32_t k_addr = q_addr + C::Q_BYTES;
+        if (elect_one()) {
 #pragma unroll
-        for (int n = 0; n < C::N_PARTS; ++n)
+          for (int sb = 0; sb < 2; ++sb) {
+            const int rb = wstart(min(g.i0 + 4 * sb, q_end - 1), p.H, L) - g.hr0;
 #pragma unroll
-          for (int k = 0; k < kD / 16; ++k)
-            mma_ss(tmem + C::S_COL + n * C::N_HALF, sdesc_sw64(q_addr + k * 32),
-                   sdesc_sw64(k_addr + n * C::N_HALF * kRowBytes + k * 32), idesc_qk, k);
-        mma_commit(s_full);
+            for (int k = 0; k < kD / 16; ++k)
+              mma_ss(tmem + ((uint32_t)(16 * sb) << 16) + slot * 256, sdesc_sw64(q_addr + sb * 4096 + k * 32),
+                     sdesc_sw64(k_addr + rb * kHCP * kRowBytes + k * 32), idesc_qk, k);
+          }
+          mma_commit(&s_full[slot]);
+        }
+        __syncwarp();
       }
-      __syncwarp();
-      mbar_wait(p_full, ph);
-      tc_fence_after();
-      if (elect_one()) {
-#pragma unroll 4
-        for (int ks = 0; ks < C::NS / 16; ++ks)
-          mma_ts(tmem + C::O_COL, tmem + C::P_COL + ks * 8, sdesc_sw64(v_addr + ks * 16 * kRowBytes), idesc_pv,
-                 ks);
-        mma_commit(o_full);
-        mma_commit(&empty[s]);
+      if (it > 0) {
+        const int pi = it - 1, s = pi % kStages, slot = pi & 1;
+        const TileGeo g = tile_geo(p, t_begin + pi, L);
+        mbar_wait(&p_full[slot], (pi >> 1) & 1);
+        tc_fence_after();
+        const uint32_t v_addr = smem_u32(smem + s * C::STAGE_BYTES) + C::Q_BYTES + C::KV_BYTES;
+        if (elect_one()) {
+#pragma unroll
+          for (int sb = 0; sb < 2; ++sb) {
+            const int rb = wstart(min(g.i0 + 4 * sb, q_end - 1), p.H, L) - g.hr0;
+            const uint32_t base = tmem + ((uint32_t)(16 * sb) << 16) + slot * 256;
+#pragma unroll 5
+            for (int ks = 0; ks < C::NSUB / 16; ++ks)
+              mma_ts(base + C::O_COL, base + C::P_COL + ks * 8,
+                     sdesc_sw64(v_addr + rb * kHCP * kRowBytes + ks * 16 * kRowBytes), idesc_pv, ks);
+          }
+          mma_commit(&o_full[slot]);
+          mma_commit(&empty[s]);
+        }
+        __syncwarp();
       }
-      __syncwarp();
     }
   } else {
-    // ================= softmax + epilogue (warps 2..5 -> TMEM lane quarters 2,3,0,1)
+    // ================= softmax + epilogue groups
+    const int grp = (warp - 2) >> 2;  // 0: warps 2-5, 1: warps 6-9
     const int quarter = warp & 3;
-    const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
-    const int TT = C::TT;
+    const int half = lane >> 4, r = (lane >> 2) & 3, c = lane & 3;
+    float *tbl = tables + grp * C::TBL_FLOATS;
+    const uint32_t tbl_s = smem_u32(tbl);
+    const int gtid = threadIdx.x - 64 - grp * 128;  // 0..127 within the group
     const int Lh = wlen(p.H, L), Lw = wlen(p.W, L);
-    const int q_end = p.q_row0 + p.q_rows;
     int cur_head = -1;
-    int it = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
-      const uint32_t ph = it & 1;
-      const int bh = t / tiles_per_map, rem = t % tiles_per_map;
-      const int h = bh % p.heads;
-      const int i0 = p.q_row0 + (rem / p.tiles_w) * kTQH, j0 = (rem % p.tiles_w) * kTQW;
-      const int hr0 = wstart(i0, p.H, L), hc0 = wstart(j0, p.W, L);
-      // this thread's query (block `quarter` = rows 4*(quarter>>1).., cols 8*(quarter&1)..)
-      const int bi0 = i0 + 4 * (quarter >> 1), bj0 = j0 + 8 * (quarter & 1);
-      const int i = bi0 + (lane >> 3), j = bj0 + (lane & 7);
-      const int ic = min(i, q_end - 1), jc = min(j, p.W - 1);
-      const int ur0 = wstart(min(bi0, q_end - 1), p.H, L) - hr0;
-      const int uc0 = (wstart(min(bj0, p.W - 1), p.W, L) - hc0) & ~1;
-      const int wr = wstart(ic, p.H, L) - hr0 - ur0;  // window origin inside the union
-      const int wc = wstart(jc, p.W, L) - hc0 - uc0;
-      // bias cell of union element (u, c): (hr0+ur0+u - ic + L-1, hc0+uc0+c - jc + L-1)
-      const int brow0 = hr0 + ur0 - ic + L - 1, bcol0 = hc0 + uc0 - jc + L - 1;
-      if (p.rpb && h != cur_head) {  // stage this head's bias table (tile-uniform branch)
-        named_bar_sync(1, 128);
-        for (int c = threadIdx.x - 64; c < TT * TT; c += 128) s_table[c] = __ldg(&p.rpb[h * TT * TT + c]);
-        named_bar_sync(1, 128);
+    for (int it = grp; it < t_end - t_begin; it += 2) {
+      const int slot = it & 1;
+      const uint32_t ph = (it >> 1) & 1;
+      const TileGeo g = tile_geo(p, t_begin + it, L);
+      const int h = g.bh % p.heads;
+      if (h != cur_head) {  // (re)build this group's masked, pre-scaled bias tables
+        named_bar_sync(1 + grp, 128);
+        for (int e = gtid; e < C::TBL_FLOATS; e += 128) {
+          const int dc = e / (C::TROWS * kTblStride);                 // column-clamp class
+          const int rr = (e / kTblStride) % C::TROWS;                 // bias row (TT = all -inf)
+          const int cb = e % kTblStride - kTblOff;                    // bias column
+          float v = -INFINITY;
+          if (rr < C::TT && cb >= dc && cb < dc + Lw)
+            v = p.rpb ? __ldg(&p.rpb[(h * C::TT + rr) * C::TT + cb]) * p.scale_log2 : 0.f;
+          tbl[e] = v;
+        }
+        named_bar_sync(1 + grp, 128);
         cur_head = h;
       }
-      mbar_wait(s_full, ph);
+      // this thread's query and window geometry
+      const int i = g.i0 + 4 * half + r, j = g.j0 + 4 * quarter + c;
+      const int ic = min(i, q_end - 1), jc = min(j, p.W - 1);
+      const int si = wstart(ic, p.H, L), sj = wstart(jc, p.W, L);
+      const int rb = wstart(min(g.i0 + 4 * half, q_end - 1), p.H, L) - g.hr0;
+      const int uc = (wstart(min(g.j0 + 4 * quarter, p.W - 1), p.W, L) - g.hc0) & ~1;  // warp-uniform
+      const int dc = sj - jc + L - 1;                                // column-clamp class
+      const int bcol0 = g.hc0 + uc - jc + L - 1;                     // bias column of union col 0
+      const uint32_t tcls = tbl_s + (uint32_t)(dc * C::TROWS * kTblStride + kTblOff + bcol0) * 4u;
+      const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16) + slot * 256;
+
+      mbar_wait(&s_full[slot], ph);
       tc_fence_after();
-      // ---- pass 1: row max over the thread's window (log2 domain)
+      // ---- pass 1: x = s*scale*log2e + T (masked); running max; x written back in place
       float mx = -INFINITY;
-      for (int u = 0; u < C::UR; ++u) {
-        uint32_t r[16];
-        tmem_ld16(lane_addr + C::S_COL + (ur0 + u) * C::HC + uc0, r);
-        tc_wait_ld();
-        const bool rv = (unsigned)(u - wr) < (unsigned)Lh;
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          const bool v = rv && (unsigned)(c - wc) < (unsigned)Lw;
-          float b = 0.f;
-          if (p.rpb && v) b = s_table[(brow0 + u) * TT + bcol0 + c];
-          const float x = (__uint_as_float(r[c]) + b) * p.scale_log2;
-          mx = v ? fmaxf(mx, x) : mx;
+      for (int u = 0; u < C::UR; ++u) {
+        const int col = u * kHCP + uc;
+        uint32_t v[C::UCW];
+        {
+          uint32_t a8[8];
+          tmem_ld8(lane_addr + col, a8);
+#pragma unroll
+          for (int z = 0; z < 8; ++z) v[z] = a8[z];
+          if constexpr (C::UCW - 8 == 4) {
+            uint32_t a4[4];
+            tmem_ld4(lane_addr + col + 8, a4);
+#pragma unroll
+            for (int z = 0; z < 4; ++z) v[8 + z] = a4[z];
+          } else if constexpr (C::UCW - 8 == 2) {
+            uint32_t a2[2];
+            tmem_ld2(lane_addr + col + 8, a2);
+            v[8] = a2[0];
+            v[9] = a2[1];
+          }
+        }
+        const int pr = g.hr0 + rb + u;  // key row
+        const bool rv = (unsigned)(pr - si) < (unsigned)Lh;
+        const uint32_t trow = tcls + (uint32_t)((rv ? pr - ic + L - 1 : C::TT) * kTblStride) * 4u;
+        tc_wait_ld();
+#pragma unroll
+        for (int z = 0; z < C::UCW; ++z) {
+          const float x = fmaf(__uint_as_float(v[z]), p.scale_log2, lds_f32(trow + 4 * z));
+          mx = fmaxf(mx, x);
+          v[z] = __float_as_uint(x);
+        }
+        {
+          uint32_t a8[8];
+#pragma unroll
+          for (int z = 0; z < 8; ++z) a8[z] = v[z];
+          tmem_st8(lane_addr + col, a8);
+          if constexpr (C::UCW - 8 == 4) {
+            uint32_t a4[4] = {v[8], v[9], v[10], v[11]};
+            tmem_st4(lane_addr + col + 8, a4);
+          } else if constexpr (C::UCW - 8 == 2) {
+            uint32_t a2[2] = {v[8], v[9]};
+            tmem_st2(lane_addr + col + 8, a2);
+          }
         }
       }
-      // ---- zero this lane's P row, then pass 2: P = exp2(x - max) on the window, sum
-#pragma unroll
-      for (int c = 0; c < C::NS / 2; c += 32) tmem_st32_zero(lane_addr + C::P_COL + c);
       tc_wait_st();
+      // ---- pass 2: P = exp2(x - max) (bf16 pairs over consumed S columns), row sums
       float sum = 0.f;
+      const int zb = uc >> 1, za = C::UCW / 2;  // packed columns before / in the union span
+#pragma unroll
       for (int u = 0; u < C::UR; ++u) {
-        uint32_t r[16];
-        const int col = (ur0 + u) * C::HC + uc0;
-        tmem_ld16(lane_addr + C::S_COL + col, r);
-        tc_wait_ld();
-        const bool rv = (unsigned)(u - wr) < (unsigned)Lh;
-        uint32_t pk[8];
+        const int col = u * kHCP + uc;
+        uint32_t v[C::UCW];
+        {
+          uint32_t a8[8];
+          tmem_ld8(lane_addr + col, a8);
 #pragma unroll
-        for (int c = 0; c < 16; c += 2) {
-          float e[2];
+          for (int z = 0; z < 8; ++z) v[z] = a8[z];
+          if constexpr (C::UCW - 8 == 4) {
+            uint32_t a4[4];
+            tmem_ld4(lane_addr + col + 8, a4);
 #pragma unroll
-          for (int z = 0; z < 2; ++z) {
-            const bool v = rv && (unsigned)(c + z - wc) < (unsigned)Lw;
-            float b = 0.f;
-            if (p.rpb && v) b = s_table[(brow0 + u) * TT + bcol0 + c + z];
-            const float x = (__uint_as_float(r[c + z]) + b) * p.scale_log2;
-            e[z] = v ? ex2(x - mx) : 0.f;
-            sum += e[z];
+            for (int z = 0; z < 4; ++z) v[8 + z] = a4[z];
+          } else if constexpr (C::UCW - 8 == 2) {
+            uint32_t a2[2];
+            tmem_ld2(lane_addr + col + 8, a2);
+            v[8] = a2[0];
+            v[9] = a2[1];
           }
-          pk[c / 2] = pack_bf16(e[0], e[1]);
         }
-        tmem_st8(lane_addr + C::P_COL + col / 2, pk);
+        tc_wait_ld();
+        uint32_t pk[C::UCW / 2];
+#pragma unroll
+        for (int z = 0; z < C::UCW; z += 2) {
+          const float e0 = ex2(__uint_as_float(v[z]) - mx);
+          const float e1 = ex2(__uint_as_float(v[z + 1]) - mx);
+          sum += e0 + e1;
+          pk[z / 2] = pack_bf16(e0, e1);
+        }
+        const uint32_t prow = lane_addr + C::P_COL + u * (kHCP / 2);
+        for (int z = 0; z < zb; ++z) tmem_st1(prow + z, 0u);
+        {
+          uint32_t a4[4] = {pk[0], pk[1], pk[2], pk[3]};
+          tmem_st4(prow + zb, a4);
+          if constexpr (C::UCW / 2 - 4 == 2) {
+            uint32_t a2[2] = {pk[4], pk[5]};
+            tmem_st2(prow + zb + 4, a2);
+          } else if constexpr (C::UCW / 2 - 4 == 1) {
+            tmem_st1(prow + zb + 4, pk[4]);
+          }
+        }
+        for (int z = zb + za; z < kHCP / 2; ++z) tmem_st1(prow + z, 0u);
       }
       tc_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
+      if (lane == 0) mbar_arrive(&p_full[slot]);
       // ---- epilogue: O / sum -> bf16, LSE
-      mbar_wait(o_full, ph);
+      mbar_wait(&o_full[slot], ph);
       tc_fence_after();
       uint32_t o[32];
       tmem_ld32(lane_addr + C::O_COL, o);
       tc_wait_ld();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tmem_free);
+      if (lane == 0) mbar_arrive(&tmem_free[slot]);
       if (i < q_end && j < p.W) {
         const float inv = 1.f / sum;
-        const size_t qi = ((size_t)bh * p.q_rows + (i - p.q_row0)) * p.W + j;
+        const size_t qi = ((size_t)g.bh * p.q_rows + (i - p.q_row0)) * p.W + j;
         uint4 *dst = (uint4 *)(p.out + qi * kD);
 #pragma unroll
-        for (int c = 0; c < kD; c += 8)
-          dst[c / 8] = make_uint4(pack_bf16(__uint_as_float(o[c]) * inv, __uint_as_float(o[c + 1]) * inv),
-                                  pack_bf16(__uint_as_float(o[c + 2]) * inv, __uint_as_float(o[c + 3]) * inv),
-                                  pack_bf16(__uint_as_float(o[c + 4]) * inv, __uint_as_float(o[c + 5]) * inv),
-                                  pack_bf16(__uint_as_float(o[c + 6]) * inv, __uint_as_float(o[c + 7]) * inv));
+        for (int z = 0; z < kD; z += 8)
+          dst[z / 8] = make_uint4(pack_bf16(__uint_as_float(o[z]) * inv, __uint_as_float(o[z + 1]) * inv),
+                                  pack_bf16(__uint_as_float(o[z + 2]) * inv, __uint_as_float(o[z + 3]) * inv),
+                                  pack_bf16(__uint_as_float(o[z + 4]) * inv, __uint_as_float(o[z + 5]) * inv),
+                                  pack_bf16(__uint_as_float(o[z + 6]) * inv, __uint_as_float(o[z + 7]) * inv));
         if (p.lse) p.lse[qi] = (mx + __log2f(sum)) * 0.69314718055994531f;
       }
     }
@@ -304,19 +401,16 @@ cudaError_t launch_fwd(const Geo &g, const void *q, const void *k, const void *v
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap tq, tk, tv;
   const int BH = g.B * g.heads;
-  if (!make_tmap_bf16_4d(&tq, q, kD, g.W, g.q_rows, BH, 8, 4) ||
-      !make_tmap_bf16_4d(&tk, k, kD, g.W, g.kv_rows, BH, C::HC, C::HR) ||
-      !make_tmap_bf16_4d(&tv, v, kD, g.W, g.kv_rows, BH, C::HC, C::HR))
+  if (!make_tmap_bf16_4d(&tq, q, kD, g.W, g.q_rows, BH, 4, 4) ||
+      !make_tmap_bf16_4d(&tk, k, kD, g.W, g.kv_rows, BH, kHCP, C::HR) ||
+      !make_tmap_bf16_4d(&tv, v, kD, g.W, g.kv_rows, BH, kHCP, C::HR))
     return cudaErrorInvalidValue;
   FwdParams p;
-  p.B = g.B;
   p.heads = g.heads;
   p.H = g.H;
   p.W = g.W;
-  p.L = L;
   p.q_rows = g.q_rows;
   p.q_row0 = g.q_row0;
-  p.kv_rows = g.kv_rows;
   p.kv_row0 = g.kv_row0;
   p.tiles_h = (g.q_rows + kTQH - 1) / kTQH;
   p.tiles_w = (g.W + kTQW - 1) / kTQW;
