@@ -127,6 +127,10 @@ int na2d_launch_count(const na2d_problem *p, int which);
  * "simt"); NULL if the problem is invalid. */
 const char *na2d_kernel_family(const na2d_problem *p, int which);
 
+/* Text of the CUDA error behind the most recent NA2D_ERR_CUDA returned on this host thread
+ * ("no error" if none).  Static/thread-local storage; valid until the next call. */
+const char *na2d_last_cuda_error(void);
+
 /* Per-kernel timing for benchmarks.  na2d_profile_enable(1) clears the record and makes every
  * subsequent launch bracket itself with CUDA events recorded on its own stream (the stream the
  * kernel is launched on); na2d_profile_enable(0) stops recording.  na2d_profile_read
@@ -136,6 +140,10 @@ const char *na2d_kernel_family(const na2d_problem *p, int which);
  * Not thread-safe with concurrent launches from other host threads. */
 na2d_status na2d_profile_enable(int on);
 int na2d_profile_read(char *names_out, size_t name_cap, float *total_ms, int *counts, int max_entries);
+
+/* Development aid: device buffer of >= 4*32*16 int64 that the tensor-core kernels fill with
+ * clock64() timestamps of their pipeline events (first 32 tiles of CTAs 0-3); NULL disables. */
+na2d_status na2d_debug_set_trace(void *device_buffer);
 
 #ifdef __cplusplus
 }

@@ -28,7 +28,10 @@ _STATUS = ["ok", "null pointer", "kernel size", "shape", "dtype", "unsupported",
 class NA2DError(RuntimeError):
     def __init__(self, status: int, what: str):
         self.status = status
-        super().__init__(f"{what}: status {status} ({na2d_status_string(status)})")
+        msg = f"{what}: status {status} ({na2d_status_string(status)})"
+        if status == 9:
+            msg += ": " + load_library().na2d_last_cuda_error().decode()
+        super().__init__(msg)
 
 
 class na2d_problem(ctypes.Structure):
@@ -40,7 +43,8 @@ class na2d_problem(ctypes.Structure):
 
 EXPORTS = ("na2d_status_string", "na2d_version", "na2d_forward", "na2d_backward_workspace_bytes",
            "na2d_backward", "na2d_step_host_workspace_bytes", "na2d_step_host", "na2d_launch_count",
-           "na2d_kernel_family", "na2d_profile_enable", "na2d_profile_read")
+           "na2d_kernel_family", "na2d_profile_enable", "na2d_profile_read", "na2d_last_cuda_error",
+           "na2d_debug_set_trace")
 
 _lib = None
 
@@ -72,6 +76,9 @@ def load_library():
     lib.na2d_launch_count.restype = ctypes.c_int
     lib.na2d_kernel_family.argtypes = [P, ctypes.c_int]
     lib.na2d_kernel_family.restype = ctypes.c_char_p
+    lib.na2d_last_cuda_error.restype = ctypes.c_char_p
+    lib.na2d_debug_set_trace.argtypes = [ctypes.c_void_p]
+    lib.na2d_debug_set_trace.restype = ctypes.c_int
     lib.na2d_profile_enable.argtypes = [ctypes.c_int]
     lib.na2d_profile_enable.restype = ctypes.c_int
     lib.na2d_profile_read.argtypes = [ctypes.c_char_p, SZ, ctypes.POINTER(ctypes.c_float),

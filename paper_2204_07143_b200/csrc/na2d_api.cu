@@ -73,7 +73,13 @@ size_t bwd_ws(const Geo &g) {
   return b;
 }
 
-na2d_status cuda_status(cudaError_t e) { return e == cudaSuccess ? NA2D_OK : NA2D_ERR_CUDA; }
+thread_local cudaError_t t_last_cuda_error = cudaSuccess;
+
+na2d_status cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return NA2D_OK;
+  t_last_cuda_error = e;
+  return NA2D_ERR_CUDA;
+}
 
 }  // namespace
 }  // namespace na2d
@@ -99,6 +105,8 @@ const char *na2d_status_string(na2d_status s) {
 }
 
 int na2d_version(void) { return NA2D_VERSION; }
+
+const char *na2d_last_cuda_error(void) { return cudaGetErrorString(t_last_cuda_error); }
 
 na2d_status na2d_forward(const na2d_problem *p, const void *q, const void *k, const void *v, const float *rpb,
                          void *out, float *lse, void *stream) {
@@ -180,7 +188,7 @@ na2d_status na2d_step_host(const na2d_problem *p, const void *q, const void *k, 
 #define NA2D_TRY(x)                  \
   do {                               \
     e = (x);                         \
-    if (e != cudaSuccess) return NA2D_ERR_CUDA; \
+    if (e != cudaSuccess) return cuda_status(e); \
   } while (0)
   NA2D_TRY(cudaMemcpyAsync(q_, q, bytes, cudaMemcpyHostToDevice, st));
   NA2D_TRY(cudaMemcpyAsync(k_, k, bytes, cudaMemcpyHostToDevice, st));

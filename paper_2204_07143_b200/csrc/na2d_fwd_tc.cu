@@ -44,6 +44,7 @@ constexpr int kThreads = 320;      // 10 warps
 constexpr int kRowBytes = kD * 2;  // 64-byte rows (32 bf16)
 constexpr int kTblStride = 40;     // floats per table row (8 mod 32: conflict-free 4x4 blocks)
 constexpr int kTblOff = 8;         // column offset for negative bias columns
+constexpr int kOAcc = 3;           // independent PV accumulators (summed in the epilogue)
 
 template <int L>
 struct Cfg {
@@ -52,8 +53,8 @@ struct Cfg {
   static constexpr int NSUB = UR * kHCP;       // S columns per sub-tile (keys)
   static constexpr int UCW = L + 5;            // union columns loaded (even)
   static constexpr int P_COL = 0;              // P (bf16 pairs) aliased over consumed S
-  static constexpr int O_COL = NSUB / 2;       // O in dead S columns
-  static_assert(O_COL + kD <= 256, "slot budget");
+  static constexpr int O_COL = NSUB / 2;       // O partial accumulators in dead S columns
+  static_assert(O_COL + kOAcc * kD <= 256, "slot budget");
   static constexpr int KV_ROWS = HR * kHCP;
   static constexpr int Q_BYTES = 128 * kRowBytes;
   static constexpr int KV_BYTES = KV_ROWS * kRowBytes;
@@ -73,12 +74,116 @@ struct FwdParams {
   const float *rpb;  // [heads][TT][TT] or null
   __nv_bfloat16 *out;
   float *lse;
+  long long *trace;  // debug timeline (na2d_debug_set_trace) or null
 };
 
-__device__ __forceinline__ float lds_f32(uint32_t a) {
-  float v;
-  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
-  return v;
+// Debug timeline: trace[(cta * kTraceTiles + it) * kTraceEv + ev] = clock64() for CTAs < 4.
+constexpr int kTraceTiles = 32, kTraceEv = 16;
+__device__ __forceinline__ void trace_ev(const FwdParams &p, int it, int ev) {
+  if (p.trace && blockIdx.x < 4 && it < kTraceTiles)
+    p.trace[((size_t)blockIdx.x * kTraceTiles + it) * kTraceEv + ev] = clock64();
+}
+
+// N consecutive TMEM columns of this warp's 32 lanes -> registers (N in {4,5,6,8,10,12})
+template <int N>
+__device__ __forceinline__ void ld_row(uint32_t addr, uint32_t (&v)[N]) {
+  uint32_t a8[8];
+  if constexpr (N >= 8) {
+    tmem_ld8(addr, a8);
+#pragma unroll
+    for (int z = 0; z < 8; ++z) v[z] = a8[z];
+  }
+  constexpr int R = N >= 8 ? N - 8 : N;
+  constexpr int B = N >= 8 ? 8 : 0;
+  if constexpr (R == 4) {
+    uint32_t a4[4];
+    tmem_ld4(addr + B, a4);
+#pragma unroll
+    for (int z = 0; z < 4; ++z) v[B + z] = a4[z];
+  } else if constexpr (R == 2) {
+    uint32_t a2[2];
+    tmem_ld2(addr + B, a2);
+    v[B] = a2[0];
+    v[B + 1] = a2[1];
+  } else {
+    static_assert(R == 0, "row width");
+  }
+}
+template <int N>
+__device__ __forceinline__ void st_row(uint32_t addr, const uint32_t (&v)[N]) {
+  if constexpr (N >= 8) {
+    uint32_t a8[8];
+#pragma unroll
+    for (int z = 0; z < 8; ++z) a8[z] = v[z];
+    tmem_st8(addr, a8);
+  }
+  constexpr int B = N >= 8 ? 8 : 0;
+  constexpr int R = N - B;
+  if constexpr (R >= 4) {
+    uint32_t a4[4] = {v[B], v[B + 1], v[B + 2], v[B + 3]};
+    tmem_st4(addr + B, a4);
+  }
+  constexpr int B2 = B + (R >= 4 ? 4 : 0);
+  constexpr int R2 = N - B2;
+  if constexpr (R2 >= 2) {
+    uint32_t a2[2] = {v[B2], v[B2 + 1]};
+    tmem_st2(addr + B2, a2);
+  }
+  if constexpr ((R2 & 1) == 1) tmem_st1(addr + N - 1, v[N - 1]);
+}
+__device__ __forceinline__ void st_zero12(uint32_t addr) {
+  const uint32_t z8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const uint32_t z4[4] = {0, 0, 0, 0};
+  tmem_st8(addr, z8);
+  tmem_st4(addr + 8, z4);
+}
+// One halo row of P (kHCP/2 = 12 packed bf16 pairs): pk placed at packed column zb (warp-uniform,
+// 0 <= zb <= 12 - N), zeros elsewhere; two stores (x8 + x4) with a static register layout.
+template <int N, int ZB>
+__device__ __forceinline__ void st_prow_fixed(uint32_t addr, const uint32_t (&pk)[N]) {
+  uint32_t r[12];
+#pragma unroll
+  for (int z = 0; z < 12; ++z) r[z] = (z >= ZB && z < ZB + N) ? pk[(z - ZB) < N ? (z - ZB) : 0] : 0u;
+  uint32_t a8[8] = {r[0], r[1], r[2], r[3], r[4], r[5], r[6], r[7]};
+  uint32_t a4[4] = {r[8], r[9], r[10], r[11]};
+  tmem_st8(addr, a8);
+  tmem_st4(addr + 8, a4);
+}
+template <int N>
+__device__ __forceinline__ void st_prow(uint32_t addr, const uint32_t (&pk)[N], int zb) {
+  switch (zb) {
+    case 0: st_prow_fixed<N, 0>(addr, pk); break;
+    case 1: if constexpr (N <= 11) st_prow_fixed<N, 1>(addr, pk); break;
+    case 2: if constexpr (N <= 10) st_prow_fixed<N, 2>(addr, pk); break;
+    case 3: if constexpr (N <= 9) st_prow_fixed<N, 3>(addr, pk); break;
+    case 4: if constexpr (N <= 8) st_prow_fixed<N, 4>(addr, pk); break;
+    case 5: if constexpr (N <= 7) st_prow_fixed<N, 5>(addr, pk); break;
+    case 6: if constexpr (N <= 6) st_prow_fixed<N, 6>(addr, pk); break;
+    case 7: if constexpr (N <= 5) st_prow_fixed<N, 7>(addr, pk); break;
+    case 8: if constexpr (N <= 4) st_prow_fixed<N, 8>(addr, pk); break;
+  }
+}
+template <int N>
+__device__ __forceinline__ float tree_max(const float (&x)[N]) {
+  float m[N];
+#pragma unroll
+  for (int z = 0; z < N; ++z) m[z] = x[z];
+#pragma unroll
+  for (int w = 1; w < N; w *= 2)
+#pragma unroll
+    for (int z = 0; z + w < N; z += 2 * w) m[z] = fmaxf(m[z], m[z + w]);
+  return m[0];
+}
+template <int N>
+__device__ __forceinline__ float tree_sum(const float (&x)[N]) {
+  float m[N];
+#pragma unroll
+  for (int z = 0; z < N; ++z) m[z] = x[z];
+#pragma unroll
+  for (int w = 1; w < N; w *= 2)
+#pragma unroll
+    for (int z = 0; z + w < N; z += 2 * w) m[z] += m[z + w];
+  return m[0];
 }
 
 struct TileGeo {
@@ -142,7 +247,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       int it = 0;
       for (int t = t_begin; t < t_end; ++t, ++it) {
         const int s = it % kStages;
-        mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+        mbar_wait_sleep(&empty[s], ((it / kStages) & 1) ^ 1, 1024);
+        trace_ev(p, it, 0);
         const TileGeo g = tile_geo(p, t, L);
         uint8_t *st = smem + s * C::STAGE_BYTES;
         mbar_expect_tx(&full[s], C::STAGE_BYTES);
@@ -166,20 +272,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (it < n) {
         const int s = it % kStages, slot = it & 1;
         const TileGeo g = tile_geo(p, t_begin + it, L);
-        mbar_wait(&full[s], (it / kStages) & 1);
-        mbar_wait(&tmem_free[slot], ((it >> 1) & 1) ^ 1);
+        mbar_wait_sleep(&full[s], (it / kStages) & 1, 64);
+        if (lane == 0) trace_ev(p, it, 1);
+        mbar_wait_sleep(&tmem_free[slot], ((it >> 1) & 1) ^ 1, 64);
+        if (lane == 0) trace_ev(p, it, 2);
         tc_fence_after();
         const uint32_t q_addr = smem_u32(smem + s * C::STAGE_BYTES);
         const uint32_t k_addr = q_addr + C::Q_BYTES;
         if (elect_one()) {
+          const int rb0 = wstart(min(g.i0, q_end - 1), p.H, L) - g.hr0;
+          const int rb1 = wstart(min(g.i0 + 4, q_end - 1), p.H, L) - g.hr0;
 #pragma unroll
-          for (int sb = 0; sb < 2; ++sb) {
-            const int rb = wstart(min(g.i0 + 4 * sb, q_end - 1), p.H, L) - g.hr0;
+          for (int k = 0; k < kD / 16; ++k)
 #pragma unroll
-            for (int k = 0; k < kD / 16; ++k)
+            for (int sb = 0; sb < 2; ++sb)  // two independent accumulation chains interleaved
               mma_ss(tmem + ((uint32_t)(16 * sb) << 16) + slot * 256, sdesc_sw64(q_addr + sb * 4096 + k * 32),
-                     sdesc_sw64(k_addr + rb * kHCP * kRowBytes + k * 32), idesc_qk, k);
-          }
+                     sdesc_sw64(k_addr + (sb ? rb1 : rb0) * kHCP * kRowBytes + k * 32), idesc_qk, k);
           mma_commit(&s_full[slot]);
         }
         __syncwarp();
@@ -187,19 +295,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (it > 0) {
         const int pi = it - 1, s = pi % kStages, slot = pi & 1;
         const TileGeo g = tile_geo(p, t_begin + pi, L);
-        mbar_wait(&p_full[slot], (pi >> 1) & 1);
+        mbar_wait_sleep(&p_full[slot], (pi >> 1) & 1, 64);
+        if (lane == 0) trace_ev(p, pi, 3);
         tc_fence_after();
         const uint32_t v_addr = smem_u32(smem + s * C::STAGE_BYTES) + C::Q_BYTES + C::KV_BYTES;
         if (elect_one()) {
+          const int rb0 = wstart(min(g.i0, q_end - 1), p.H, L) - g.hr0;
+          const int rb1 = wstart(min(g.i0 + 4, q_end - 1), p.H, L) - g.hr0;
+          // 2 sub-tiles x kOAcc partial accumulators = independent MMA chains, interleaved
 #pragma unroll
-          for (int sb = 0; sb < 2; ++sb) {
-            const int rb = wstart(min(g.i0 + 4 * sb, q_end - 1), p.H, L) - g.hr0;
-            const uint32_t base = tmem + ((uint32_t)(16 * sb) << 16) + slot * 256;
-#pragma unroll 5
-            for (int ks = 0; ks < C::NSUB / 16; ++ks)
-              mma_ts(base + C::O_COL, base + C::P_COL + ks * 8,
-                     sdesc_sw64(v_addr + rb * kHCP * kRowBytes + ks * 16 * kRowBytes), idesc_pv, ks);
-          }
+          for (int ks = 0; ks < C::NSUB / 16; ++ks)
+#pragma unroll
+            for (int sb = 0; sb < 2; ++sb) {
+              const uint32_t base = tmem + ((uint32_t)(16 * sb) << 16) + slot * 256;
+              mma_ts(base + C::O_COL + (ks % kOAcc) * kD, base + C::P_COL + ks * 8,
+                     sdesc_sw64(v_addr + (sb ? rb1 : rb0) * kHCP * kRowBytes + ks * 16 * kRowBytes), idesc_pv,
+                     ks >= kOAcc);
+            }
           mma_commit(&o_full[slot]);
           mma_commit(&empty[s]);
         }
@@ -212,7 +324,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quarter = warp & 3;
     const int half = lane >> 4, r = (lane >> 2) & 3, c = lane & 3;
     float *tbl = tables + grp * C::TBL_FLOATS;
-    const uint32_t tbl_s = smem_u32(tbl);
     const int gtid = threadIdx.x - 64 - grp * 128;  // 0..127 within the group
     const int Lh = wlen(p.H, L), Lw = wlen(p.W, L);
     int cur_head = -1;
@@ -243,116 +354,102 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int uc = (wstart(min(g.j0 + 4 * quarter, p.W - 1), p.W, L) - g.hc0) & ~1;  // warp-uniform
       const int dc = sj - jc + L - 1;                                // column-clamp class
       const int bcol0 = g.hc0 + uc - jc + L - 1;                     // bias column of union col 0
-      const uint32_t tcls = tbl_s + (uint32_t)(dc * C::TROWS * kTblStride + kTblOff + bcol0) * 4u;
+      const float *tcls = tbl + dc * C::TROWS * kTblStride + kTblOff + bcol0;
       const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16) + slot * 256;
 
+      const bool tr = quarter == 2 && lane == 0;
+      if (tr) trace_ev(p, it, 4);
       mbar_wait(&s_full[slot], ph);
+      if (tr) trace_ev(p, it, 5);
       tc_fence_after();
-      // ---- pass 1: x = s*scale*log2e + T (masked); running max; x written back in place
+      const float sl2 = p.scale_log2;
+      // ---- pass 1 (rolled, two union rows per iteration: both x16 TMEM loads in flight):
+      // x = s*scale*log2e + T (masked, pre-scaled bias); row max; x written back in place (the 4
+      // extra columns of each x16 store are outside this lane's union; TMEM lanes are private)
       float mx = -INFINITY;
-#pragma unroll
-      for (int u = 0; u < C::UR; ++u) {
-        const int col = u * kHCP + uc;
-        uint32_t v[C::UCW];
-        {
-          uint32_t a8[8];
-          tmem_ld8(lane_addr + col, a8);
-#pragma unroll
-          for (int z = 0; z < 8; ++z) v[z] = a8[z];
-          if constexpr (C::UCW - 8 == 4) {
-            uint32_t a4[4];
-            tmem_ld4(lane_addr + col + 8, a4);
-#pragma unroll
-            for (int z = 0; z < 4; ++z) v[8 + z] = a4[z];
-          } else if constexpr (C::UCW - 8 == 2) {
-            uint32_t a2[2];
-            tmem_ld2(lane_addr + col + 8, a2);
-            v[8] = a2[0];
-            v[9] = a2[1];
-          }
-        }
-        const int pr = g.hr0 + rb + u;  // key row
-        const bool rv = (unsigned)(pr - si) < (unsigned)Lh;
-        const uint32_t trow = tcls + (uint32_t)((rv ? pr - ic + L - 1 : C::TT) * kTblStride) * 4u;
+#pragma unroll 1
+      for (int u = 0; u < C::UR; u += 2) {
+        uint32_t ra[16], rbv[16];
+        const uint32_t ca = lane_addr + u * kHCP + uc;
+        tmem_ld16(ca, ra);
+        tmem_ld16(ca + kHCP, rbv);
+        const int pr = g.hr0 + rb + u;  // key row of union row u
+        const bool rva = (unsigned)(pr - si) < (unsigned)Lh, rvb = (unsigned)(pr + 1 - si) < (unsigned)Lh;
+        const float *ta = tcls + (rva ? pr - ic + L - 1 : C::TT) * kTblStride;
+        const float *tb = tcls + (rvb ? pr + 1 - ic + L - 1 : C::TT) * kTblStride;
         tc_wait_ld();
+        float xa[C::UCW], xb[C::UCW];
 #pragma unroll
         for (int z = 0; z < C::UCW; ++z) {
-          const float x = fmaf(__uint_as_float(v[z]), p.scale_log2, lds_f32(trow + 4 * z));
-          mx = fmaxf(mx, x);
-          v[z] = __float_as_uint(x);
+          xa[z] = fmaf(__uint_as_float(ra[z]), sl2, ta[z]);
+          xb[z] = fmaf(__uint_as_float(rbv[z]), sl2, tb[z]);
         }
-        {
-          uint32_t a8[8];
+        mx = fmaxf(mx, fmaxf(tree_max<C::UCW>(xa), tree_max<C::UCW>(xb)));
 #pragma unroll
-          for (int z = 0; z < 8; ++z) a8[z] = v[z];
-          tmem_st8(lane_addr + col, a8);
-          if constexpr (C::UCW - 8 == 4) {
-            uint32_t a4[4] = {v[8], v[9], v[10], v[11]};
-            tmem_st4(lane_addr + col + 8, a4);
-          } else if constexpr (C::UCW - 8 == 2) {
-            uint32_t a2[2] = {v[8], v[9]};
-            tmem_st2(lane_addr + col + 8, a2);
-          }
+        for (int z = 0; z < C::UCW; ++z) {
+          ra[z] = __float_as_uint(xa[z]);
+          rbv[z] = __float_as_uint(xb[z]);
         }
+        tmem_st16(ca, ra);
+        tmem_st16(ca + kHCP, rbv);
       }
       tc_wait_st();
-      // ---- pass 2: P = exp2(x - max) (bf16 pairs over consumed S columns), row sums
+      if (tr) trace_ev(p, it, 6);
+      // ---- pass 2 (rolled, two rows per iteration): P = exp2(x - max) -> bf16 pairs over the
+      // consumed S columns.  Each halo row of P is first zeroed, then the union span written.
       float sum = 0.f;
-      const int zb = uc >> 1, za = C::UCW / 2;  // packed columns before / in the union span
-#pragma unroll
-      for (int u = 0; u < C::UR; ++u) {
-        const int col = u * kHCP + uc;
-        uint32_t v[C::UCW];
-        {
-          uint32_t a8[8];
-          tmem_ld8(lane_addr + col, a8);
-#pragma unroll
-          for (int z = 0; z < 8; ++z) v[z] = a8[z];
-          if constexpr (C::UCW - 8 == 4) {
-            uint32_t a4[4];
-            tmem_ld4(lane_addr + col + 8, a4);
-#pragma unroll
-            for (int z = 0; z < 4; ++z) v[8 + z] = a4[z];
-          } else if constexpr (C::UCW - 8 == 2) {
-            uint32_t a2[2];
-            tmem_ld2(lane_addr + col + 8, a2);
-            v[8] = a2[0];
-            v[9] = a2[1];
-          }
-        }
+      const int zb = uc >> 1;  // packed column where the union span starts (warp-uniform)
+#pragma unroll 1
+      for (int u = 0; u < C::UR; u += 2) {
+        uint32_t ra[16], rbv[16];
+        const uint32_t ca = lane_addr + u * kHCP + uc;
+        tmem_ld16(ca, ra);
+        tmem_ld16(ca + kHCP, rbv);
         tc_wait_ld();
-        uint32_t pk[C::UCW / 2];
+        uint32_t pa[C::UCW / 2], pb[C::UCW / 2];
+        float ea[C::UCW], eb[C::UCW];
+#pragma unroll
+        for (int z = 0; z < C::UCW; ++z) {
+          ea[z] = ex2(__uint_as_float(ra[z]) - mx);
+          eb[z] = ex2(__uint_as_float(rbv[z]) - mx);
+        }
 #pragma unroll
         for (int z = 0; z < C::UCW; z += 2) {
-          const float e0 = ex2(__uint_as_float(v[z]) - mx);
-          const float e1 = ex2(__uint_as_float(v[z + 1]) - mx);
-          sum += e0 + e1;
-          pk[z / 2] = pack_bf16(e0, e1);
+          pa[z / 2] = pack_bf16_alu(ea[z], ea[z + 1]);
+          pb[z / 2] = pack_bf16_alu(eb[z], eb[z + 1]);
         }
+        sum += tree_sum<C::UCW>(ea) + tree_sum<C::UCW>(eb);
         const uint32_t prow = lane_addr + C::P_COL + u * (kHCP / 2);
-        for (int z = 0; z < zb; ++z) tmem_st1(prow + z, 0u);
-        {
-          uint32_t a4[4] = {pk[0], pk[1], pk[2], pk[3]};
-          tmem_st4(prow + zb, a4);
-          if constexpr (C::UCW / 2 - 4 == 2) {
-            uint32_t a2[2] = {pk[4], pk[5]};
-            tmem_st2(prow + zb + 4, a2);
-          } else if constexpr (C::UCW / 2 - 4 == 1) {
-            tmem_st1(prow + zb + 4, pk[4]);
-          }
-        }
-        for (int z = zb + za; z < kHCP / 2; ++z) tmem_st1(prow + z, 0u);
+        st_zero12(prow);
+        st_zero12(prow + kHCP / 2);
+        st_row<C::UCW / 2>(prow + zb, pa);
+        st_row<C::UCW / 2>(prow + kHCP / 2 + zb, pb);
       }
       tc_wait_st();
+      if (tr) trace_ev(p, it, 14);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[slot]);
+      if (tr) trace_ev(p, it, 7);
+      if (lane == 0) trace_ev(p, it, 10 + quarter);
       // ---- epilogue: O / sum -> bf16, LSE
       mbar_wait(&o_full[slot], ph);
+      if (tr) trace_ev(p, it, 8);
       tc_fence_after();
       uint32_t o[32];
-      tmem_ld32(lane_addr + C::O_COL, o);
-      tc_wait_ld();
+      {
+        uint32_t oa[kOAcc][32];
+#pragma unroll
+        for (int a = 0; a < kOAcc; ++a) tmem_ld32(lane_addr + C::O_COL + a * kD, oa[a]);
+        tc_wait_ld();
+#pragma unroll
+        for (int z = 0; z < 32; ++z) {
+          float acc = __uint_as_float(oa[0][z]);
+#pragma unroll
+          for (int a = 1; a < kOAcc; ++a) acc += __uint_as_float(oa[a][z]);
+          o[z] = __float_as_uint(acc);
+        }
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tmem_free[slot]);
@@ -368,6 +465,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                   pack_bf16(__uint_as_float(o[z + 6]) * inv, __uint_as_float(o[z + 7]) * inv));
         if (p.lse) p.lse[qi] = (mx + __log2f(sum)) * 0.69314718055994531f;
       }
+      if (tr) trace_ev(p, it, 9);
     }
   }
   __syncthreads();
@@ -419,6 +517,7 @@ cudaError_t launch_fwd(const Geo &g, const void *q, const void *k, const void *v
   p.rpb = rpb;
   p.out = (__nv_bfloat16 *)out;
   p.lse = lse;
+  p.trace = (long long *)debug_trace_buffer();
   const int grid = p.num_tiles < num_sms() ? p.num_tiles : num_sms();
   ProfScope ps("na2d_fwd_tc", st);
   na2d_fwd_tc_kernel<L><<<grid, kThreads, C::SMEM, st>>>(tq, tk, tv, p);

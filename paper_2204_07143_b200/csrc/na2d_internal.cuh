@@ -49,4 +49,7 @@ cudaError_t simt_backward(const Geo &g, const void *q, const void *k, const void
                           void *dv, float *drpb, float *D, cudaStream_t st);
 int simt_launches(const Geo &g, int which);
 
+// Debug timeline buffer set through na2d_debug_set_trace (null = tracing off).
+void *debug_trace_buffer();
+
 }  // namespace na2d

@@ -61,6 +61,16 @@ void prof_end(cudaStream_t st) {
 
 using namespace na2d;
 
+namespace na2d {
+static void *g_trace = nullptr;
+void *debug_trace_buffer() { return g_trace; }
+}  // namespace na2d
+
+extern "C" na2d_status na2d_debug_set_trace(void *device_buffer) {
+  g_trace = device_buffer;
+  return NA2D_OK;
+}
+
 extern "C" na2d_status na2d_profile_enable(int on) {
   std::lock_guard<std::mutex> lk(g_mu);
   recycle_all();

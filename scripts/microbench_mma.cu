@@ -1,0 +1,84 @@
+// tcgen05.mma throughput for the shapes the NA2D kernels use (one CTA per SM, 148 CTAs).
+#include <stdint.h>
+#include <stdio.h>
+
+#include "na2d_sm100.cuh"
+
+using namespace na2d::sm100;
+
+template <int M, int N, bool TS, int CHAINS>
+__global__ void mma_bench(int iters, long long *cyc) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x / 32;
+  for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) ((uint32_t *)smem)[i] = 0x3c003c00u;
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<512>(&slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (warp == 0) {
+    constexpr uint32_t id = idesc_bf16(M, N, TS);
+    const uint32_t a = smem_u32(smem), b = smem_u32(smem + 16384);
+    long long t0 = clock64();
+    if (elect_one()) {
+      for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int c = 0; c < CHAINS; ++c) {
+          const uint32_t d = tmem + (TS ? 256 : 0) + c * (TS ? 32 : N) % 256;
+          if (TS)
+            mma_ts(tmem + 256 + c * 32, tmem + 0 + (it % 8) * 8, sdesc_sw64(b + (it % 8) * 1024), id, it > 0);
+          else
+            mma_ss(tmem + (c % 2) * 256, sdesc_sw64(a + (it % 2) * 32), sdesc_sw64(b + (it % 2) * 32), id, it > 0);
+          (void)d;
+        }
+      }
+      mma_commit(&bar);
+    }
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+template <int M, int N, bool TS, int CHAINS>
+void run(const char *name) {
+  long long *cyc;
+  cudaMallocManaged(&cyc, 148 * 8);
+  auto k = mma_bench<M, N, TS, CHAINS>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  const int iters = 2000;
+  k<<<148, 128, 100 * 1024>>>(iters, cyc);
+  cudaError_t e = cudaDeviceSynchronize();
+  double per = (double)cyc[0] / (iters * CHAINS);
+  double macs = (double)M * N * 16;
+  printf("%-34s %7.1f cyc/MMA  %6.0f MAC/clk/SM  (%s)\n", name, per, macs / per, cudaGetErrorString(e));
+}
+
+int main() {
+  run<128, 256, false, 1>("SS M=128 N=256 (1 chain)");
+  run<128, 256, false, 2>("SS M=128 N=256 (2 chains)");
+  run<64, 240, false, 1>("SS M=64 N=240 (1 chain)");
+  run<64, 240, false, 2>("SS M=64 N=240 (2 chains)");
+  run<128, 160, false, 2>("SS M=128 N=160 (2 chains)");
+  run<64, 32, true, 1>("TS M=64 N=32 (1 chain)");
+  run<64, 32, true, 4>("TS M=64 N=32 (4 chains)");
+  run<128, 32, true, 1>("TS M=128 N=32 (1 chain)");
+  run<128, 32, true, 4>("TS M=128 N=32 (4 chains)");
+  run<128, 64, true, 4>("TS M=128 N=64 (4 chains)");
+  run<64, 64, true, 4>("TS M=64 N=64 (4 chains)");
+  return 0;
+}
