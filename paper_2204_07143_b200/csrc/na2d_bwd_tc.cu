@@ -1,0 +1,71 @@
+// na2d_bwd_tc.cu -- tcgen05 backward driver: kernel B1 (dQ, D, dRPB; na2d_bwd_dq_tc.cu) then
+// dK/dV, plus the class-grouped tile order shared by the backward kernels.
+#include "na2d_internal.cuh"
+#include "na2d_tc.cuh"
+#include "na2d_tc_bwd.cuh"
+#include "na2d_tmap.cuh"
+
+namespace na2d {
+
+TileOrder make_tile_order(const Geo &g, int L) {
+  TileOrder o{};
+  o.B = g.B;
+  o.heads = g.heads;
+  o.q_row0 = g.q_row0;
+  const int ns = (L - 1) / 2, q_end = g.q_row0 + g.q_rows;
+  const int tiles_h = (g.q_rows + tc::kTQH - 1) / tc::kTQH, tiles_w = (g.W + tc::kTQW - 1) / tc::kTQW;
+  auto groups = [&](int n, int tile, int first, int end, int axis, int *start, int *count) {
+    int ng = 0;
+    int tr = 0;
+    while (tr < n) {
+      auto interior = [&](int t) {
+        const int a = first + t * tile, b = a + tile - 1;
+        return L < axis && b < end && a - ns >= 0 && b <= axis - 1 - ns;
+      };
+      if (interior(tr)) {
+        int e = tr;
+        while (e < n && interior(e)) ++e;
+        start[ng] = tr;
+        count[ng] = e - tr;
+        tr = e;
+      } else {
+        start[ng] = tr;
+        count[ng] = 1;
+        ++tr;
+      }
+      ++ng;
+    }
+    return ng;
+  };
+  o.n_rg = groups(tiles_h, tc::kTQH, g.q_row0, q_end, g.H, o.rg_start, o.rg_count);
+  o.n_cg = groups(tiles_w, tc::kTQW, 0, g.W, g.W, o.cg_start, o.cg_count);
+  o.num_tiles = g.B * g.heads * tiles_h * tiles_w;
+  return o;
+}
+
+bool tc_backward_supported(const Geo &g) {
+  if (!(g.dtype == NA2D_BF16 && g.d == tc::kD && (g.L == 3 || g.L == 5 || g.L == 7) && tmap_available()))
+    return false;
+  const TileOrder o = make_tile_order(g, g.L);
+  return o.n_rg <= TileOrder::kMaxGroups && o.n_cg <= TileOrder::kMaxGroups;
+}
+
+size_t tc_backward_scratch_bytes(const Geo &g) {
+  const int TT = 2 * g.L - 1;
+  return sizeof(float) * (size_t)dq_grid(g) * g.heads * TT * TT;
+}
+
+cudaError_t tc_backward(const Geo &g, const void *q, const void *k, const void *v, const float *rpb,
+                        const void *out, const float *lse, const void *dout, void *dq, void *dk, void *dv,
+                        float *drpb, float *D, void *scratch, cudaStream_t st) {
+  cudaError_t e = tc_backward_dq(g, q, k, v, rpb, out, lse, dout, dq, drpb, D, (float *)scratch, st);
+  if (e != cudaSuccess) return e;
+  return simt_backward_dkdv(g, q, k, v, rpb, lse, dout, D, dk, dv, st);
+}
+
+int tc_launches(const Geo &g, int which) {
+  if (which == 0) return 1;
+  return 2 + (1 /* dK/dV */);
+}
+
+}  // namespace na2d

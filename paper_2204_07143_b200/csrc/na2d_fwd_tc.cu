@@ -30,20 +30,17 @@
 #include "na2d_profile.cuh"
 #include "na2d_sm100.cuh"
 #include "na2d_tc.cuh"
+#include "na2d_tc_common.cuh"
 #include "na2d_tmap.cuh"
 
 namespace na2d {
 namespace {
 
 using namespace sm100;
+using namespace tc;
 
-constexpr int kTQH = 8, kTQW = 16, kD = 32;
-constexpr int kHCP = 24;           // halo row pitch (keys)
 constexpr int kStages = 3;
 constexpr int kThreads = 320;      // 10 warps
-constexpr int kRowBytes = kD * 2;  // 64-byte rows (32 bf16)
-constexpr int kTblStride = 40;     // floats per table row (8 mod 32: conflict-free 4x4 blocks)
-constexpr int kTblOff = 8;         // column offset for negative bias columns
 constexpr int kOAcc = 3;           // independent PV accumulators (summed in the epilogue)
 
 template <int L>
@@ -82,108 +79,6 @@ constexpr int kTraceTiles = 32, kTraceEv = 16;
 __device__ __forceinline__ void trace_ev(const FwdParams &p, int it, int ev) {
   if (p.trace && blockIdx.x < 4 && it < kTraceTiles)
     p.trace[((size_t)blockIdx.x * kTraceTiles + it) * kTraceEv + ev] = clock64();
-}
-
-// N consecutive TMEM columns of this warp's 32 lanes -> registers (N in {4,5,6,8,10,12})
-template <int N>
-__device__ __forceinline__ void ld_row(uint32_t addr, uint32_t (&v)[N]) {
-  uint32_t a8[8];
-  if constexpr (N >= 8) {
-    tmem_ld8(addr, a8);
-#pragma unroll
-    for (int z = 0; z < 8; ++z) v[z] = a8[z];
-  }
-  constexpr int R = N >= 8 ? N - 8 : N;
-  constexpr int B = N >= 8 ? 8 : 0;
-  if constexpr (R == 4) {
-    uint32_t a4[4];
-    tmem_ld4(addr + B, a4);
-#pragma unroll
-    for (int z = 0; z < 4; ++z) v[B + z] = a4[z];
-  } else if constexpr (R == 2) {
-    uint32_t a2[2];
-    tmem_ld2(addr + B, a2);
-    v[B] = a2[0];
-    v[B + 1] = a2[1];
-  } else {
-    static_assert(R == 0, "row width");
-  }
-}
-template <int N>
-__device__ __forceinline__ void st_row(uint32_t addr, const uint32_t (&v)[N]) {
-  if constexpr (N >= 8) {
-    uint32_t a8[8];
-#pragma unroll
-    for (int z = 0; z < 8; ++z) a8[z] = v[z];
-    tmem_st8(addr, a8);
-  }
-  constexpr int B = N >= 8 ? 8 : 0;
-  constexpr int R = N - B;
-  if constexpr (R >= 4) {
-    uint32_t a4[4] = {v[B], v[B + 1], v[B + 2], v[B + 3]};
-    tmem_st4(addr + B, a4);
-  }
-  constexpr int B2 = B + (R >= 4 ? 4 : 0);
-  constexpr int R2 = N - B2;
-  if constexpr (R2 >= 2) {
-    uint32_t a2[2] = {v[B2], v[B2 + 1]};
-    tmem_st2(addr + B2, a2);
-  }
-  if constexpr ((R2 & 1) == 1) tmem_st1(addr + N - 1, v[N - 1]);
-}
-__device__ __forceinline__ void st_zero12(uint32_t addr) {
-  const uint32_t z8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  const uint32_t z4[4] = {0, 0, 0, 0};
-  tmem_st8(addr, z8);
-  tmem_st4(addr + 8, z4);
-}
-// One halo row of P (kHCP/2 = 12 packed bf16 pairs): pk placed at packed column zb (warp-uniform,
-// 0 <= zb <= 12 - N), zeros elsewhere; two stores (x8 + x4) with a static register layout.
-template <int N, int ZB>
-__device__ __forceinline__ void st_prow_fixed(uint32_t addr, const uint32_t (&pk)[N]) {
-  uint32_t r[12];
-#pragma unroll
-  for (int z = 0; z < 12; ++z) r[z] = (z >= ZB && z < ZB + N) ? pk[(z - ZB) < N ? (z - ZB) : 0] : 0u;
-  uint32_t a8[8] = {r[0], r[1], r[2], r[3], r[4], r[5], r[6], r[7]};
-  uint32_t a4[4] = {r[8], r[9], r[10], r[11]};
-  tmem_st8(addr, a8);
-  tmem_st4(addr + 8, a4);
-}
-template <int N>
-__device__ __forceinline__ void st_prow(uint32_t addr, const uint32_t (&pk)[N], int zb) {
-  switch (zb) {
-    case 0: st_prow_fixed<N, 0>(addr, pk); break;
-    case 1: if constexpr (N <= 11) st_prow_fixed<N, 1>(addr, pk); break;
-    case 2: if constexpr (N <= 10) st_prow_fixed<N, 2>(addr, pk); break;
-    case 3: if constexpr (N <= 9) st_prow_fixed<N, 3>(addr, pk); break;
-    case 4: if constexpr (N <= 8) st_prow_fixed<N, 4>(addr, pk); break;
-    case 5: if constexpr (N <= 7) st_prow_fixed<N, 5>(addr, pk); break;
-    case 6: if constexpr (N <= 6) st_prow_fixed<N, 6>(addr, pk); break;
-    case 7: if constexpr (N <= 5) st_prow_fixed<N, 7>(addr, pk); break;
-    case 8: if constexpr (N <= 4) st_prow_fixed<N, 8>(addr, pk); break;
-  }
-}
-template <int N>
-__device__ __forceinline__ float tree_max(const float (&x)[N]) {
-  float m[N];
-#pragma unroll
-  for (int z = 0; z < N; ++z) m[z] = x[z];
-#pragma unroll
-  for (int w = 1; w < N; w *= 2)
-#pragma unroll
-    for (int z = 0; z + w < N; z += 2 * w) m[z] = fmaxf(m[z], m[z + w]);
-  return m[0];
-}
-template <int N>
-__device__ __forceinline__ float tree_sum(const float (&x)[N]) {
-  float m[N];
-#pragma unroll
-  for (int z = 0; z < N; ++z) m[z] = x[z];
-#pragma unroll
-  for (int w = 1; w < N; w *= 2)
-#pragma unroll
-    for (int z = 0; z + w < N; z += 2 * w) m[z] += m[z + w];
-  return m[0];
 }
 
 struct TileGeo {
@@ -334,15 +229,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int h = g.bh % p.heads;
       if (h != cur_head) {  // (re)build this group's masked, pre-scaled bias tables
         named_bar_sync(1 + grp, 128);
-        for (int e = gtid; e < C::TBL_FLOATS; e += 128) {
-          const int dc = e / (C::TROWS * kTblStride);                 // column-clamp class
-          const int rr = (e / kTblStride) % C::TROWS;                 // bias row (TT = all -inf)
-          const int cb = e % kTblStride - kTblOff;                    // bias column
-          float v = -INFINITY;
-          if (rr < C::TT && cb >= dc && cb < dc + Lw)
-            v = p.rpb ? __ldg(&p.rpb[(h * C::TT + rr) * C::TT + cb]) * p.scale_log2 : 0.f;
-          tbl[e] = v;
-        }
+        BiasTable<L>::build(tbl, p.rpb, h, Lw, p.scale_log2, gtid, 128);
         named_bar_sync(1 + grp, 128);
         cur_head = h;
       }
@@ -473,18 +360,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
-}
-
-int num_sms() {
-  static int n = 0;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  });
-  return n;
 }
 
 template <int L>

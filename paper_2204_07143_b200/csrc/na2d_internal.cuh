@@ -48,6 +48,10 @@ cudaError_t simt_backward(const Geo &g, const void *q, const void *k, const void
                           const void *out, const float *lse, const void *dout, void *dq, void *dk,
                           void *dv, float *drpb, float *D, cudaStream_t st);
 int simt_launches(const Geo &g, int which);
+// SIMT dK/dV only (uses D and LSE already computed)
+cudaError_t simt_backward_dkdv(const Geo &g, const void *q, const void *k, const void *v, const float *rpb,
+                               const float *lse, const void *dout, const float *D, void *dk, void *dv,
+                               cudaStream_t st);
 
 // Debug timeline buffer set through na2d_debug_set_trace (null = tracing off).
 void *debug_trace_buffer();

@@ -253,6 +253,15 @@ cudaError_t bwd_t(const Geo &g, const void *q, const void *k, const void *v, con
   return cudaGetLastError();
 }
 
+template <typename T, int DMAX>
+cudaError_t dkdv_t(const Geo &g, const void *q, const void *k, const void *v, const float *rpb, const float *lse,
+                   const void *dout, const float *D, void *dk, void *dv, cudaStream_t st) {
+  ProfScope ps("na2d_bwd_dkdv_simt", st);
+  dkdv_simt<T, DMAX><<<grid_for((long)g.kv_rows * g.W, g.B * g.heads), kThreads, 0, st>>>(
+      g, (const T *)q, (const T *)k, (const T *)v, rpb, lse, (const T *)dout, D, (T *)dk, (T *)dv);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 #define NA2D_DISPATCH_D(FN, T, ...)              \
@@ -276,5 +285,12 @@ cudaError_t simt_backward(const Geo &g, const void *q, const void *k, const void
 }
 
 int simt_launches(const Geo &, int which) { return which == 0 ? 1 : 3; }
+
+cudaError_t simt_backward_dkdv(const Geo &g, const void *q, const void *k, const void *v, const float *rpb,
+                               const float *lse, const void *dout, const float *D, void *dk, void *dv,
+                               cudaStream_t st) {
+  if (g.dtype == NA2D_F32) return NA2D_DISPATCH_D(dkdv_t, float, g, q, k, v, rpb, lse, dout, D, dk, dv, st);
+  return NA2D_DISPATCH_D(dkdv_t, __nv_bfloat16, g, q, k, v, rpb, lse, dout, D, dk, dv, st);
+}
 
 }  // namespace na2d

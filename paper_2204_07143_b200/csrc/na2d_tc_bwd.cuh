@@ -1,0 +1,66 @@
+// na2d_tc_bwd.cuh -- shared definitions of the tcgen05 backward kernels.
+#pragma once
+
+#include <cuda_bf16.h>
+
+#include "na2d_internal.cuh"
+#include "na2d_tc_common.cuh"
+
+namespace na2d {
+
+// Tile visiting order grouped by geometry class.  Tile rows (columns) whose 8 (16) query rows
+// (columns) are all unclamped and inside the map form one "interior" group; every other tile row
+// (column) is a group of its own.  A class is a (row group, column group) pair; tiles are
+// enumerated class-major, then head, then batch, then row, then column, so the per-lane union
+// geometry is identical for consecutive tiles of a class.
+struct TileOrder {
+  static constexpr int kMaxGroups = 16;
+  int B, heads, q_row0, num_tiles;
+  int n_rg, n_cg;
+  int rg_start[kMaxGroups], rg_count[kMaxGroups], cg_start[kMaxGroups], cg_count[kMaxGroups];
+  struct Tile {
+    int bh, i0, j0, cls;
+  };
+  __device__ __forceinline__ Tile decode(int t) const {
+    Tile x{0, 0, 0, 0};
+    for (int a = 0; a < n_rg; ++a)
+      for (int b = 0; b < n_cg; ++b) {
+        const int per_map = rg_count[a] * cg_count[b];
+        const int cnt = B * heads * per_map;
+        if (t < cnt) {
+          const int hb = t / per_map, rem = t - hb * per_map;
+          const int h = hb / B, bb = hb - h * B;
+          x.bh = bb * heads + h;
+          x.i0 = q_row0 + (rg_start[a] + rem / cg_count[b]) * tc::kTQH;
+          x.j0 = (cg_start[b] + rem % cg_count[b]) * tc::kTQW;
+          x.cls = a * n_cg + b;
+          return x;
+        }
+        t -= cnt;
+      }
+    return x;
+  }
+};
+
+// Build the class-grouped order for query tiles of a (band of a) map.
+TileOrder make_tile_order(const Geo &g, int L);
+
+struct BwdQParams {
+  int heads, H, W, q_rows, q_row0, kv_row0;
+  int num_tiles;
+  TileOrder order;
+  float scale;
+  const float *rpb;
+  const float *lse;
+  const __nv_bfloat16 *out, *dout;
+  __nv_bfloat16 *dq;
+  float *D;          // [B*heads*q_rows*W] written
+  float *drpb_part;  // [grid][heads][TT*TT] partial tables (null if no rpb)
+};
+
+int dq_grid(const Geo &g);
+cudaError_t tc_backward_dq(const Geo &g, const void *q, const void *k, const void *v, const float *rpb,
+                           const void *out, const float *lse, const void *dout, void *dq, float *drpb, float *D,
+                           float *part, cudaStream_t st);
+
+}  // namespace na2d

@@ -1,0 +1,124 @@
+// na2d_tc_common.cuh -- pieces shared by the tcgen05 NA2D kernels (forward, backward):
+// tile geometry constants, TMEM row load/store helpers, reductions and the masked
+// relative-positional-bias table.
+#pragma once
+
+#include <math.h>
+
+#include "na2d_internal.cuh"
+#include "na2d_sm100.cuh"
+
+namespace na2d {
+namespace tc {
+
+using namespace sm100;
+
+constexpr int kTQH = 8, kTQW = 16, kD = 32;  // tile: 8 x 16 queries (keys), head dim 32
+constexpr int kHCP = 24;                    // halo row pitch (keys)
+constexpr int kRowBytes = kD * 2;           // 64-byte rows (32 bf16)
+constexpr int kTblStride = 40;              // floats per table row (8 mod 32: conflict-free 4x4 blocks)
+constexpr int kTblOff = 8;                  // column offset for negative bias columns
+
+// Masked, pre-scaled bias table for one head:
+//   T[dc][a][kTblOff + b] = B[h][a][b] * mul   if b in [dc, dc + Lw)   (a < 2L-1)
+//                          = -inf               otherwise, and for the extra row a = 2L-1
+// dc = wstart(j) - j + L - 1 is the column-clamp class of the query, a/b the bias row/column
+// (key - query + L - 1).  Row validity is applied by pointing at row 2L-1 instead.
+template <int L>
+struct BiasTable {
+  static constexpr int TT = 2 * L - 1;
+  static constexpr int TROWS = TT + 1;
+  static constexpr int FLOATS = L * TROWS * kTblStride;
+  __device__ static void build(float *tbl, const float *rpb, int h, int Lw, float mul, int tid, int nthreads) {
+    for (int e = tid; e < FLOATS; e += nthreads) {
+      const int dc = e / (TROWS * kTblStride);
+      const int rr = (e / kTblStride) % TROWS;
+      const int cb = e % kTblStride - kTblOff;
+      float v = -INFINITY;
+      if (rr < TT && cb >= dc && cb < dc + Lw) v = rpb ? __ldg(&rpb[(h * TT + rr) * TT + cb]) * mul : 0.f;
+      tbl[e] = v;
+    }
+  }
+};
+
+// N consecutive TMEM columns of this warp's 32 lanes -> registers (N in {4,5,6,8,10,12})
+template <int N>
+__device__ __forceinline__ void ld_row(uint32_t addr, uint32_t (&v)[N]) {
+  uint32_t a8[8];
+  if constexpr (N >= 8) {
+    tmem_ld8(addr, a8);
+#pragma unroll
+    for (int z = 0; z < 8; ++z) v[z] = a8[z];
+  }
+  constexpr int R = N >= 8 ? N - 8 : N;
+  constexpr int B = N >= 8 ? 8 : 0;
+  if constexpr (R == 4) {
+    uint32_t a4[4];
+    tmem_ld4(addr + B, a4);
+#pragma unroll
+    for (int z = 0; z < 4; ++z) v[B + z] = a4[z];
+  } else if constexpr (R == 2) {
+    uint32_t a2[2];
+    tmem_ld2(addr + B, a2);
+    v[B] = a2[0];
+    v[B + 1] = a2[1];
+  } else {
+    static_assert(R == 0, "row width");
+  }
+}
+template <int N>
+__device__ __forceinline__ void st_row(uint32_t addr, const uint32_t (&v)[N]) {
+  if constexpr (N >= 8) {
+    uint32_t a8[8];
+#pragma unroll
+    for (int z = 0; z < 8; ++z) a8[z] = v[z];
+    tmem_st8(addr, a8);
+  }
+  constexpr int B = N >= 8 ? 8 : 0;
+  constexpr int R = N - B;
+  if constexpr (R >= 4) {
+    uint32_t a4[4] = {v[B], v[B + 1], v[B + 2], v[B + 3]};
+    tmem_st4(addr + B, a4);
+  }
+  constexpr int B2 = B + (R >= 4 ? 4 : 0);
+  constexpr int R2 = N - B2;
+  if constexpr (R2 >= 2) {
+    uint32_t a2[2] = {v[B2], v[B2 + 1]};
+    tmem_st2(addr + B2, a2);
+  }
+  if constexpr ((R2 & 1) == 1) tmem_st1(addr + N - 1, v[N - 1]);
+}
+__device__ __forceinline__ void st_zero12(uint32_t addr) {
+  const uint32_t z8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const uint32_t z4[4] = {0, 0, 0, 0};
+  tmem_st8(addr, z8);
+  tmem_st4(addr + 8, z4);
+}
+template <int N>
+__device__ __forceinline__ float tree_max(const float (&x)[N]) {
+  float m[N];
+#pragma unroll
+  for (int z = 0; z < N; ++z) m[z] = x[z];
+#pragma unroll
+  for (int w = 1; w < N; w *= 2)
+#pragma unroll
+    for (int z = 0; z + w < N; z += 2 * w) m[z] = fmaxf(m[z], m[z + w]);
+  return m[0];
+}
+template <int N>
+__device__ __forceinline__ float tree_sum(const float (&x)[N]) {
+  float m[N];
+#pragma unroll
+  for (int z = 0; z < N; ++z) m[z] = x[z];
+#pragma unroll
+  for (int w = 1; w < N; w *= 2)
+#pragma unroll
+    for (int z = 0; z + w < N; z += 2 * w) m[z] += m[z + w];
+  return m[0];
+}
+
+
+int num_sms();
+
+}  // namespace tc
+}  // namespace na2d
