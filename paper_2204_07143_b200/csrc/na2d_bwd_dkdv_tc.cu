@@ -1,0 +1,518 @@
+// na2d_bwd_dkdv_tc.cu -- backward kernel B2 (key-centric) on tcgen05/TMEM/TMA, sm_100a:
+// step a8 of the analytic gradient of Eq. 2 (R5):
+//   dV_k = sum_{q : k in rho(q)} P[q,k] dO_q,     dK_k = scale sum_{q : k in rho(q)} dS[q,k] Q_q
+// over the inverse neighbourhood of each key (the queries whose clamped window holds it).
+//
+// A CTA tile is 8 x 16 keys = two M=64 sub-tiles (key rows 0-3 / 4-7); TMEM lane quarter q owns
+// the 4 x 4 key blocks at columns [4q, 4q+4) of both.  The queries that see the tile lie in a
+// halo of rows [ilo(kr0), ihi(kr0+7)] x cols [jlo(kc0), jhi(kc0+15)] (<= 8+3NS rows, <= 16+3NS
+// columns), staged by TMA (Q, dO; row pitch QP) together with their LSE and D values.  Each
+// sub-tile's query rows are processed in chunks of CR rows (N = CR*QP = 96 queries):
+//   S^T = K_s Q_c^T, dP^T = V_s dO_c^T   (tcgen05 SS, M=64, N=96)      -> TMEM chunk slot
+//   elementwise: P = exp2(s*scale*log2e + B' - LSE*log2e), dS = P (dP - D), both bf16 -> TMEM
+//   dV_s += P^T dO_c, dK_s += dS^T Q_c     (tcgen05 TS, A from TMEM)    -> TMEM accumulators
+// Chunk slots are double-buffered; the MMA warp issues chunk k+1's S/dP before chunk k's dV/dK,
+// and two elementwise groups alternate chunks.  B' is the forward's masked bias table indexed by
+// the query's column-clamp class; rows outside the query's window use the all -inf row.
+#include <math.h>
+
+#include <mutex>
+
+#include "na2d_internal.cuh"
+#include "na2d_profile.cuh"
+#include "na2d_sm100.cuh"
+#include "na2d_tc.cuh"
+#include "na2d_tc_bwd.cuh"
+#include "na2d_tc_common.cuh"
+#include "na2d_tmap.cuh"
+
+namespace na2d {
+namespace {
+
+using namespace sm100;
+using namespace tc;
+
+constexpr int kStages = 2;
+constexpr int kThreads = 320;  // warp 0 producer, warp 1 MMA, warps 2-5 / 6-9 elementwise groups
+constexpr int kNCH = 96;       // queries per chunk (N of the S^T / dP^T MMAs)
+constexpr int kSlot = 192;     // TMEM columns per chunk slot: S^T [0,96), dP^T [96,192)
+constexpr int kDV_COL = 384, kDK_COL = 448;  // 2 partial accumulators each
+
+template <int L, int QP>
+struct CfgK {
+  static constexpr int NS = (L - 1) / 2;
+  static constexpr int CR = kNCH / QP;             // query rows per chunk
+  static constexpr int QRH = kTQH + 3 * NS;        // halo rows loaded (max needed)
+  static constexpr int QRA = QRH + CR;             // halo rows allocated (tail zero)
+  static constexpr int UCW = ((4 + 3 * NS + 1) + 1) / 2 * 2;  // union columns per quarter (even)
+  static_assert(UCW <= 16, "union width");
+  static constexpr int Q_BYTES = (QRA * QP * kRowBytes + 1023) / 1024 * 1024;  // 1 KB aligned (swizzle)
+  static constexpr int KT_BYTES = 128 * kRowBytes;
+  static constexpr int LD_FLOATS = QRA * QP;       // LSE*log2e and D halo values
+  static constexpr int STAGE_BYTES = (2 * Q_BYTES + 2 * KT_BYTES + 2 * LD_FLOATS * 4 + 1023) / 1024 * 1024;
+  static constexpr int TX_BYTES = 2 * QRH * QP * kRowBytes + 2 * KT_BYTES;
+  static_assert(STAGE_BYTES % 1024 == 0 && Q_BYTES % 1024 == 0, "1 KB alignment");
+  static constexpr int TT = 2 * L - 1;
+  static constexpr int TROWS = TT + 1;
+  static constexpr int TBL_FLOATS = (L + 1) * TROWS * kTblStride;  // + all -inf class (OOB columns)
+  static constexpr int TBL_OFF = kStages * STAGE_BYTES;
+  static constexpr int BAR_OFF = TBL_OFF + TBL_FLOATS * 4;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+  static constexpr int MAX_CHUNKS = (4 + 3 * NS + CR - 1) / CR;
+};
+
+struct BwdKParams {
+  int B, heads, H, W, q_rows, q_row0, kv_rows, kv_row0;
+  int tiles_h, tiles_w, num_tiles;
+  float scale;
+  const float *rpb, *lse, *D;
+  __nv_bfloat16 *dk, *dv;
+};
+
+// first / last query row (column) of the band whose window holds key row (column) p
+__device__ __forceinline__ int inv_lo(int p, int n, int L, int lo, int hi) {
+  const int len = wlen(n, L);
+  int i = max(lo, p - L + 1);
+  while (i < hi && wstart(i, n, L) + len - 1 < p) ++i;
+  return i;
+}
+__device__ __forceinline__ int inv_hi(int p, int n, int L, int lo, int hi) {
+  int i = min(hi - 1, p + L - 1);
+  while (i >= lo && wstart(i, n, L) > p) --i;
+  return i;
+}
+
+struct KTile {
+  int bh, kr0, kc0;   // key tile origin (global row, column)
+  int qr0, qc0;       // query halo origin (global)
+  int qs_lo[2], qs_n[2];  // per sub-tile: first query row, number of query rows
+  int nchunks;
+};
+
+template <int L, int QP>
+__device__ __forceinline__ KTile ktile(const BwdKParams &p, int t) {
+  using C = CfgK<L, QP>;
+  KTile g;
+  const int per = p.tiles_h * p.tiles_w;
+  g.bh = t / per;
+  const int rem = t - g.bh * per;
+  g.kr0 = p.kv_row0 + (rem / p.tiles_w) * kTQH;
+  g.kc0 = (rem % p.tiles_w) * kTQW;
+  const int q_end = p.q_row0 + p.q_rows, kv_end = p.kv_row0 + p.kv_rows;
+  g.qr0 = inv_lo(min(g.kr0, kv_end - 1), p.H, L, p.q_row0, q_end);
+  g.qc0 = inv_lo(min(g.kc0, p.W - 1), p.W, L, 0, p.W);
+  int nmax = 0;
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const int a = min(g.kr0 + 4 * s, kv_end - 1), b = min(g.kr0 + 4 * s + 3, kv_end - 1);
+    g.qs_lo[s] = inv_lo(a, p.H, L, p.q_row0, q_end);
+    const int hi = inv_hi(b, p.H, L, p.q_row0, q_end);
+    g.qs_n[s] = max(0, hi - g.qs_lo[s] + 1);
+    nmax = max(nmax, g.qs_n[s]);
+  }
+  g.nchunks = max(1, (nmax + C::CR - 1) / C::CR);
+  return g;
+}
+
+template <int L, int QP>
+__global__ void __launch_bounds__(kThreads, 1)
+    na2d_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
+                         const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                         const BwdKParams p) {
+  using C = CfgK<L, QP>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  float *tbl = (float *)(smem + C::TBL_OFF);
+  uint64_t *bars = (uint64_t *)(smem + C::BAR_OFF);
+  uint64_t *full = bars, *empty = bars + kStages;
+  uint64_t *s_full = bars + 2 * kStages, *ds_full = s_full + 2, *acc_full = s_full + 4, *acc_free = s_full + 5;
+  uint32_t *tmem_slot = (uint32_t *)(bars + 2 * kStages + 6);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int t_begin = (int)((long)p.num_tiles * blockIdx.x / gridDim.x);
+  const int t_end = (int)((long)p.num_tiles * (blockIdx.x + 1) / gridDim.x);
+  const int q_end = p.q_row0 + p.q_rows, kv_end = p.kv_row0 + p.kv_rows;
+
+  // zero the never-loaded tail rows of the Q / dO halos (read by partial chunks)
+  for (int s = 0; s < kStages; ++s)
+    for (int q2 = 0; q2 < 2; ++q2) {
+      uint8_t *base = smem + s * C::STAGE_BYTES + q2 * C::Q_BYTES + C::QRH * QP * kRowBytes;
+      for (int off = threadIdx.x * 16; off < (C::QRA - C::QRH) * QP * kRowBytes; off += kThreads * 16)
+        *(uint4 *)(base + off) = make_uint4(0, 0, 0, 0);
+    }
+  fence_proxy_async_smem();
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1 + 32);  // expect_tx arrive + 32 lanes staging LSE / D
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&ds_full[s], 4);
+    }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_free, 4);
+    fence_barrier_init();
+    tma_prefetch(&tm_q);
+    tma_prefetch(&tm_do);
+    tma_prefetch(&tm_k);
+    tma_prefetch(&tm_v);
+  }
+  if (warp == 0) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const float log2e = 1.4426950408889634f;
+
+  if (warp == 0) {
+    // ================= producer: TMA (K, V sub-tile blocks; Q, dO halos) + LSE / D halos
+    int it = 0;
+    for (int t = t_begin; t < t_end; ++t, ++it) {
+      const int s = it % kStages;
+      mbar_wait_sleep(&empty[s], ((it / kStages) & 1) ^ 1, 1024);
+      const KTile g = ktile<L, QP>(p, t);
+      uint8_t *st = smem + s * C::STAGE_BYTES;
+      if (elect_one()) {
+        mbar_expect_tx(&full[s], C::TX_BYTES);
+        uint8_t *kt = st + 2 * C::Q_BYTES;
+#pragma unroll
+        for (int sb = 0; sb < 2; ++sb)
+#pragma unroll
+          for (int qb = 0; qb < 4; ++qb) {
+            const int r0 = (64 * sb + 16 * qb) * kRowBytes;
+            tma_load_4d(kt + r0, &tm_k, &full[s], 0, g.kc0 + 4 * qb, g.kr0 - p.kv_row0 + 4 * sb, g.bh);
+            tma_load_4d(kt + C::KT_BYTES + r0, &tm_v, &full[s], 0, g.kc0 + 4 * qb, g.kr0 - p.kv_row0 + 4 * sb, g.bh);
+          }
+        tma_load_4d(st, &tm_q, &full[s], 0, g.qc0, g.qr0 - p.q_row0, g.bh);
+        tma_load_4d(st + C::Q_BYTES, &tm_do, &full[s], 0, g.qc0, g.qr0 - p.q_row0, g.bh);
+      }
+      __syncwarp();
+      // LSE (x log2e) and D of the halo queries; 0 outside the band / map (always masked)
+      float *lsd = (float *)(st + 2 * C::Q_BYTES + 2 * C::KT_BYTES);
+      for (int e = lane; e < C::QRA * QP; e += 32) {
+        const int i = g.qr0 + e / QP, j = g.qc0 + e % QP;
+        float l = 0.f, d = 0.f;
+        if (i < q_end && j < p.W) {
+          const size_t qi = ((size_t)g.bh * p.q_rows + (i - p.q_row0)) * p.W + j;
+          l = __ldg(&p.lse[qi]) * log2e;
+          d = __ldg(&p.D[qi]);
+        }
+        lsd[e] = l;
+        lsd[C::LD_FLOATS + e] = d;
+      }
+      mbar_arrive(&full[s]);
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer: S^T/dP^T of chunk c, then dV/dK of chunk c-1 (in-order tensor
+    // core => a chunk slot is rewritten only after the dV/dK MMAs that read it)
+    constexpr uint32_t idesc_s = idesc_bf16(64, kNCH, false);
+    constexpr uint32_t idesc_o = idesc_bf16(64, kD, true);
+    const int ntiles = t_end - t_begin;
+    int it = 0, k = 0, c = 0, tiles_done = 0;
+    KTile g{};
+    if (ntiles > 0) g = ktile<L, QP>(p, t_begin);
+    bool prev = false, prev_first = false, prev_last = false;
+    int prev_stage = 0, prev_k = 0;
+    KTile pg{};
+    for (;;) {
+      const bool have = it < ntiles;
+      const int stage = it % kStages;
+      if (have) {
+        if (k == 0) {
+          mbar_wait_sleep(&full[stage], (it / kStages) & 1, 64);
+          tc_fence_after();
+        }
+        const int x = c & 1;
+        const uint32_t q_addr = smem_u32(smem + stage * C::STAGE_BYTES);
+        const uint32_t do_addr = q_addr + C::Q_BYTES;
+        const uint32_t k_addr = q_addr + 2 * C::Q_BYTES;
+        const uint32_t v_addr = k_addr + C::KT_BYTES;
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < kD / 16; ++kk)
+#pragma unroll
+            for (int sb = 0; sb < 2; ++sb) {
+              const uint32_t lo = ((uint32_t)(16 * sb) << 16) + x * kSlot;
+              const int row = g.qs_lo[sb] - g.qr0 + C::CR * k;
+              mma_ss(tmem + lo, sdesc_sw64(k_addr + sb * 4096 + kk * 32),
+                     sdesc_sw64(q_addr + row * QP * kRowBytes + kk * 32), idesc_s, kk);
+              mma_ss(tmem + lo + kNCH, sdesc_sw64(v_addr + sb * 4096 + kk * 32),
+                     sdesc_sw64(do_addr + row * QP * kRowBytes + kk * 32), idesc_s, kk);
+            }
+          mma_commit(&s_full[x]);
+        }
+        __syncwarp();
+      }
+      if (prev) {
+        const int x = (c - 1) & 1;
+        mbar_wait_sleep(&ds_full[x], ((c - 1) >> 1) & 1, 64);
+        if (prev_first) mbar_wait_sleep(acc_free, (tiles_done & 1) ^ 1, 64);
+        tc_fence_after();
+        const uint32_t q_addr = smem_u32(smem + prev_stage * C::STAGE_BYTES);
+        const uint32_t do_addr = q_addr + C::Q_BYTES;
+        if (elect_one()) {
+#pragma unroll 1
+          for (int ks = 0; ks < kNCH / 16; ++ks)
+#pragma unroll
+            for (int sb = 0; sb < 2; ++sb) {
+              const uint32_t lo = (uint32_t)(16 * sb) << 16;
+              const int row = pg.qs_lo[sb] - pg.qr0 + C::CR * prev_k;
+              const uint32_t b_off = row * QP * kRowBytes + ks * 16 * kRowBytes;
+              const uint32_t acc = (prev_first && ks < 2) ? 0u : 1u;
+              mma_ts(tmem + lo + kDV_COL + (ks & 1) * kD, tmem + lo + x * kSlot + ks * 8,
+                     sdesc_sw64(do_addr + b_off), idesc_o, acc);
+              mma_ts(tmem + lo + kDK_COL + (ks & 1) * kD, tmem + lo + x * kSlot + kNCH + ks * 8,
+                     sdesc_sw64(q_addr + b_off), idesc_o, acc);
+            }
+          if (prev_last) {
+            mma_commit(acc_full);
+            mma_commit(&empty[prev_stage]);
+          }
+        }
+        __syncwarp();
+        if (prev_last) ++tiles_done;
+      }
+      if (!have) break;
+      prev = true;
+      prev_first = k == 0;
+      prev_last = k == g.nchunks - 1;
+      prev_stage = stage;
+      prev_k = k;
+      pg = g;
+      ++c;
+      if (++k == g.nchunks) {
+        k = 0;
+        if (++it < ntiles) g = ktile<L, QP>(p, t_begin + it);
+      }
+    }
+  } else {
+    // ================= elementwise groups: group grp handles CTA-global chunks c with c % 2 == grp
+    const int grp = (warp - 2) >> 2;
+    const int quarter = warp & 3;
+    const int half = lane >> 4, r = (lane >> 2) & 3, cc = lane & 3;
+    const int gtid = threadIdx.x - 64 - grp * 128;
+    const int Lh = wlen(p.H, L), Lw = wlen(p.W, L);
+    const uint32_t lane_q = tmem + ((uint32_t)(quarter * 32) << 16);
+    const float sl2 = p.scale * log2e;
+    int cur_head = -1;
+    int c = 0, tile_count = 0;
+    for (int t = t_begin; t < t_end; ++t) {
+      const int it = t - t_begin, stage = it % kStages;
+      const KTile g = ktile<L, QP>(p, t);
+      const int h = g.bh % p.heads;
+      if (h != cur_head) {  // both groups rebuild the shared table: sync all 256 threads
+        named_bar_sync(1, 256);
+        const int tid256 = threadIdx.x - 64;
+        BiasTable<L>::build(tbl, p.rpb, h, Lw, sl2, tid256, 256);
+        for (int e = BiasTable<L>::FLOATS + tid256; e < C::TBL_FLOATS; e += 256) tbl[e] = -INFINITY;
+        named_bar_sync(1, 256);
+        cur_head = h;
+      }
+      // this thread's key and geometry
+      const int pk = g.kr0 + 4 * half + r, qk = g.kc0 + 4 * quarter + cc;
+      const bool kvalid = pk < kv_end && qk < p.W;
+      // union columns of this quarter's key block (warp-uniform), loaded as UCW columns from an even
+      // origin clamped so the load stays inside the QP-wide halo row
+      const int uc = min((inv_lo(min(g.kc0 + 4 * quarter, p.W - 1), p.W, L, 0, p.W) - g.qc0) & ~1, QP - C::UCW);
+      const float *lsd = (const float *)(smem + stage * C::STAGE_BYTES + 2 * C::Q_BYTES + 2 * C::KT_BYTES);
+      // per union column: table class offset (column-clamp class of the query, or the -inf class)
+      int colterm[C::UCW];
+#pragma unroll
+      for (int z = 0; z < C::UCW; ++z) {
+        const int j = g.qc0 + uc + z;
+        const int dcl = j < p.W ? wstart(j, p.W, L) - j + L - 1 : L;
+        colterm[z] = dcl * C::TROWS * kTblStride - j;
+      }
+      const int nch = g.nchunks;
+      bool first_wait = true;
+      for (int k = 0; k < nch; ++k, ++c) {
+        if ((c & 1) != grp) continue;
+        const int x = c & 1;
+        if (first_wait) {
+          mbar_wait(&full[stage], (it / kStages) & 1);  // LSE / D staging visible
+          first_wait = false;
+        }
+        mbar_wait(&s_full[x], (c >> 1) & 1);
+        tc_fence_after();
+        const int i_base = g.qs_lo[half] + C::CR * k;  // query row of chunk row 0 (this half)
+        const int rows_here = g.qs_n[half] - C::CR * k;
+        const uint32_t lane_addr = lane_q + x * kSlot;
+#pragma unroll 1
+        for (int u = 0; u < C::CR; ++u) {
+          uint32_t sv[16], dpv[16];
+          const uint32_t ca = lane_addr + u * QP + uc;
+          tmem_ld16(ca, sv);
+          tmem_ld16(ca + kNCH, dpv);
+          const int i = i_base + u;
+          // row validity: i in the band, inside this half's query rows, and key row in window(i)
+          const int a = pk - i + L - 1;
+          const int dri = (i >= p.q_row0 && i < q_end) ? wstart(i, p.H, L) - i + L - 1 : -1000;
+          const bool rv = u < rows_here && (unsigned)(a - dri) < (unsigned)Lh;
+          const float *trow = tbl + (rv ? a : C::TT) * kTblStride + kTblOff + qk + L - 1;
+          const float *lrow = lsd + (i - g.qr0) * QP + uc;
+          tc_wait_ld();
+          uint32_t pp[C::UCW / 2], dd[C::UCW / 2];
+#pragma unroll
+          for (int z = 0; z < C::UCW; z += 2) {
+            float pe[2], de[2];
+#pragma unroll
+            for (int y = 0; y < 2; ++y) {
+              const float xv = fmaf(__uint_as_float(sv[z + y]), sl2, trow[colterm[z + y]]);
+              const float P = ex2(xv - lrow[z + y]);
+              pe[y] = P;
+              de[y] = P * (__uint_as_float(dpv[z + y]) - lrow[C::LD_FLOATS + z + y]);
+            }
+            pp[z / 2] = pack_bf16_alu(pe[0], pe[1]);
+            dd[z / 2] = pack_bf16_alu(de[0], de[1]);
+          }
+          const uint32_t prow = lane_addr + u * (QP / 2);
+          const uint32_t drow = prow + kNCH;
+          if constexpr (QP == 24) {
+            st_zero12(prow);
+            st_zero12(drow);
+          } else {
+            st_zero12(prow);
+            st_zero12(drow);
+            const uint32_t z4[4] = {0, 0, 0, 0};
+            tmem_st4(prow + 12, z4);
+            tmem_st4(drow + 12, z4);
+          }
+          st_row<C::UCW / 2>(prow + uc / 2, pp);
+          st_row<C::UCW / 2>(drow + uc / 2, dd);
+        }
+        tc_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ds_full[x]);
+        if (k == nch - 1) {
+          // ---- epilogue of the tile: dV, dK (scale) from the partial accumulators
+          mbar_wait(acc_full, tile_count & 1);
+          tc_fence_after();
+          uint32_t a0[32], a1[32];
+          tmem_ld32(lane_q + kDV_COL, a0);
+          tmem_ld32(lane_q + kDV_COL + kD, a1);
+          tc_wait_ld();
+          uint32_t ov[16];
+#pragma unroll
+          for (int z = 0; z < 32; z += 2)
+            ov[z / 2] = pack_bf16(__uint_as_float(a0[z]) + __uint_as_float(a1[z]),
+                                  __uint_as_float(a0[z + 1]) + __uint_as_float(a1[z + 1]));
+          tmem_ld32(lane_q + kDK_COL, a0);
+          tmem_ld32(lane_q + kDK_COL + kD, a1);
+          tc_wait_ld();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(acc_free);
+          if (kvalid) {
+            const size_t ki = ((size_t)g.bh * p.kv_rows + (pk - p.kv_row0)) * p.W + qk;
+            uint4 *dv = (uint4 *)(p.dv + ki * kD), *dk = (uint4 *)(p.dk + ki * kD);
+#pragma unroll
+            for (int z = 0; z < 4; ++z) dv[z] = make_uint4(ov[4 * z], ov[4 * z + 1], ov[4 * z + 2], ov[4 * z + 3]);
+#pragma unroll
+            for (int z = 0; z < 32; z += 8)
+              dk[z / 8] = make_uint4(
+                  pack_bf16((__uint_as_float(a0[z]) + __uint_as_float(a1[z])) * p.scale,
+                            (__uint_as_float(a0[z + 1]) + __uint_as_float(a1[z + 1])) * p.scale),
+                  pack_bf16((__uint_as_float(a0[z + 2]) + __uint_as_float(a1[z + 2])) * p.scale,
+                            (__uint_as_float(a0[z + 3]) + __uint_as_float(a1[z + 3])) * p.scale),
+                  pack_bf16((__uint_as_float(a0[z + 4]) + __uint_as_float(a1[z + 4])) * p.scale,
+                            (__uint_as_float(a0[z + 5]) + __uint_as_float(a1[z + 5])) * p.scale),
+                  pack_bf16((__uint_as_float(a0[z + 6]) + __uint_as_float(a1[z + 6])) * p.scale,
+                            (__uint_as_float(a0[z + 7]) + __uint_as_float(a1[z + 7])) * p.scale));
+          }
+        }
+      }
+      // the group that did not take the tile's last chunk still tracks the tile count
+      ++tile_count;
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+template <int L, int QP>
+cudaError_t launch_dkdv_t(const Geo &g, const void *q, const void *k, const void *v, const float *rpb,
+                          const float *lse, const void *dout, const float *D, void *dk, void *dv, cudaStream_t st) {
+  using C = CfgK<L, QP>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err =
+        cudaFuncSetAttribute(na2d_bwd_dkdv_kernel<L, QP>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  CUtensorMap tq, tdo, tk, tv;
+  const int BH = g.B * g.heads;
+  if (!make_tmap_bf16_4d(&tq, q, kD, g.W, g.q_rows, BH, QP, C::QRH) ||
+      !make_tmap_bf16_4d(&tdo, dout, kD, g.W, g.q_rows, BH, QP, C::QRH) ||
+      !make_tmap_bf16_4d(&tk, k, kD, g.W, g.kv_rows, BH, 4, 4) ||
+      !make_tmap_bf16_4d(&tv, v, kD, g.W, g.kv_rows, BH, 4, 4))
+    return cudaErrorInvalidValue;
+  BwdKParams p;
+  p.B = g.B;
+  p.heads = g.heads;
+  p.H = g.H;
+  p.W = g.W;
+  p.q_rows = g.q_rows;
+  p.q_row0 = g.q_row0;
+  p.kv_rows = g.kv_rows;
+  p.kv_row0 = g.kv_row0;
+  p.tiles_h = (g.kv_rows + kTQH - 1) / kTQH;
+  p.tiles_w = (g.W + kTQW - 1) / kTQW;
+  p.num_tiles = BH * p.tiles_h * p.tiles_w;
+  p.scale = g.scale;
+  p.rpb = rpb;
+  p.lse = lse;
+  p.D = D;
+  p.dk = (__nv_bfloat16 *)dk;
+  p.dv = (__nv_bfloat16 *)dv;
+  const int grid = p.num_tiles < tc::num_sms() ? p.num_tiles : tc::num_sms();
+  ProfScope ps("na2d_bwd_dkdv_tc", st);
+  na2d_bwd_dkdv_kernel<L, QP><<<grid, kThreads, C::SMEM, st>>>(tq, tdo, tk, tv, p);
+  return cudaGetLastError();
+}
+
+// widest query halo over the key tile columns (host replica of inv_lo / inv_hi)
+int max_query_halo_width(const Geo &g) {
+  const int L = g.L, W = g.W, len = wlen(W, L);
+  auto lo = [&](int p) {
+    int i = p - L + 1 > 0 ? p - L + 1 : 0;
+    while (i < W && wstart(i, W, L) + len - 1 < p) ++i;
+    return i;
+  };
+  auto hi = [&](int p) {
+    int i = p + L - 1 < W - 1 ? p + L - 1 : W - 1;
+    while (i >= 0 && wstart(i, W, L) > p) --i;
+    return i;
+  };
+  int w = 0;
+  for (int c0 = 0; c0 < W; c0 += tc::kTQW) {
+    const int c1 = c0 + tc::kTQW - 1 < W - 1 ? c0 + tc::kTQW - 1 : W - 1;
+    const int ww = hi(c1) - lo(c0) + 1;
+    w = ww > w ? ww : w;
+  }
+  return w;
+}
+
+}  // namespace
+
+cudaError_t tc_backward_dkdv(const Geo &g, const void *q, const void *k, const void *v, const float *rpb,
+                             const float *lse, const void *dout, const float *D, void *dk, void *dv,
+                             cudaStream_t st) {
+  const bool wide = max_query_halo_width(g) > 24;
+  switch (g.L) {
+    case 3: return wide ? launch_dkdv_t<3, 32>(g, q, k, v, rpb, lse, dout, D, dk, dv, st)
+                        : launch_dkdv_t<3, 24>(g, q, k, v, rpb, lse, dout, D, dk, dv, st);
+    case 5: return wide ? launch_dkdv_t<5, 32>(g, q, k, v, rpb, lse, dout, D, dk, dv, st)
+                        : launch_dkdv_t<5, 24>(g, q, k, v, rpb, lse, dout, D, dk, dv, st);
+    case 7: return wide ? launch_dkdv_t<7, 32>(g, q, k, v, rpb, lse, dout, D, dk, dv, st)
+                        : launch_dkdv_t<7, 24>(g, q, k, v, rpb, lse, dout, D, dk, dv, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace na2d

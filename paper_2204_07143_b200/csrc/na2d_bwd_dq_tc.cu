@@ -52,6 +52,7 @@ struct CfgQ {
   static constexpr int Q_BYTES = 128 * kRowBytes;
   static constexpr int KV_BYTES = KV_ROWS * kRowBytes;
   static constexpr int STAGE_BYTES = 2 * Q_BYTES + 2 * KV_BYTES;  // Q, dO, K, V
+  static_assert(STAGE_BYTES % 1024 == 0, "stages must stay 1 KB aligned (swizzled TMA / UMMA)");
   static constexpr int TT = 2 * L - 1;
   static constexpr int TBL_OFF = kStages * STAGE_BYTES;
   static constexpr int DB_OFF = TBL_OFF + BiasTable<L>::FLOATS * 4;

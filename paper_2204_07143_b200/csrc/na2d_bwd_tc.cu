@@ -60,7 +60,7 @@ cudaError_t tc_backward(const Geo &g, const void *q, const void *k, const void *
                         float *drpb, float *D, void *scratch, cudaStream_t st) {
   cudaError_t e = tc_backward_dq(g, q, k, v, rpb, out, lse, dout, dq, drpb, D, (float *)scratch, st);
   if (e != cudaSuccess) return e;
-  return simt_backward_dkdv(g, q, k, v, rpb, lse, dout, D, dk, dv, st);
+  return tc_backward_dkdv(g, q, k, v, rpb, lse, dout, D, dk, dv, st);
 }
 
 int tc_launches(const Geo &g, int which) {

@@ -56,6 +56,7 @@ struct Cfg {
   static constexpr int Q_BYTES = 128 * kRowBytes;
   static constexpr int KV_BYTES = KV_ROWS * kRowBytes;
   static constexpr int STAGE_BYTES = Q_BYTES + 2 * KV_BYTES;
+  static_assert(STAGE_BYTES % 1024 == 0, "stages must stay 1 KB aligned (swizzled TMA / UMMA)");
   static constexpr int TT = 2 * L - 1;
   static constexpr int TROWS = TT + 1;                             // + all -inf row
   static constexpr int TBL_FLOATS = L * TROWS * kTblStride;        // one table set (per group)

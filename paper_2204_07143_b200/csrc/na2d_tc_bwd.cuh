@@ -59,6 +59,9 @@ struct BwdQParams {
 };
 
 int dq_grid(const Geo &g);
+cudaError_t tc_backward_dkdv(const Geo &g, const void *q, const void *k, const void *v, const float *rpb,
+                             const float *lse, const void *dout, const float *D, void *dk, void *dv,
+                             cudaStream_t st);
 cudaError_t tc_backward_dq(const Geo &g, const void *q, const void *k, const void *v, const float *rpb,
                            const void *out, const float *lse, const void *dout, void *dq, float *drpb, float *D,
                            float *part, cudaStream_t st);

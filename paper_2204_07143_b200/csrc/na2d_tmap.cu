@@ -42,4 +42,17 @@ bool make_tmap_bf16_4d(CUtensorMap *m, const void *base, int dim, int W, int row
   return r == CUDA_SUCCESS;
 }
 
+bool make_tmap_f32_3d(CUtensorMap *m, const void *base, int W, int rows, int outer, int box_w, int box_h) {
+  EncodeFn fn = encode_fn();
+  if (!fn || (box_w * 4) % 16 != 0 || ((size_t)W * 4) % 16 != 0) return false;
+  const cuuint64_t gdim[3] = {(cuuint64_t)W, (cuuint64_t)rows, (cuuint64_t)outer};
+  const cuuint64_t gstride[2] = {(cuuint64_t)W * 4, (cuuint64_t)rows * W * 4};
+  const cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)box_h, 1};
+  const cuuint32_t estride[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void *>(base), gdim, gstride, box, estride,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 }  // namespace na2d

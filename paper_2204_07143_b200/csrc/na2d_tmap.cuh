@@ -15,3 +15,9 @@ bool tmap_available();
 bool make_tmap_bf16_4d(CUtensorMap *m, const void *base, int dim, int W, int rows, int outer, int box_w, int box_h);
 
 }  // namespace na2d
+
+namespace na2d {
+// 3-D fp32 tensor [outer][rows][W] (W innermost) with a box of {box_w, box_h, 1}, no swizzle
+// (LSE / D halos).  box_w * 4 must be a multiple of 16 bytes.
+bool make_tmap_f32_3d(CUtensorMap *m, const void *base, int W, int rows, int outer, int box_w, int box_h);
+}  // namespace na2d
