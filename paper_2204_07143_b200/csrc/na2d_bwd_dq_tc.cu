@@ -1,6 +1,6 @@
 // na2d_bwd_dq_tc.cu -- backward kernel B1 (query-centric) on tcgen05/TMEM/TMA, sm_100a:
 // steps a6, a7, a9, a10 of the analytic gradient of Eq. 2 (R5):
-//   D_q   = dO_q . O_q                                  (computed here, written for kernel B2)
+//   D_q   = dO_q . O_q = sum_k P dP  (exact fp32 from the recomputed P, dP; written for B2)
 //   P     = exp2(s*scale*log2e + B' - LSE_q*log2e)      (recomputed; B' masked pre-scaled bias)
 //   dP    = dO_q . v_k                                  (tcgen05, TMEM)
 //   dS    = P (dP - D_q)
@@ -244,30 +244,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         f_brow = brow0;
         f_bcol = bcol0;
       }
-      // own query: LSE (log2 units) and D = dO . O (written for kernel B2)
+      // own query: LSE (log2 units)
       const bool qvalid = i < q_end && j < p.W;
       const size_t qi = ((size_t)g.bh * p.q_rows + (ic - p.q_row0)) * p.W + jc;
-      float lse2 = 0.f, Dq = 0.f;
-      if (qvalid) {
-        lse2 = p.lse[qi] * 1.4426950408889634f;
-        const uint4 *po = (const uint4 *)(p.out + qi * kD), *pd = (const uint4 *)(p.dout + qi * kD);
-#pragma unroll
-        for (int z = 0; z < kD / 8; ++z) {
-          const uint4 a = __ldg(po + z), b = __ldg(pd + z);
-          const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, bw[4] = {b.x, b.y, b.z, b.w};
-#pragma unroll
-          for (int w = 0; w < 4; ++w) {
-            Dq = fmaf(__uint_as_float(aw[w] << 16), __uint_as_float(bw[w] << 16), Dq);
-            Dq = fmaf(__uint_as_float(aw[w] & 0xffff0000u), __uint_as_float(bw[w] & 0xffff0000u), Dq);
-          }
-        }
-        p.D[qi] = Dq;
-      }
+      const float lse2 = qvalid ? p.lse[qi] * 1.4426950408889634f : 0.f;
       const float *tcls = tbl + dc * BiasTable<L>::TROWS * kTblStride + kTblOff + bcol0;
       mbar_wait(sp_full, ph);
       tc_fence_after();
-      const int zb = uc >> 1;
-#pragma unroll
+      // ---- pass 1: P = exp2(s*scale*log2e + B' - LSE*log2e) (fp32, written over S in place) and
+      // D = dO.O = sum_window P dP (exact in fp32: O = sum P V, so dO.O = sum P (dO.v))
+      float Dq = 0.f;
+#pragma unroll 1
       for (int u = 0; u < C::UR; u += 2) {
         uint32_t sa[16], sb_[16], pa_[16], pb_[16];
         const uint32_t ca = lane_addr + u * kHCP + uc;
@@ -280,16 +267,42 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float *ta = tcls + (rva ? pr - ic + L - 1 : C::TT) * kTblStride;
         const float *tb = tcls + (rvb ? pr + 1 - ic + L - 1 : C::TT) * kTblStride;
         tc_wait_ld();
+        float da = 0.f, db = 0.f;
+#pragma unroll
+        for (int z = 0; z < C::UCW; ++z) {
+          const float P0 = ex2(fmaf(__uint_as_float(sa[z]), sl2, ta[z]) - lse2);
+          const float P1 = ex2(fmaf(__uint_as_float(sb_[z]), sl2, tb[z]) - lse2);
+          da = fmaf(P0, __uint_as_float(pa_[z]), da);
+          db = fmaf(P1, __uint_as_float(pb_[z]), db);
+          sa[z] = __float_as_uint(P0);
+          sb_[z] = __float_as_uint(P1);
+        }
+        Dq += da + db;
+        tmem_st16(ca, sa);
+        tmem_st16(ca + kHCP, sb_);
+      }
+      if (qvalid) p.D[qi] = Dq;
+      tc_wait_st();
+      // ---- pass 2: dS = P (dP - D) -> dRPB accumulators (union coordinates) and bf16 pairs over
+      // the consumed S/P columns (the dQ MMA's A operand)
+      const int zb = uc >> 1;
+#pragma unroll
+      for (int u = 0; u < C::UR; u += 2) {
+        uint32_t sa[16], sb_[16], pa_[16], pb_[16];
+        const uint32_t ca = lane_addr + u * kHCP + uc;
+        tmem_ld16(ca, sa);
+        tmem_ld16(ca + kHCP, sb_);
+        tmem_ld16(ca + kDP_COL, pa_);
+        tmem_ld16(ca + kDP_COL + kHCP, pb_);
+        tc_wait_ld();
         uint32_t da[C::UCW / 2], db[C::UCW / 2];
 #pragma unroll
         for (int z = 0; z < C::UCW; z += 2) {
           float d2[2][2];
 #pragma unroll
           for (int y = 0; y < 2; ++y) {
-            const float P0 = ex2(fmaf(__uint_as_float(sa[z + y]), sl2, ta[z + y]) - lse2);
-            const float P1 = ex2(fmaf(__uint_as_float(sb_[z + y]), sl2, tb[z + y]) - lse2);
-            d2[0][y] = P0 * (__uint_as_float(pa_[z + y]) - Dq);
-            d2[1][y] = P1 * (__uint_as_float(pb_[z + y]) - Dq);
+            d2[0][y] = __uint_as_float(sa[z + y]) * (__uint_as_float(pa_[z + y]) - Dq);
+            d2[1][y] = __uint_as_float(sb_[z + y]) * (__uint_as_float(pb_[z + y]) - Dq);
             acc[u][z + y] += d2[0][y];
             acc[u + 1][z + y] += d2[1][y];
           }

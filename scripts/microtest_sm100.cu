@@ -6,6 +6,7 @@
 //  4. shared-memory fp32 atomic add throughput (distinct addresses per lane, same address).
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O2 -I../paper_2204_07143_b200/csrc microtest_sm100.cu
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -144,6 +145,54 @@ __global__ void test_m64(float *outD, float *outD2, const float *A, const float 
   }
 }
 
+// A (fp16 pairs) from TMEM x B (bf16, smem MN-major): can kind::f16 mix operand types?
+__global__ void test_mixed(const float *A, const float *B, float *out, int a_fmt) {
+  __shared__ __align__(1024) uint8_t sv[64 * 64];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  for (int i = tid; i < 64 * 32; i += blockDim.x) store_sw64(sv, i / 32, i % 32, __float2bfloat16(B[i]));
+  fence_proxy_async_smem();
+  if (tid == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
+  if (warp == 0) tmem_alloc<256>(&slot);
+  tc_fence_before(); __syncthreads(); tc_fence_after();
+  const uint32_t tmem = slot;
+  // row m = lane of quarter: A[m][k] for k < 64, packed fp16 (a_fmt 0) or bf16 (a_fmt 1)
+  {
+    const int m = warp * 32 + lane;
+    uint32_t pk[8];
+    for (int g = 0; g < 4; ++g) {
+      for (int c = 0; c < 8; ++c) {
+        float lo = A[(m % 64) * 64 + g * 16 + 2 * c], hi = A[(m % 64) * 64 + g * 16 + 2 * c + 1];
+        if (a_fmt == 0) {
+          __half2 h = __floats2half2_rn(lo, hi);
+          pk[c] = *(uint32_t *)&h;
+        } else pk[c] = pack_bf16(lo, hi);
+      }
+      tmem_st8(tmem + ((uint32_t)(warp * 32) << 16) + g * 8, pk);
+    }
+    tc_wait_st();
+  }
+  tc_fence_before(); __syncthreads(); tc_fence_after();
+  if (warp == 0) {
+    if (elect_one()) {
+      const uint32_t id = ((1u << 4) | ((uint32_t)a_fmt << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(32 >> 3) << 17) |
+                           ((uint32_t)(128 >> 4) << 24));
+      for (int ks = 0; ks < 4; ++ks) mma_ts(tmem + 128, tmem + ks * 8, sdesc_sw64(smem_u32(sv) + ks * 1024), id, ks);
+      mma_commit(&bar);
+    }
+    __syncwarp();
+  }
+  mbar_wait(&bar, 0);
+  tc_fence_after();
+  uint32_t r[32];
+  tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + 128, r);
+  tc_wait_ld();
+  for (int c = 0; c < 32; ++c) out[(warp * 32 + lane) * 32 + c] = __uint_as_float(r[c]);
+  tc_fence_before(); __syncthreads();
+  if (warp == 0) { tc_fence_after(); tmem_dealloc<256>(tmem); }
+}
+
 __global__ void atom_bench(float *out, int mode, int iters, long long *cycles) {
   __shared__ float acc[4096];
   for (int i = threadIdx.x; i < 4096; i += blockDim.x) acc[i] = 0.f;
@@ -218,6 +267,29 @@ int main() {
     }
   }
   printf("TS MMA mismatches %d\n", badts);
+  {
+    float *A2, *B2, *O2;
+    cudaMallocManaged(&A2, 64 * 64 * 4);
+    cudaMallocManaged(&B2, 64 * 32 * 4);
+    cudaMallocManaged(&O2, 128 * 32 * 4);
+    for (int i = 0; i < 64 * 64; ++i) A2[i] = (float)(rand() % 20001 - 10000) * 1.2345e-5f;  // fine-grained values
+    for (int i = 0; i < 64 * 32; ++i) B2[i] = (float)((rand() % 17) - 8) / 8.f;
+    for (int fmt = 0; fmt < 2; ++fmt) {
+      test_mixed<<<1, 128>>>(A2, B2, O2, fmt);
+      cudaError_t e = cudaDeviceSynchronize();
+      printf("test_mixed fmt %d: %s\n", fmt, cudaGetErrorString(e));
+      fflush(stdout);
+      if (e != cudaSuccess) return 1;
+      double maxerr = 0;
+      for (int m = 0; m < 128; ++m)
+        for (int d = 0; d < 32; ++d) {
+          double ex = 0;
+          for (int k = 0; k < 64; ++k) ex += (double)A2[(m % 64) * 64 + k] * B2[k * 32 + d];
+          maxerr = fmax(maxerr, fabs(ex - O2[m * 32 + d]));
+        }
+      printf("TS A=%s (TMEM) x B=bf16: %s, max abs err vs fp64 %.3e\n", fmt == 0 ? "fp16" : "bf16", cudaGetErrorString(e), maxerr);
+    }
+  }
   float *out;
   long long *cyc;
   cudaMallocManaged(&out, 4096 * 4);
