@@ -1,0 +1,176 @@
+"""Multi-GPU partitioning of NA2D: one process per GPU, torch.distributed (NCCL on
+GPUs, gloo in the CPU tests) for the plumbing.  The kernels stay in libna2d; this module only plans
+the partition and moves the few bytes that cross it.
+
+* Batch x heads sharding -- every (b, h) map is independent.  Ranks hold contiguous
+  batch shards; forward needs no communication; backward's only exchange is the all-reduce of the
+  dRPB partial (all ranks share the heads' bias tables): heads * (2L-1)^2 * 4 bytes.
+* Row bands -- for maps too large for one rank (COCO-shaped 200 x 336): rank r owns query rows
+  [r0, r1) of every map.  Its queries' windows need K/V rows [wstart(r0), wstart(r1-1) + L), i.e.
+  at most (L-1)/2 rows of each neighbour (band height >= L).  Forward: receive those halo rows
+  (send/recv with ranks r-1 and r+1), run the band kernel in global coordinates.  Backward: run
+  the band kernel over the extended K/V rows (dK/dV partials for the halo rows come from this
+  rank's queries), send the halo partials back to their owners, add the received ones, and
+  all-reduce dRPB.
+
+Compute functions are injectable (``forward_fn``, ``backward_fn``) so the host logic is tested on
+CPU with gloo and the fp64 oracle; the defaults call the CUDA library.
+"""
+from __future__ import annotations
+
+import dataclasses
+
+import torch
+import torch.distributed as dist
+
+
+def _wstart(i: int, n: int, L: int) -> int:
+    if L >= n:
+        return 0
+    return min(max(i - (L - 1) // 2, 0), n - L)
+
+
+# ------------------------------------------------------------------ batch x heads sharding
+
+def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous [start, stop) of n units owned by `rank` (sizes differ by at most 1)."""
+    return n * rank // world, n * (rank + 1) // world
+
+
+def allreduce_drpb(drpb: torch.Tensor | None, group=None) -> torch.Tensor | None:
+    """Sum the dRPB partials of all ranks in place (the only exchange of the sharded backward)."""
+    if drpb is not None and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(drpb, op=dist.ReduceOp.SUM, group=group)
+    return drpb
+
+
+# ------------------------------------------------------------------ row bands
+
+@dataclasses.dataclass(frozen=True)
+class Band:
+    rank: int
+    world: int
+    H: int
+    L: int
+    r0: int   # owned query / key rows [r0, r1)
+    r1: int
+    k0: int   # K/V rows the owned queries need [k0, k1)
+    k1: int
+
+    @property
+    def top(self) -> int:     # halo rows received from rank-1 (its last rows)
+        return self.r0 - self.k0
+
+    @property
+    def bottom(self) -> int:  # halo rows received from rank+1 (its first rows)
+        return self.k1 - self.r1
+
+
+def band_plan(H: int, world: int, L: int) -> list[Band]:
+    """Equal row bands; every band must hold >= L rows so halos only reach adjacent ranks and
+    never exceed (L-1)/2 rows."""
+    bands = []
+    for r in range(world):
+        r0, r1 = H * r // world, H * (r + 1) // world
+        if r1 - r0 < L:
+            raise ValueError(f"band {r} has {r1 - r0} rows < kernel size {L}")
+        k0 = _wstart(r0, H, L)
+        k1 = _wstart(r1 - 1, H, L) + min(L, H)
+        assert r0 - k0 <= (L - 1) // 2 and k1 - r1 <= (L - 1) // 2
+        bands.append(Band(r, world, H, L, r0, r1, k0, k1))
+    return bands
+
+
+def _exchange_rows(own: torch.Tensor, band: Band, group=None) -> torch.Tensor:
+    """own: [..., r1-r0, W, d] rows of this rank -> [..., k1-k0, W, d] with neighbour halos."""
+    rows = own.shape[-3]
+    ops, recv_top, recv_bot = [], None, None
+    prev, nxt = band.rank - 1, band.rank + 1
+    # what the neighbours need from us: rank-1's bottom halo = our first rows; rank+1's top = our last
+    if prev >= 0:
+        need_prev = _neighbour(band, prev).bottom
+        if need_prev:
+            ops.append(dist.P2POp(dist.isend, own[..., :need_prev, :, :].contiguous(), prev, group))
+        if band.top:
+            recv_top = torch.empty_like(own[..., :band.top, :, :])
+            ops.append(dist.P2POp(dist.irecv, recv_top, prev, group))
+    if nxt < band.world:
+        need_next = _neighbour(band, nxt).top
+        if need_next:
+            ops.append(dist.P2POp(dist.isend, own[..., rows - need_next:, :, :].contiguous(), nxt, group))
+        if band.bottom:
+            recv_bot = torch.empty_like(own[..., :band.bottom, :, :])
+            ops.append(dist.P2POp(dist.irecv, recv_bot, nxt, group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    parts = [x for x in (recv_top, own, recv_bot) if x is not None]
+    return torch.cat(parts, dim=-3) if len(parts) > 1 else own
+
+
+def _return_partials(ext: torch.Tensor, band: Band, group=None) -> torch.Tensor:
+    """ext: [..., k1-k0, W, d] partial gradients for the extended rows; send the halo rows back to
+    their owners, add what the neighbours computed for our rows; returns [..., r1-r0, W, d] (>= fp32)."""
+    ext = ext if ext.dtype == torch.float64 else ext.float()  # accumulate partials in >= fp32
+    own = ext[..., band.top:band.top + (band.r1 - band.r0), :, :].clone()
+    ops, recvs = [], []
+    prev, nxt = band.rank - 1, band.rank + 1
+    if prev >= 0:
+        if band.top:
+            ops.append(dist.P2POp(dist.isend, ext[..., :band.top, :, :].contiguous(), prev, group))
+        nb = _neighbour(band, prev).bottom  # rank-1 computed partials for our first nb rows
+        if nb:
+            buf = torch.empty_like(own[..., :nb, :, :])
+            ops.append(dist.P2POp(dist.irecv, buf, prev, group))
+            recvs.append((0, buf))
+    if nxt < band.world:
+        if band.bottom:
+            ops.append(dist.P2POp(dist.isend, ext[..., ext.shape[-3] - band.bottom:, :, :].contiguous(), nxt, group))
+        nt = _neighbour(band, nxt).top  # rank+1 computed partials for our last nt rows
+        if nt:
+            buf = torch.empty_like(own[..., :nt, :, :])
+            ops.append(dist.P2POp(dist.irecv, buf, nxt, group))
+            recvs.append((own.shape[-3] - nt, buf))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    for off, buf in recvs:
+        own[..., off:off + buf.shape[-3], :, :] += buf
+    return own
+
+
+def _neighbour(band: Band, r: int) -> Band:
+    return band_plan(band.H, band.world, band.L)[r]
+
+
+def _cuda_forward(q, k, v, rpb, L, scale, *, map_height, q_row0, kv_row0):
+    from . import forward
+    return forward(q, k, v, rpb, L, scale, map_height=map_height, q_row0=q_row0, kv_row0=kv_row0)
+
+
+def _cuda_backward(q, k, v, rpb, out, lse, dout, L, scale, *, map_height, q_row0, kv_row0):
+    from . import backward
+    return backward(q, k, v, rpb, out, lse, dout, L, scale, map_height=map_height, q_row0=q_row0,
+                    kv_row0=kv_row0)
+
+
+def band_forward(q, k, v, rpb, L: int, scale: float | None, band: Band, group=None, forward_fn=None):
+    """q, k, v: this rank's own rows [B, heads, r1-r0, W, d].  Returns (out, lse) for own rows."""
+    fn = forward_fn or _cuda_forward
+    k_ext = _exchange_rows(k, band, group)
+    v_ext = _exchange_rows(v, band, group)
+    out, lse = fn(q, k_ext, v_ext, rpb, L, scale, map_height=band.H, q_row0=band.r0, kv_row0=band.k0)
+    return out, lse, (k_ext, v_ext)
+
+
+def band_backward(q, k_ext, v_ext, rpb, out, lse, dout, L: int, scale: float | None, band: Band, group=None,
+                  backward_fn=None):
+    """Backward of a band given the extended K/V from band_forward.  Returns (dq, dk, dv, drpb) for
+    own rows (dk, dv in fp32 after the halo-partial exchange; drpb all-reduced)."""
+    fn = backward_fn or _cuda_backward
+    dq, dk_ext, dv_ext, drpb = fn(q, k_ext, v_ext, rpb, out, lse, dout, L, scale, map_height=band.H,
+                                  q_row0=band.r0, kv_row0=band.k0)
+    dk = _return_partials(dk_ext, band, group)
+    dv = _return_partials(dv_ext, band, group)
+    allreduce_drpb(drpb, group)
+    return dq, dk, dv, drpb
