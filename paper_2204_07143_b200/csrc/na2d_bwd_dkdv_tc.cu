@@ -46,9 +46,14 @@ struct CfgK {
   static constexpr int QRA = QRH + CR;             // halo rows allocated (tail zero)
   static constexpr int UCW = ((4 + 3 * NS + 1) + 1) / 2 * 2;  // union columns per quarter (even)
   static_assert(UCW <= 16, "union width");
+  // interior quarters (every union column of clamp class NS): union of 4 keys' inverse neighbourhoods
+  // is 4 + 2NS columns, + 1 for the even origin
+  static constexpr int UCWF = ((4 + 2 * NS + 1) + 1) / 2 * 2;
   static constexpr int Q_BYTES = (QRA * QP * kRowBytes + 1023) / 1024 * 1024;  // 1 KB aligned (swizzle)
   static constexpr int KT_BYTES = 128 * kRowBytes;
-  static constexpr int LD_FLOATS = QRA * QP;       // LSE*log2e and D halo values
+  // LSE and D halo values: pitch LP = QP + 4 so the TMA box can start at a 16-byte aligned column
+  static constexpr int LP = QP + 4;
+  static constexpr int LD_FLOATS = (QRA * LP + 31) / 32 * 32;  // 128 B aligned
   static constexpr int STAGE_BYTES = (2 * Q_BYTES + 2 * KT_BYTES + 2 * LD_FLOATS * 4 + 1023) / 1024 * 1024;
   static constexpr int TX_BYTES = 2 * QRH * QP * kRowBytes + 2 * KT_BYTES;
   static_assert(STAGE_BYTES % 1024 == 0 && Q_BYTES % 1024 == 0, "1 KB alignment");
@@ -64,22 +69,27 @@ struct CfgK {
 struct BwdKParams {
   int B, heads, H, W, q_rows, q_row0, kv_rows, kv_row0;
   int tiles_h, tiles_w, num_tiles;
+  int tma_lsd;  // LSE / D halos by TMA (W * 4 bytes 16-byte aligned) instead of lane loads
   float scale;
   const float *rpb, *lse, *D;
   __nv_bfloat16 *dk, *dv;
+  long long *trace;
 };
+// debug timeline: trace[(cta * 32 + chunk) * 16 + ev] for CTAs < 4 (chunk = CTA-global chunk index)
+__device__ __forceinline__ void ktrace(const BwdKParams &p, int c, int ev) {
+  if (p.trace && blockIdx.x < 4 && c < 32) p.trace[((size_t)blockIdx.x * 32 + c) * 16 + ev] = clock64();
+}
 
-// first / last query row (column) of the band whose window holds key row (column) p
+// first / last query row (column) in [lo, hi) whose clamped window holds key row (column) p.
+// Closed form of the inverse neighbourhood: for L < n, wstart(i) + L - 1 >= p  <=>  i >= p - NS
+// (when p >= L) and wstart(i) <= p  <=>  i <= p + NS (when p < n - L); else unbounded.
 __device__ __forceinline__ int inv_lo(int p, int n, int L, int lo, int hi) {
-  const int len = wlen(n, L);
-  int i = max(lo, p - L + 1);
-  while (i < hi && wstart(i, n, L) + len - 1 < p) ++i;
-  return i;
+  const int ns = (L - 1) / 2;
+  return (L >= n || p < L) ? lo : max(lo, p - ns);
 }
 __device__ __forceinline__ int inv_hi(int p, int n, int L, int lo, int hi) {
-  int i = min(hi - 1, p + L - 1);
-  while (i >= lo && wstart(i, n, L) > p) --i;
-  return i;
+  const int ns = (L - 1) / 2;
+  return (L >= n || p >= n - L) ? hi - 1 : min(hi - 1, p + ns);
 }
 
 struct KTile {
@@ -100,7 +110,8 @@ __device__ __forceinline__ KTile ktile(const BwdKParams &p, int t) {
   g.kc0 = (rem % p.tiles_w) * kTQW;
   const int q_end = p.q_row0 + p.q_rows, kv_end = p.kv_row0 + p.kv_rows;
   g.qr0 = inv_lo(min(g.kr0, kv_end - 1), p.H, L, p.q_row0, q_end);
-  g.qc0 = inv_lo(min(g.kc0, p.W - 1), p.W, L, 0, p.W);
+  // even origin: (qc0 & 3) + uc is even, so LSE / D pairs are 8-byte aligned (LDS.64)
+  g.qc0 = inv_lo(min(g.kc0, p.W - 1), p.W, L, 0, p.W) & ~1;
   int nmax = 0;
 #pragma unroll
   for (int s = 0; s < 2; ++s) {
@@ -114,10 +125,80 @@ __device__ __forceinline__ KTile ktile(const BwdKParams &p, int t) {
   return g;
 }
 
+// Elementwise rows of one chunk for one lane (one key): for each chunk row u and union column z
+//   P = exp2(s*scale*log2e + B'[row][col] - LSE*log2e),  dS = P (dP - D)  -> bf16 pairs over S / dP.
+// FAST: every union column of the quarter is an interior column (column-clamp class NS), so the
+// bias address is trow - z (immediate offsets); otherwise per-column class offsets (colterm).
+template <int L, int QP, bool FAST>
+__device__ __forceinline__ void chunk_rows(uint32_t lane_addr, int uc, const float *tbl_row0,
+                                           const int (&colterm)[CfgK<L, QP>::UCW], const float *lrow0,
+                                           int pk, int i_base, int H, int rows_here, int Lh, float sl2) {
+  using C = CfgK<L, QP>;
+  constexpr int UW = FAST ? C::UCWF : C::UCW;
+  constexpr float log2e = 1.4426950408889634f;
+#pragma unroll
+  for (int u0 = 0; u0 < C::CR; u0 += 2) {
+    // two chunk rows per step: all four x16 TMEM loads in flight before the wait
+    constexpr int NR = 2;
+    uint32_t sv[NR][16], dpv[NR][16];
+    const float *trow[NR], *lrow[NR];
+#pragma unroll
+    for (int y = 0; y < NR; ++y) {
+      const int u = u0 + y;
+      if (u >= C::CR) break;
+      const uint32_t ca = lane_addr + u * QP + uc;
+      tmem_ld16(ca, sv[y]);
+      tmem_ld16(ca + kNCH, dpv[y]);
+      // row validity: inside this half's query rows and key row pk in window(i); a = pk - i + L - 1
+      const int i = i_base + u;
+      const bool rv = u < rows_here && (unsigned)(pk - wstart(i, H, L)) < (unsigned)Lh;
+      const int a = pk - i + L - 1;
+      trow[y] = tbl_row0 + (rv ? a : C::TT) * kTblStride;
+      lrow[y] = lrow0 + u * C::LP;
+    }
+    tc_wait_ld();
+#pragma unroll
+    for (int y = 0; y < NR; ++y) {
+      const int u = u0 + y;
+      if (u >= C::CR) break;
+      uint32_t pp[UW / 2], dd[UW / 2];
+#pragma unroll
+      for (int z = 0; z < UW; z += 2) {
+        // one element pair per step in packed fp32x2 arithmetic (FFMA2 / FADD2 / FMUL2; half the
+        // issue slots of scalar code), bf16x2 packs by F2FP (full rate, not on the MUFU pipe)
+        const float2 lz = *reinterpret_cast<const float2 *>(lrow[y] + z);
+        const float2 dz = *reinterpret_cast<const float2 *>(lrow[y] + C::LD_FLOATS + z);
+        const float2 tb = FAST ? make_float2(trow[y][-z], trow[y][-(z + 1)])
+                               : make_float2(trow[y][colterm[z]], trow[y][colterm[z + 1]]);
+        const float2 sz = make_float2(__uint_as_float(sv[y][z]), __uint_as_float(sv[y][z + 1]));
+        const float2 xv = __ffma2_rn(sz, make_float2(sl2, sl2), tb);
+        const float2 ar = __ffma2_rn(lz, make_float2(-log2e, -log2e), xv);
+        const float2 P = make_float2(ex2(ar.x), ex2(ar.y));
+        const float2 dp = make_float2(__uint_as_float(dpv[y][z]), __uint_as_float(dpv[y][z + 1]));
+        const float2 dS = __fmul2_rn(P, __fadd2_rn(dp, make_float2(-dz.x, -dz.y)));
+        pp[z / 2] = pack_bf16(P.x, P.y);
+        dd[z / 2] = pack_bf16(dS.x, dS.y);
+      }
+      const uint32_t prow = lane_addr + u * (QP / 2);
+      const uint32_t drow = prow + kNCH;
+      st_zero12(prow);
+      st_zero12(drow);
+      if constexpr (QP == 32) {
+        const uint32_t z4[4] = {0, 0, 0, 0};
+        tmem_st4(prow + 12, z4);
+        tmem_st4(drow + 12, z4);
+      }
+      st_row<UW / 2>(prow + uc / 2, pp);
+      st_row<UW / 2>(drow + uc / 2, dd);
+    }
+  }
+}
+
 template <int L, int QP>
 __global__ void __launch_bounds__(kThreads, 1)
     na2d_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                          const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                         const __grid_constant__ CUtensorMap tm_lse, const __grid_constant__ CUtensorMap tm_d,
                          const BwdKParams p) {
   using C = CfgK<L, QP>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -140,10 +221,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int off = threadIdx.x * 16; off < (C::QRA - C::QRH) * QP * kRowBytes; off += kThreads * 16)
         *(uint4 *)(base + off) = make_uint4(0, 0, 0, 0);
     }
+  for (int s = 0; s < kStages; ++s) {  // LSE / D halo rows the TMA box never covers
+    float *lsd = (float *)(smem + s * C::STAGE_BYTES + 2 * C::Q_BYTES + 2 * C::KT_BYTES);
+    for (int e = C::QRH * C::LP + threadIdx.x; e < C::LD_FLOATS; e += kThreads) {
+      lsd[e] = 0.f;
+      lsd[C::LD_FLOATS + e] = 0.f;
+    }
+  }
   fence_proxy_async_smem();
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1 + 32);  // expect_tx arrive + 32 lanes staging LSE / D
+      mbar_init(&full[s], p.tma_lsd ? 1 : 1 + 32);  // expect_tx arrive (+ 32 lanes staging LSE / D)
       mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
@@ -157,6 +245,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&tm_do);
     tma_prefetch(&tm_k);
     tma_prefetch(&tm_v);
+    if (p.tma_lsd) {
+      tma_prefetch(&tm_lse);
+      tma_prefetch(&tm_d);
+    }
   }
   if (warp == 0) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
@@ -171,10 +263,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int t = t_begin; t < t_end; ++t, ++it) {
       const int s = it % kStages;
       mbar_wait_sleep(&empty[s], ((it / kStages) & 1) ^ 1, 1024);
+      if (lane == 0) ktrace(p, it, 14);
       const KTile g = ktile<L, QP>(p, t);
       uint8_t *st = smem + s * C::STAGE_BYTES;
+      float *lsd = (float *)(st + 2 * C::Q_BYTES + 2 * C::KT_BYTES);
       if (elect_one()) {
-        mbar_expect_tx(&full[s], C::TX_BYTES);
+        mbar_expect_tx(&full[s], C::TX_BYTES + (p.tma_lsd ? 2 * C::QRH * C::LP * 4 : 0));
+        if (p.tma_lsd) {  // box origin column rounded down to a multiple of 4 (16-byte aligned)
+          tma_load_3d(lsd, &tm_lse, &full[s], g.qc0 & ~3, g.qr0 - p.q_row0, g.bh);
+          tma_load_3d(lsd + C::LD_FLOATS, &tm_d, &full[s], g.qc0 & ~3, g.qr0 - p.q_row0, g.bh);
+        }
         uint8_t *kt = st + 2 * C::Q_BYTES;
 #pragma unroll
         for (int sb = 0; sb < 2; ++sb)
@@ -188,20 +286,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_4d(st + C::Q_BYTES, &tm_do, &full[s], 0, g.qc0, g.qr0 - p.q_row0, g.bh);
       }
       __syncwarp();
-      // LSE (x log2e) and D of the halo queries; 0 outside the band / map (always masked)
-      float *lsd = (float *)(st + 2 * C::Q_BYTES + 2 * C::KT_BYTES);
-      for (int e = lane; e < C::QRA * QP; e += 32) {
-        const int i = g.qr0 + e / QP, j = g.qc0 + e % QP;
-        float l = 0.f, d = 0.f;
-        if (i < q_end && j < p.W) {
-          const size_t qi = ((size_t)g.bh * p.q_rows + (i - p.q_row0)) * p.W + j;
-          l = __ldg(&p.lse[qi]) * log2e;
-          d = __ldg(&p.D[qi]);
+      if (!p.tma_lsd) {
+        // LSE and D of the halo queries by lane loads (W * 4 not 16-byte aligned); 0 outside the
+        // band / map (always masked).  All of a lane's loads are issued before its stores.
+        constexpr int PER_LANE = (C::QRH * C::LP + 31) / 32;
+        float lv[PER_LANE], dv[PER_LANE];
+#pragma unroll
+        for (int u = 0; u < PER_LANE; ++u) {
+          const int e = lane + 32 * u;
+          const int i = g.qr0 + e / C::LP, j = (g.qc0 & ~3) + e % C::LP;
+          lv[u] = 0.f;
+          dv[u] = 0.f;
+          if (e < C::QRH * C::LP && i < q_end && j < p.W) {
+            const size_t qi = ((size_t)g.bh * p.q_rows + (i - p.q_row0)) * p.W + j;
+            lv[u] = __ldg(&p.lse[qi]);
+            dv[u] = __ldg(&p.D[qi]);
+          }
         }
-        lsd[e] = l;
-        lsd[C::LD_FLOATS + e] = d;
+#pragma unroll
+        for (int u = 0; u < PER_LANE; ++u) {
+          const int e = lane + 32 * u;
+          if (e < C::QRH * C::LP) {
+            lsd[e] = lv[u];
+            lsd[C::LD_FLOATS + e] = dv[u];
+          }
+        }
       }
-      mbar_arrive(&full[s]);
+      if (lane == 0) ktrace(p, it, 15);
+      if (!p.tma_lsd) mbar_arrive(&full[s]);
     }
   } else if (warp == 1) {
     // ================= MMA issuer: S^T/dP^T of chunk c, then dV/dK of chunk c-1 (in-order tensor
@@ -221,6 +333,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (have) {
         if (k == 0) {
           mbar_wait_sleep(&full[stage], (it / kStages) & 1, 64);
+          if (lane == 0) ktrace(p, c, 3);
           tc_fence_after();
         }
         const int x = c & 1;
@@ -243,16 +356,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           mma_commit(&s_full[x]);
         }
         __syncwarp();
+        if (lane == 0) ktrace(p, c, 0);
       }
       if (prev) {
         const int x = (c - 1) & 1;
         mbar_wait_sleep(&ds_full[x], ((c - 1) >> 1) & 1, 64);
+        if (lane == 0) ktrace(p, c - 1, 1);
         if (prev_first) mbar_wait_sleep(acc_free, (tiles_done & 1) ^ 1, 64);
+        if (lane == 0) ktrace(p, c - 1, 2);
         tc_fence_after();
         const uint32_t q_addr = smem_u32(smem + prev_stage * C::STAGE_BYTES);
         const uint32_t do_addr = q_addr + C::Q_BYTES;
         if (elect_one()) {
-#pragma unroll 1
+#pragma unroll
           for (int ks = 0; ks < kNCH / 16; ++ks)
 #pragma unroll
             for (int sb = 0; sb < 2; ++sb) {
@@ -291,7 +407,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int grp = (warp - 2) >> 2;
     const int quarter = warp & 3;
     const int half = lane >> 4, r = (lane >> 2) & 3, cc = lane & 3;
-    const int gtid = threadIdx.x - 64 - grp * 128;
     const int Lh = wlen(p.H, L), Lw = wlen(p.W, L);
     const uint32_t lane_q = tmem + ((uint32_t)(quarter * 32) << 16);
     const float sl2 = p.scale * log2e;
@@ -314,16 +429,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool kvalid = pk < kv_end && qk < p.W;
       // union columns of this quarter's key block (warp-uniform), loaded as UCW columns from an even
       // origin clamped so the load stays inside the QP-wide halo row
-      const int uc = min((inv_lo(min(g.kc0 + 4 * quarter, p.W - 1), p.W, L, 0, p.W) - g.qc0) & ~1, QP - C::UCW);
+      const int ucr = (inv_lo(min(g.kc0 + 4 * quarter, p.W - 1), p.W, L, 0, p.W) - g.qc0) & ~1;
+      // interior quarters (all union columns of class NS, UCWF wide) take the immediate-offset path
+      const bool fast = L < p.W && g.qc0 + ucr >= C::NS && g.qc0 + ucr + C::UCWF - 1 < p.W - C::NS &&
+                        ucr + C::UCWF <= QP;
+      const int uc = fast ? ucr : min(ucr, QP - C::UCW);
       const float *lsd = (const float *)(smem + stage * C::STAGE_BYTES + 2 * C::Q_BYTES + 2 * C::KT_BYTES);
       // per union column: table class offset (column-clamp class of the query, or the -inf class)
+      const int jb = g.qc0 + uc;
       int colterm[C::UCW];
 #pragma unroll
       for (int z = 0; z < C::UCW; ++z) {
-        const int j = g.qc0 + uc + z;
+        const int j = jb + z;
         const int dcl = j < p.W ? wstart(j, p.W, L) - j + L - 1 : L;
         colterm[z] = dcl * C::TROWS * kTblStride - j;
       }
+      const float *tbl_row0 = tbl + kTblOff + qk + L - 1 + (fast ? C::NS * C::TROWS * kTblStride - jb : 0);
       const int nch = g.nchunks;
       bool first_wait = true;
       for (int k = 0; k < nch; ++k, ++c) {
@@ -333,61 +454,29 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&full[stage], (it / kStages) & 1);  // LSE / D staging visible
           first_wait = false;
         }
+        const bool trq = quarter == 2 && lane == 0;
+        if (trq) ktrace(p, c, 4);
         mbar_wait(&s_full[x], (c >> 1) & 1);
+        if (trq) ktrace(p, c, 5);
         tc_fence_after();
         const int i_base = g.qs_lo[half] + C::CR * k;  // query row of chunk row 0 (this half)
-        const int rows_here = g.qs_n[half] - C::CR * k;
+        const int rows_here = min(g.qs_n[half] - C::CR * k, q_end - i_base);
+        const float *lrow0 = lsd + (i_base - g.qr0) * C::LP + (g.qc0 & 3) + uc;
         const uint32_t lane_addr = lane_q + x * kSlot;
-#pragma unroll 1
-        for (int u = 0; u < C::CR; ++u) {
-          uint32_t sv[16], dpv[16];
-          const uint32_t ca = lane_addr + u * QP + uc;
-          tmem_ld16(ca, sv);
-          tmem_ld16(ca + kNCH, dpv);
-          const int i = i_base + u;
-          // row validity: i in the band, inside this half's query rows, and key row in window(i)
-          const int a = pk - i + L - 1;
-          const int dri = (i >= p.q_row0 && i < q_end) ? wstart(i, p.H, L) - i + L - 1 : -1000;
-          const bool rv = u < rows_here && (unsigned)(a - dri) < (unsigned)Lh;
-          const float *trow = tbl + (rv ? a : C::TT) * kTblStride + kTblOff + qk + L - 1;
-          const float *lrow = lsd + (i - g.qr0) * QP + uc;
-          tc_wait_ld();
-          uint32_t pp[C::UCW / 2], dd[C::UCW / 2];
-#pragma unroll
-          for (int z = 0; z < C::UCW; z += 2) {
-            float pe[2], de[2];
-#pragma unroll
-            for (int y = 0; y < 2; ++y) {
-              const float xv = fmaf(__uint_as_float(sv[z + y]), sl2, trow[colterm[z + y]]);
-              const float P = ex2(xv - lrow[z + y]);
-              pe[y] = P;
-              de[y] = P * (__uint_as_float(dpv[z + y]) - lrow[C::LD_FLOATS + z + y]);
-            }
-            pp[z / 2] = pack_bf16_alu(pe[0], pe[1]);
-            dd[z / 2] = pack_bf16_alu(de[0], de[1]);
-          }
-          const uint32_t prow = lane_addr + u * (QP / 2);
-          const uint32_t drow = prow + kNCH;
-          if constexpr (QP == 24) {
-            st_zero12(prow);
-            st_zero12(drow);
-          } else {
-            st_zero12(prow);
-            st_zero12(drow);
-            const uint32_t z4[4] = {0, 0, 0, 0};
-            tmem_st4(prow + 12, z4);
-            tmem_st4(drow + 12, z4);
-          }
-          st_row<C::UCW / 2>(prow + uc / 2, pp);
-          st_row<C::UCW / 2>(drow + uc / 2, dd);
-        }
+        if (fast)
+          chunk_rows<L, QP, true>(lane_addr, uc, tbl_row0, colterm, lrow0, pk, i_base, p.H, rows_here, Lh, sl2);
+        else
+          chunk_rows<L, QP, false>(lane_addr, uc, tbl_row0, colterm, lrow0, pk, i_base, p.H, rows_here, Lh, sl2);
         tc_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&ds_full[x]);
+        if (trq) ktrace(p, c, 6);
+        if (lane == 0) ktrace(p, c, 10 + quarter);
         if (k == nch - 1) {
           // ---- epilogue of the tile: dV, dK (scale) from the partial accumulators
           mbar_wait(acc_full, tile_count & 1);
+          if (trq) ktrace(p, c, 7);
           tc_fence_after();
           uint32_t a0[32], a1[32];
           tmem_ld32(lane_q + kDV_COL, a0);
@@ -404,6 +493,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(acc_free);
+          if (trq) ktrace(p, c, 8);
           if (kvalid) {
             const size_t ki = ((size_t)g.bh * p.kv_rows + (pk - p.kv_row0)) * p.W + qk;
             uint4 *dv = (uint4 *)(p.dv + ki * kD), *dk = (uint4 *)(p.dk + ki * kD);
@@ -421,6 +511,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                   pack_bf16((__uint_as_float(a0[z + 6]) + __uint_as_float(a1[z + 6])) * p.scale,
                             (__uint_as_float(a0[z + 7]) + __uint_as_float(a1[z + 7])) * p.scale));
           }
+          if (trq) ktrace(p, c, 9);
         }
       }
       // the group that did not take the tile's last chunk still tracks the tile count
@@ -452,7 +543,12 @@ cudaError_t launch_dkdv_t(const Geo &g, const void *q, const void *k, const void
       !make_tmap_bf16_4d(&tk, k, kD, g.W, g.kv_rows, BH, 4, 4) ||
       !make_tmap_bf16_4d(&tv, v, kD, g.W, g.kv_rows, BH, 4, 4))
     return cudaErrorInvalidValue;
+  CUtensorMap tl, td;
+  const bool tma_lsd = (g.W * 4) % 16 == 0 && make_tmap_f32_3d(&tl, lse, g.W, g.q_rows, BH, C::LP, C::QRH) &&
+                       make_tmap_f32_3d(&td, D, g.W, g.q_rows, BH, C::LP, C::QRH);
+  if (!tma_lsd) tl = td = tq;  // unused
   BwdKParams p;
+  p.tma_lsd = tma_lsd ? 1 : 0;
   p.B = g.B;
   p.heads = g.heads;
   p.H = g.H;
@@ -470,9 +566,10 @@ cudaError_t launch_dkdv_t(const Geo &g, const void *q, const void *k, const void
   p.D = D;
   p.dk = (__nv_bfloat16 *)dk;
   p.dv = (__nv_bfloat16 *)dv;
+  p.trace = (long long *)debug_trace_buffer();
   const int grid = p.num_tiles < tc::num_sms() ? p.num_tiles : tc::num_sms();
   ProfScope ps("na2d_bwd_dkdv_tc", st);
-  na2d_bwd_dkdv_kernel<L, QP><<<grid, kThreads, C::SMEM, st>>>(tq, tdo, tk, tv, p);
+  na2d_bwd_dkdv_kernel<L, QP><<<grid, kThreads, C::SMEM, st>>>(tq, tdo, tk, tv, tl, td, p);
   return cudaGetLastError();
 }
 
@@ -492,7 +589,7 @@ int max_query_halo_width(const Geo &g) {
   int w = 0;
   for (int c0 = 0; c0 < W; c0 += tc::kTQW) {
     const int c1 = c0 + tc::kTQW - 1 < W - 1 ? c0 + tc::kTQW - 1 : W - 1;
-    const int ww = hi(c1) - lo(c0) + 1;
+    const int ww = hi(c1) - (lo(c0) & ~1) + 1;  // the kernel rounds the halo origin down to even
     w = ww > w ? ww : w;
   }
   return w;

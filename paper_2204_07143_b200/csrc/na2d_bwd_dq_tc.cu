@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait_sleep(ds_full, ph, 64);
       tc_fence_after();
       if (elect_one()) {
-#pragma unroll 1
+#pragma unroll
         for (int ks = 0; ks < C::NSUB / 16; ++ks)
 #pragma unroll
           for (int sb = 0; sb < 2; ++sb) {
@@ -361,13 +361,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// drpb[h][c] = sum over CTAs (fixed order) of drpb_part[cta][h][c]
+// drpb[h][c] = sum over CTAs of drpb_part[cta][h][c]: one warp per cell, lane l sums CTAs
+// l, l+32, ... in order, then a fixed butterfly -- deterministic for a given CTA count.
 __global__ void drpb_reduce_kernel(const float *__restrict__ part, int ctas, int n, float *__restrict__ drpb) {
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (int b = 0; b < ctas; ++b) s += part[(size_t)b * n + e];
-    drpb[e] = s;
-  }
+  const int e = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (e >= n) return;
+  float s = 0.f;
+  for (int b = lane; b < ctas; b += 32) s += part[(size_t)b * n + e];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) drpb[e] = s;
 }
 
 template <int L>
@@ -421,7 +424,7 @@ cudaError_t launch_dq(const Geo &g, const void *q, const void *k, const void *v,
   {
     ProfScope ps("na2d_bwd_drpb_reduce", st);
     const int n = g.heads * TT * TT;
-    drpb_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(part, grid, n, drpb);
+    drpb_reduce_kernel<<<(n + 3) / 4, 128, 0, st>>>(part, grid, n, drpb);
   }
   return cudaGetLastError();
 }

@@ -370,3 +370,20 @@ def test_inputs_are_bf16_and_sliceable():
     x = np.array([1 + 2 ** -8, 1 + 3 * 2 ** -8, -2.5], np.float32)
     np.testing.assert_array_equal(bf16_round(x), np.array([1.0, 1 + 2 ** -6, -2.5], np.float32))
     assert bf16_bits(np.array([1.0], np.float32))[0] == 0x3F80
+
+
+@pytest.mark.parametrize("L", [3, 5, 7, 9])
+def test_inverse_neighbourhood_closed_form(oracle_lib, L):
+    """The kernels' closed-form inverse neighbourhood (first/last query whose clamped window holds
+    a key) equals brute-force enumeration over the oracle's windows, incl. bands [lo, hi)."""
+    ns = (L - 1) // 2
+    for n in range(1, 45):
+        for lo, hi in [(0, n), (min(2, n - 1), n), (0, max(1, n - 3))]:
+            for p in range(n):
+                qs = [i for i in range(lo, hi) if oracle.window_start(i, n, L) <= p < oracle.window_start(i, n, L) + oracle.window_len(n, L)]
+                cl = lo if (L >= n or p < L) else max(lo, p - ns)
+                ch = hi - 1 if (L >= n or p >= n - L) else min(hi - 1, p + ns)
+                if qs:
+                    assert (cl, ch) == (qs[0], qs[-1]), (n, L, p, lo, hi)
+                else:
+                    assert cl > ch or not any(lo <= i < hi for i in range(cl, ch + 1)), (n, L, p, lo, hi)
