@@ -36,7 +36,8 @@ constexpr int kStages = 2;
 constexpr int kThreads = 320;  // warp 0 producer, warp 1 MMA, warps 2-5 / 6-9 elementwise groups
 constexpr int kNCH = 96;       // queries per chunk (N of the S^T / dP^T MMAs)
 constexpr int kSlot = 192;     // TMEM columns per chunk slot: S^T [0,96), dP^T [96,192)
-constexpr int kDV_COL = 384, kDK_COL = 448;  // 2 partial accumulators each
+constexpr int kACC_COL = 384;  // dV / dK accumulators: buffer b at 384 + 64b (dV), + 32 (dK)
+constexpr int kTileInfoBytes = 512;
 
 template <int L, int QP>
 struct CfgK {
@@ -61,9 +62,12 @@ struct CfgK {
   static constexpr int TROWS = TT + 1;
   static constexpr int TBL_FLOATS = (L + 1) * TROWS * kTblStride;  // + all -inf class (OOB columns)
   static constexpr int TBL_OFF = kStages * STAGE_BYTES;
-  static constexpr int BAR_OFF = TBL_OFF + TBL_FLOATS * 4;
+  // dV / dK output staging: 2 groups x 4 warps x 4 KB (SW64 boxes, 1 KB aligned)
+  static constexpr int OUT_OFF = (TBL_OFF + TBL_FLOATS * 4 + 1023) / 1024 * 1024;
+  static constexpr int TI_OFF = OUT_OFF + 8 * 4096;
+  static constexpr int BAR_OFF = TI_OFF + kStages * kTileInfoBytes;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
-  static constexpr int MAX_CHUNKS = (4 + 3 * NS + CR - 1) / CR;
+  static_assert(SMEM <= 232448, "shared memory");
 };
 
 struct BwdKParams {
@@ -75,9 +79,9 @@ struct BwdKParams {
   __nv_bfloat16 *dk, *dv;
   long long *trace;
 };
-// debug timeline: trace[(cta * 32 + chunk) * 16 + ev] for CTAs < 4 (chunk = CTA-global chunk index)
+// debug timeline: trace[(cta * 32 + chunk) * 32 + ev] for CTAs < 4 (chunk = CTA-global chunk index)
 __device__ __forceinline__ void ktrace(const BwdKParams &p, int c, int ev) {
-  if (p.trace && blockIdx.x < 4 && c < 32) p.trace[((size_t)blockIdx.x * 32 + c) * 16 + ev] = clock64();
+  if (p.trace && blockIdx.x < 4 && c < 32) p.trace[((size_t)blockIdx.x * 32 + c) * 32 + ev] = clock64();
 }
 
 // first / last query row (column) in [lo, hi) whose clamped window holds key row (column) p.
@@ -183,36 +187,44 @@ __device__ __forceinline__ void chunk_rows(uint32_t lane_addr, int uc, const flo
       const uint32_t drow = prow + kNCH;
       st_zero12(prow);
       st_zero12(drow);
-      if constexpr (QP == 32) {
-        const uint32_t z4[4] = {0, 0, 0, 0};
-        tmem_st4(prow + 12, z4);
-        tmem_st4(drow + 12, z4);
-      }
+      static_assert(QP == 24, "zero fill covers 12 bf16-pair columns");
       st_row<UW / 2>(prow + uc / 2, pp);
       st_row<UW / 2>(drow + uc / 2, dd);
     }
   }
 }
 
+// Per-stage tile description, written by the producer warp before it arms full[stage] (so the MMA
+// and elementwise warps only read it): the key tile, its query halo and per lane-quarter union.
+struct TileInfo {
+  int bh, kr0, kc0, qr0, qc0, nchunks, head, pad;
+  int qs_lo[2], qs_n[2];
+  int uc[4], fast[4];
+  int colterm[4][16];  // per union column: bias-table class offset (slow path)
+};
+static_assert(sizeof(TileInfo) <= kTileInfoBytes, "TileInfo size");
+
 template <int L, int QP>
 __global__ void __launch_bounds__(kThreads, 1)
     na2d_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                          const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                          const __grid_constant__ CUtensorMap tm_lse, const __grid_constant__ CUtensorMap tm_d,
+                         const __grid_constant__ CUtensorMap tm_dk, const __grid_constant__ CUtensorMap tm_dv,
                          const BwdKParams p) {
   using C = CfgK<L, QP>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   float *tbl = (float *)(smem + C::TBL_OFF);
+  TileInfo *tinfo = (TileInfo *)(smem + C::TI_OFF);
   uint64_t *bars = (uint64_t *)(smem + C::BAR_OFF);
   uint64_t *full = bars, *empty = bars + kStages;
-  uint64_t *s_full = bars + 2 * kStages, *ds_full = s_full + 2, *acc_full = s_full + 4, *acc_free = s_full + 5;
-  uint32_t *tmem_slot = (uint32_t *)(bars + 2 * kStages + 6);
+  uint64_t *s_full = bars + 2 * kStages, *ds_full = s_full + 2, *acc_full = s_full + 4, *acc_free = s_full + 6;
+  uint32_t *tmem_slot = (uint32_t *)(bars + 2 * kStages + 8);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int t_begin = (int)((long)p.num_tiles * blockIdx.x / gridDim.x);
   const int t_end = (int)((long)p.num_tiles * (blockIdx.x + 1) / gridDim.x);
-  const int q_end = p.q_row0 + p.q_rows, kv_end = p.kv_row0 + p.kv_rows;
+  const int q_end = p.q_row0 + p.q_rows;
 
   // zero the never-loaded tail rows of the Q / dO halos (read by partial chunks)
   for (int s = 0; s < kStages; ++s)
@@ -232,14 +244,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], p.tma_lsd ? 1 : 1 + 32);  // expect_tx arrive (+ 32 lanes staging LSE / D)
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], 1 + 8);                  // MMA commit + the 8 elementwise warps
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&s_full[s], 1);
       mbar_init(&ds_full[s], 4);
+      mbar_init(&acc_full[s], 1);
+      mbar_init(&acc_free[s], 4);
     }
-    mbar_init(acc_full, 1);
-    mbar_init(acc_free, 4);
     fence_barrier_init();
     tma_prefetch(&tm_q);
     tma_prefetch(&tm_do);
@@ -258,13 +270,44 @@ __global__ void __launch_bounds__(kThreads, 1)
   const float log2e = 1.4426950408889634f;
 
   if (warp == 0) {
-    // ================= producer: TMA (K, V sub-tile blocks; Q, dO halos) + LSE / D halos
+    // ================= producer: tile description, TMA (K, V sub-tile blocks; Q, dO halos) + LSE / D
     int it = 0;
     for (int t = t_begin; t < t_end; ++t, ++it) {
       const int s = it % kStages;
       mbar_wait_sleep(&empty[s], ((it / kStages) & 1) ^ 1, 1024);
       if (lane == 0) ktrace(p, it, 14);
       const KTile g = ktile<L, QP>(p, t);
+      TileInfo *ti = tinfo + s;
+      if (lane < 4) {  // union origin of lane quarter q = lane (warp-uniform in the consumers)
+        const int ucr = (inv_lo(min(g.kc0 + 4 * lane, p.W - 1), p.W, L, 0, p.W) - g.qc0) & ~1;
+        // interior quarters (all union columns of class NS, UCWF wide) take the immediate-offset path
+        const bool fast = L < p.W && g.qc0 + ucr >= C::NS && g.qc0 + ucr + C::UCWF - 1 < p.W - C::NS &&
+                          ucr + C::UCWF <= QP;
+        ti->uc[lane] = fast ? ucr : min(ucr, QP - C::UCW);
+        ti->fast[lane] = fast;
+      }
+      if (lane == 0) {
+        ti->bh = g.bh;
+        ti->kr0 = g.kr0;
+        ti->kc0 = g.kc0;
+        ti->qr0 = g.qr0;
+        ti->qc0 = g.qc0;
+        ti->nchunks = g.nchunks;
+        ti->head = g.bh % p.heads;
+        ti->qs_lo[0] = g.qs_lo[0];
+        ti->qs_lo[1] = g.qs_lo[1];
+        ti->qs_n[0] = g.qs_n[0];
+        ti->qs_n[1] = g.qs_n[1];
+      }
+      __syncwarp();
+#pragma unroll
+      for (int e = lane; e < 64; e += 32) {  // class offset of union column z of quarter q
+        const int q = e >> 4, z = e & 15;
+        const int j = g.qc0 + ti->uc[q] + z;
+        const int dcl = j < p.W ? wstart(j, p.W, L) - j + L - 1 : L;
+        ti->colterm[q][z] = dcl * C::TROWS * kTblStride - j;
+      }
+      __syncwarp();
       uint8_t *st = smem + s * C::STAGE_BYTES;
       float *lsd = (float *)(st + 2 * C::Q_BYTES + 2 * C::KT_BYTES);
       if (elect_one()) {
@@ -311,22 +354,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             lsd[C::LD_FLOATS + e] = dv[u];
           }
         }
+        mbar_arrive(&full[s]);
       }
       if (lane == 0) ktrace(p, it, 15);
-      if (!p.tma_lsd) mbar_arrive(&full[s]);
     }
   } else if (warp == 1) {
     // ================= MMA issuer: S^T/dP^T of chunk c, then dV/dK of chunk c-1 (in-order tensor
-    // core => a chunk slot is rewritten only after the dV/dK MMAs that read it)
+    // core => a chunk slot is rewritten only after the dV/dK MMAs that read it).  dV/dK accumulate
+    // in TMEM buffer (tile & 1), so a tile's MMAs never wait for the previous tile's epilogue.
     constexpr uint32_t idesc_s = idesc_bf16(64, kNCH, false);
     constexpr uint32_t idesc_o = idesc_bf16(64, kD, true);
     const int ntiles = t_end - t_begin;
-    int it = 0, k = 0, c = 0, tiles_done = 0;
-    KTile g{};
-    if (ntiles > 0) g = ktile<L, QP>(p, t_begin);
+    int it = 0, k = 0, c = 0;
+    int nch = 1, row0[2] = {0, 0};  // current tile: chunks, first halo row of each sub-tile
     bool prev = false, prev_first = false, prev_last = false;
-    int prev_stage = 0, prev_k = 0;
-    KTile pg{};
+    int prev_stage = 0, prev_it = 0, prev_row[2] = {0, 0};
     for (;;) {
       const bool have = it < ntiles;
       const int stage = it % kStages;
@@ -335,6 +377,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait_sleep(&full[stage], (it / kStages) & 1, 64);
           if (lane == 0) ktrace(p, c, 3);
           tc_fence_after();
+          const TileInfo &ti = tinfo[stage];
+          nch = ti.nchunks;
+          row0[0] = ti.qs_lo[0] - ti.qr0;
+          row0[1] = ti.qs_lo[1] - ti.qr0;
         }
         const int x = c & 1;
         const uint32_t q_addr = smem_u32(smem + stage * C::STAGE_BYTES);
@@ -347,7 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int sb = 0; sb < 2; ++sb) {
               const uint32_t lo = ((uint32_t)(16 * sb) << 16) + x * kSlot;
-              const int row = g.qs_lo[sb] - g.qr0 + C::CR * k;
+              const int row = row0[sb] + C::CR * k;
               mma_ss(tmem + lo, sdesc_sw64(k_addr + sb * 4096 + kk * 32),
                      sdesc_sw64(q_addr + row * QP * kRowBytes + kk * 32), idesc_s, kk);
               mma_ss(tmem + lo + kNCH, sdesc_sw64(v_addr + sb * 4096 + kk * 32),
@@ -359,10 +405,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) ktrace(p, c, 0);
       }
       if (prev) {
-        const int x = (c - 1) & 1;
+        const int x = (c - 1) & 1, b = prev_it & 1;
         mbar_wait_sleep(&ds_full[x], ((c - 1) >> 1) & 1, 64);
         if (lane == 0) ktrace(p, c - 1, 1);
-        if (prev_first) mbar_wait_sleep(acc_free, (tiles_done & 1) ^ 1, 64);
+        if (prev_first) mbar_wait_sleep(&acc_free[b], ((prev_it >> 1) & 1) ^ 1, 64);
         if (lane == 0) ktrace(p, c - 1, 2);
         tc_fence_after();
         const uint32_t q_addr = smem_u32(smem + prev_stage * C::STAGE_BYTES);
@@ -373,33 +419,33 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int sb = 0; sb < 2; ++sb) {
               const uint32_t lo = (uint32_t)(16 * sb) << 16;
-              const int row = pg.qs_lo[sb] - pg.qr0 + C::CR * prev_k;
+              const int row = prev_row[sb];
               const uint32_t b_off = row * QP * kRowBytes + ks * 16 * kRowBytes;
-              const uint32_t acc = (prev_first && ks < 2) ? 0u : 1u;
-              mma_ts(tmem + lo + kDV_COL + (ks & 1) * kD, tmem + lo + x * kSlot + ks * 8,
+              const uint32_t acc = (prev_first && ks == 0) ? 0u : 1u;
+              mma_ts(tmem + lo + kACC_COL + b * 2 * kD, tmem + lo + x * kSlot + ks * 8,
                      sdesc_sw64(do_addr + b_off), idesc_o, acc);
-              mma_ts(tmem + lo + kDK_COL + (ks & 1) * kD, tmem + lo + x * kSlot + kNCH + ks * 8,
+              mma_ts(tmem + lo + kACC_COL + b * 2 * kD + kD, tmem + lo + x * kSlot + kNCH + ks * 8,
                      sdesc_sw64(q_addr + b_off), idesc_o, acc);
             }
           if (prev_last) {
-            mma_commit(acc_full);
+            mma_commit(&acc_full[b]);
             mma_commit(&empty[prev_stage]);
           }
         }
         __syncwarp();
-        if (prev_last) ++tiles_done;
       }
       if (!have) break;
       prev = true;
       prev_first = k == 0;
-      prev_last = k == g.nchunks - 1;
+      prev_last = k == nch - 1;
       prev_stage = stage;
-      prev_k = k;
-      pg = g;
+      prev_it = it;
+      prev_row[0] = row0[0] + C::CR * k;
+      prev_row[1] = row0[1] + C::CR * k;
       ++c;
-      if (++k == g.nchunks) {
+      if (++k == nch) {
         k = 0;
-        if (++it < ntiles) g = ktile<L, QP>(p, t_begin + it);
+        ++it;
       }
     }
   } else {
@@ -410,12 +456,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int Lh = wlen(p.H, L), Lw = wlen(p.W, L);
     const uint32_t lane_q = tmem + ((uint32_t)(quarter * 32) << 16);
     const float sl2 = p.scale * log2e;
+    // output staging of this warp (dV, dK: two 4x4-key blocks each, SW64 layout of the TMA store)
+    uint8_t *ostage = smem + C::OUT_OFF + (grp * 4 + quarter) * 4096;
+    const bool trq = quarter == 2 && lane == 0;
     int cur_head = -1;
-    int c = 0, tile_count = 0;
+    int c = 0;
     for (int t = t_begin; t < t_end; ++t) {
       const int it = t - t_begin, stage = it % kStages;
-      const KTile g = ktile<L, QP>(p, t);
-      const int h = g.bh % p.heads;
+      mbar_wait(&full[stage], (it / kStages) & 1);  // tile description, LSE / D staged
+      if (trq) ktrace(p, c, 16 + 4 * grp);
+      const TileInfo &ti = tinfo[stage];
+      const int h = ti.head, bh = ti.bh, kr0 = ti.kr0, kc0 = ti.kc0, qr0 = ti.qr0, qc0 = ti.qc0;
+      const int nch = ti.nchunks, qs_lo = ti.qs_lo[half], qs_n = ti.qs_n[half];
+      const int uc = ti.uc[quarter];
+      const bool fast = ti.fast[quarter];
+      int colterm[C::UCW];
+#pragma unroll
+      for (int z = 0; z < C::UCW; ++z) colterm[z] = ti.colterm[quarter][z];
       if (h != cur_head) {  // both groups rebuild the shared table: sync all 256 threads
         named_bar_sync(1, 256);
         const int tid256 = threadIdx.x - 64;
@@ -424,44 +481,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         named_bar_sync(1, 256);
         cur_head = h;
       }
-      // this thread's key and geometry
-      const int pk = g.kr0 + 4 * half + r, qk = g.kc0 + 4 * quarter + cc;
-      const bool kvalid = pk < kv_end && qk < p.W;
-      // union columns of this quarter's key block (warp-uniform), loaded as UCW columns from an even
-      // origin clamped so the load stays inside the QP-wide halo row
-      const int ucr = (inv_lo(min(g.kc0 + 4 * quarter, p.W - 1), p.W, L, 0, p.W) - g.qc0) & ~1;
-      // interior quarters (all union columns of class NS, UCWF wide) take the immediate-offset path
-      const bool fast = L < p.W && g.qc0 + ucr >= C::NS && g.qc0 + ucr + C::UCWF - 1 < p.W - C::NS &&
-                        ucr + C::UCWF <= QP;
-      const int uc = fast ? ucr : min(ucr, QP - C::UCW);
+      // this thread's key
+      const int pk = kr0 + 4 * half + r, qk = kc0 + 4 * quarter + cc;
       const float *lsd = (const float *)(smem + stage * C::STAGE_BYTES + 2 * C::Q_BYTES + 2 * C::KT_BYTES);
-      // per union column: table class offset (column-clamp class of the query, or the -inf class)
-      const int jb = g.qc0 + uc;
-      int colterm[C::UCW];
-#pragma unroll
-      for (int z = 0; z < C::UCW; ++z) {
-        const int j = jb + z;
-        const int dcl = j < p.W ? wstart(j, p.W, L) - j + L - 1 : L;
-        colterm[z] = dcl * C::TROWS * kTblStride - j;
-      }
-      const float *tbl_row0 = tbl + kTblOff + qk + L - 1 + (fast ? C::NS * C::TROWS * kTblStride - jb : 0);
-      const int nch = g.nchunks;
-      bool first_wait = true;
+      const float *tbl_row0 = tbl + kTblOff + qk + L - 1 + (fast ? C::NS * C::TROWS * kTblStride - (qc0 + uc) : 0);
+      if (trq) ktrace(p, c, 17 + 4 * grp);
+      bool last_mine = false;
       for (int k = 0; k < nch; ++k, ++c) {
         if ((c & 1) != grp) continue;
         const int x = c & 1;
-        if (first_wait) {
-          mbar_wait(&full[stage], (it / kStages) & 1);  // LSE / D staging visible
-          first_wait = false;
-        }
-        const bool trq = quarter == 2 && lane == 0;
         if (trq) ktrace(p, c, 4);
         mbar_wait(&s_full[x], (c >> 1) & 1);
         if (trq) ktrace(p, c, 5);
         tc_fence_after();
-        const int i_base = g.qs_lo[half] + C::CR * k;  // query row of chunk row 0 (this half)
-        const int rows_here = min(g.qs_n[half] - C::CR * k, q_end - i_base);
-        const float *lrow0 = lsd + (i_base - g.qr0) * C::LP + (g.qc0 & 3) + uc;
+        const int i_base = qs_lo + C::CR * k;  // query row of chunk row 0 (this half)
+        const int rows_here = min(qs_n - C::CR * k, q_end - i_base);
+        const float *lrow0 = lsd + (i_base - qr0) * C::LP + (qc0 & 3) + uc;
         const uint32_t lane_addr = lane_q + x * kSlot;
         if (fast)
           chunk_rows<L, QP, true>(lane_addr, uc, tbl_row0, colterm, lrow0, pk, i_base, p.H, rows_here, Lh, sl2);
@@ -473,50 +508,57 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive(&ds_full[x]);
         if (trq) ktrace(p, c, 6);
         if (lane == 0) ktrace(p, c, 10 + quarter);
-        if (k == nch - 1) {
-          // ---- epilogue of the tile: dV, dK (scale) from the partial accumulators
-          mbar_wait(acc_full, tile_count & 1);
-          if (trq) ktrace(p, c, 7);
-          tc_fence_after();
-          uint32_t a0[32], a1[32];
-          tmem_ld32(lane_q + kDV_COL, a0);
-          tmem_ld32(lane_q + kDV_COL + kD, a1);
-          tc_wait_ld();
-          uint32_t ov[16];
-#pragma unroll
-          for (int z = 0; z < 32; z += 2)
-            ov[z / 2] = pack_bf16(__uint_as_float(a0[z]) + __uint_as_float(a1[z]),
-                                  __uint_as_float(a0[z + 1]) + __uint_as_float(a1[z + 1]));
-          tmem_ld32(lane_q + kDK_COL, a0);
-          tmem_ld32(lane_q + kDK_COL + kD, a1);
-          tc_wait_ld();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(acc_free);
-          if (trq) ktrace(p, c, 8);
-          if (kvalid) {
-            const size_t ki = ((size_t)g.bh * p.kv_rows + (pk - p.kv_row0)) * p.W + qk;
-            uint4 *dv = (uint4 *)(p.dv + ki * kD), *dk = (uint4 *)(p.dk + ki * kD);
-#pragma unroll
-            for (int z = 0; z < 4; ++z) dv[z] = make_uint4(ov[4 * z], ov[4 * z + 1], ov[4 * z + 2], ov[4 * z + 3]);
-#pragma unroll
-            for (int z = 0; z < 32; z += 8)
-              dk[z / 8] = make_uint4(
-                  pack_bf16((__uint_as_float(a0[z]) + __uint_as_float(a1[z])) * p.scale,
-                            (__uint_as_float(a0[z + 1]) + __uint_as_float(a1[z + 1])) * p.scale),
-                  pack_bf16((__uint_as_float(a0[z + 2]) + __uint_as_float(a1[z + 2])) * p.scale,
-                            (__uint_as_float(a0[z + 3]) + __uint_as_float(a1[z + 3])) * p.scale),
-                  pack_bf16((__uint_as_float(a0[z + 4]) + __uint_as_float(a1[z + 4])) * p.scale,
-                            (__uint_as_float(a0[z + 5]) + __uint_as_float(a1[z + 5])) * p.scale),
-                  pack_bf16((__uint_as_float(a0[z + 6]) + __uint_as_float(a1[z + 6])) * p.scale,
-                            (__uint_as_float(a0[z + 7]) + __uint_as_float(a1[z + 7])) * p.scale));
-          }
-          if (trq) ktrace(p, c, 9);
-        }
+        last_mine = k == nch - 1;
       }
-      // the group that did not take the tile's last chunk still tracks the tile count
-      ++tile_count;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);  // done with this stage's LSE / D and TileInfo
+      if (last_mine) {
+        // ---- epilogue of the tile: dV, dK (scale) from accumulator buffer b, TMA-stored via smem
+        const int b = it & 1, cl = c - 1;
+        mbar_wait(&acc_full[b], (it >> 1) & 1);
+        if (trq) ktrace(p, cl, 7);
+        tc_fence_after();
+        uint32_t a0[32], a1[32];
+        tmem_ld32(lane_q + kACC_COL + b * 2 * kD, a0);
+        tmem_ld32(lane_q + kACC_COL + b * 2 * kD + kD, a1);
+        tc_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_free[b]);
+        if (trq) ktrace(p, cl, 8);
+        if (lane == 0) bulk_wait_read0();  // this warp's previous stores have left the staging
+        __syncwarp();
+        // key (r, cc) of block `half` is row R of the 1 KB box; SW64: 16-byte chunk z at z ^ (R/2 % 4)
+        const int R = r * 4 + cc;
+        uint8_t *rv = ostage + half * 1024 + R * 64, *rk = rv + 2048;
+#pragma unroll
+        for (int z = 0; z < 4; ++z) {
+          const int zz = (z ^ (R >> 1)) & 3;
+          *(uint4 *)(rv + 16 * zz) = make_uint4(
+              pack_bf16(__uint_as_float(a0[8 * z]), __uint_as_float(a0[8 * z + 1])),
+              pack_bf16(__uint_as_float(a0[8 * z + 2]), __uint_as_float(a0[8 * z + 3])),
+              pack_bf16(__uint_as_float(a0[8 * z + 4]), __uint_as_float(a0[8 * z + 5])),
+              pack_bf16(__uint_as_float(a0[8 * z + 6]), __uint_as_float(a0[8 * z + 7])));
+          *(uint4 *)(rk + 16 * zz) = make_uint4(
+              pack_bf16(__uint_as_float(a1[8 * z]) * p.scale, __uint_as_float(a1[8 * z + 1]) * p.scale),
+              pack_bf16(__uint_as_float(a1[8 * z + 2]) * p.scale, __uint_as_float(a1[8 * z + 3]) * p.scale),
+              pack_bf16(__uint_as_float(a1[8 * z + 4]) * p.scale, __uint_as_float(a1[8 * z + 5]) * p.scale),
+              pack_bf16(__uint_as_float(a1[8 * z + 6]) * p.scale, __uint_as_float(a1[8 * z + 7]) * p.scale));
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {  // out-of-range keys (map / band edge) are clipped by the TMA unit
+#pragma unroll
+          for (int sb = 0; sb < 2; ++sb) {
+            tma_store_4d(&tm_dv, ostage + sb * 1024, 0, kc0 + 4 * quarter, kr0 - p.kv_row0 + 4 * sb, bh);
+            tma_store_4d(&tm_dk, ostage + 2048 + sb * 1024, 0, kc0 + 4 * quarter, kr0 - p.kv_row0 + 4 * sb, bh);
+          }
+          bulk_commit();
+        }
+        if (trq) ktrace(p, cl, 9);
+      }
     }
+    if (lane == 0) bulk_wait0();
   }
   __syncthreads();
   if (warp == 0) {
@@ -536,12 +578,14 @@ cudaError_t launch_dkdv_t(const Geo &g, const void *q, const void *k, const void
         cudaFuncSetAttribute(na2d_bwd_dkdv_kernel<L, QP>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   });
   if (attr_err != cudaSuccess) return attr_err;
-  CUtensorMap tq, tdo, tk, tv;
+  CUtensorMap tq, tdo, tk, tv, tdk, tdv;
   const int BH = g.B * g.heads;
   if (!make_tmap_bf16_4d(&tq, q, kD, g.W, g.q_rows, BH, QP, C::QRH) ||
       !make_tmap_bf16_4d(&tdo, dout, kD, g.W, g.q_rows, BH, QP, C::QRH) ||
       !make_tmap_bf16_4d(&tk, k, kD, g.W, g.kv_rows, BH, 4, 4) ||
-      !make_tmap_bf16_4d(&tv, v, kD, g.W, g.kv_rows, BH, 4, 4))
+      !make_tmap_bf16_4d(&tv, v, kD, g.W, g.kv_rows, BH, 4, 4) ||
+      !make_tmap_bf16_4d(&tdk, dk, kD, g.W, g.kv_rows, BH, 4, 4) ||
+      !make_tmap_bf16_4d(&tdv, dv, kD, g.W, g.kv_rows, BH, 4, 4))
     return cudaErrorInvalidValue;
   CUtensorMap tl, td;
   const bool tma_lsd = (g.W * 4) % 16 == 0 && make_tmap_f32_3d(&tl, lse, g.W, g.q_rows, BH, C::LP, C::QRH) &&
@@ -569,7 +613,7 @@ cudaError_t launch_dkdv_t(const Geo &g, const void *q, const void *k, const void
   p.trace = (long long *)debug_trace_buffer();
   const int grid = p.num_tiles < tc::num_sms() ? p.num_tiles : tc::num_sms();
   ProfScope ps("na2d_bwd_dkdv_tc", st);
-  na2d_bwd_dkdv_kernel<L, QP><<<grid, kThreads, C::SMEM, st>>>(tq, tdo, tk, tv, tl, td, p);
+  na2d_bwd_dkdv_kernel<L, QP><<<grid, kThreads, C::SMEM, st>>>(tq, tdo, tk, tv, tl, td, tdk, tdv, p);
   return cudaGetLastError();
 }
 
@@ -600,14 +644,12 @@ int max_query_halo_width(const Geo &g) {
 cudaError_t tc_backward_dkdv(const Geo &g, const void *q, const void *k, const void *v, const float *rpb,
                              const float *lse, const void *dout, const float *D, void *dk, void *dv,
                              cudaStream_t st) {
-  const bool wide = max_query_halo_width(g) > 24;
+  // the query halo of a 16-column key tile is at most 16 + 2NS + 1 <= 23 columns for L <= 7
+  if (max_query_halo_width(g) > 24) return cudaErrorNotSupported;
   switch (g.L) {
-    case 3: return wide ? launch_dkdv_t<3, 32>(g, q, k, v, rpb, lse, dout, D, dk, dv, st)
-                        : launch_dkdv_t<3, 24>(g, q, k, v, rpb, lse, dout, D, dk, dv, st);
-    case 5: return wide ? launch_dkdv_t<5, 32>(g, q, k, v, rpb, lse, dout, D, dk, dv, st)
-                        : launch_dkdv_t<5, 24>(g, q, k, v, rpb, lse, dout, D, dk, dv, st);
-    case 7: return wide ? launch_dkdv_t<7, 32>(g, q, k, v, rpb, lse, dout, D, dk, dv, st)
-                        : launch_dkdv_t<7, 24>(g, q, k, v, rpb, lse, dout, D, dk, dv, st);
+    case 3: return launch_dkdv_t<3, 24>(g, q, k, v, rpb, lse, dout, D, dk, dv, st);
+    case 5: return launch_dkdv_t<5, 24>(g, q, k, v, rpb, lse, dout, D, dk, dv, st);
+    case 7: return launch_dkdv_t<7, 24>(g, q, k, v, rpb, lse, dout, D, dk, dv, st);
   }
   return cudaErrorInvalidValue;
 }

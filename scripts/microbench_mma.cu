@@ -68,7 +68,94 @@ void run(const char *name) {
   printf("%-34s %7.1f cyc/MMA  %6.0f MAC/clk/SM  (%s)\n", name, per, macs / per, cudaGetErrorString(e));
 }
 
+
+// B2's per-chunk tensor sequence: S^T/dP^T (8 SS, M=64 N=96, sub-tiles at TMEM lane offsets 0 / 16)
+// into slot x, then dV/dK (24 TS, M=64 N=32, A = bf16 P^T / dS^T from the slot) into 8 chains.
+// MODE 1: S only, 2: dV/dK only, 3: both.  Reports cycles per chunk and the issue time per chunk.
+template <int MODE>
+__global__ void chunk_bench(int iters, long long *cyc) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x / 32;
+  for (int i = threadIdx.x; i < 96 * 1024 / 4; i += blockDim.x) ((uint32_t *)smem)[i] = 0x3c003c00u;
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<512>(&slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (warp == 0) {
+    constexpr uint32_t ids = idesc_bf16(64, 96, false), ido = idesc_bf16(64, 32, true);
+    const uint32_t q = smem_u32(smem), dO = q + 24576, k = q + 49152, v = k + 8192;
+    long long t0 = clock64(), tiss = 0;
+    if (elect_one()) {
+      for (int it = 0; it < iters; ++it) {
+        const uint32_t x = (it & 1) * 192;
+        const int row = (it % 3) * 4;
+        long long a = clock64();
+        if (MODE & 1) {
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk)
+#pragma unroll
+            for (int sb = 0; sb < 2; ++sb) {
+              const uint32_t lo = ((uint32_t)(16 * sb) << 16) + x;
+              mma_ss(tmem + lo, sdesc_sw64(k + sb * 4096 + kk * 32), sdesc_sw64(q + row * 24 * 64 + kk * 32), ids, kk);
+              mma_ss(tmem + lo + 96, sdesc_sw64(v + sb * 4096 + kk * 32), sdesc_sw64(dO + row * 24 * 64 + kk * 32), ids, kk);
+            }
+        }
+        if (MODE & 2) {
+#pragma unroll
+          for (int ks = 0; ks < 6; ++ks)
+#pragma unroll
+            for (int sb = 0; sb < 2; ++sb) {
+              const uint32_t lo = (uint32_t)(16 * sb) << 16;
+              const uint32_t boff = row * 24 * 64 + ks * 16 * 64;
+              mma_ts(tmem + lo + 384 + (ks & 1) * 32, tmem + lo + x + ks * 8, sdesc_sw64(dO + boff), ido, it > 0 || ks >= 2);
+              mma_ts(tmem + lo + 448 + (ks & 1) * 32, tmem + lo + x + 96 + ks * 8, sdesc_sw64(q + boff), ido, it > 0 || ks >= 2);
+            }
+        }
+        tiss += clock64() - a;
+      }
+      mma_commit(&bar);
+    }
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    if (threadIdx.x == 0) {
+      cyc[2 * blockIdx.x] = t1 - t0;
+      cyc[2 * blockIdx.x + 1] = tiss;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+template <int MODE>
+void run_chunk(const char *name) {
+  long long *cyc;
+  cudaMallocManaged(&cyc, 2 * 148 * 8);
+  auto kf = chunk_bench<MODE>;
+  cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  const int iters = 1000;
+  kf<<<148, 128, 100 * 1024>>>(iters, cyc);
+  cudaError_t e = cudaDeviceSynchronize();
+  printf("%-34s %7.1f cyc/chunk  issue %6.1f cyc/chunk (%s)\n", name, (double)cyc[0] / iters, (double)cyc[1] / iters,
+         cudaGetErrorString(e));
+}
+
 int main() {
+  run_chunk<1>("B2 chunk: S/dP only");
+  run_chunk<2>("B2 chunk: dV/dK only");
+  run_chunk<3>("B2 chunk: S/dP + dV/dK");
   run<128, 256, false, 1>("SS M=128 N=256 (1 chain)");
   run<128, 256, false, 2>("SS M=128 N=256 (2 chains)");
   run<64, 240, false, 1>("SS M=64 N=240 (1 chain)");
