@@ -498,10 +498,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int rows_here = min(qs_n - C::CR * k, q_end - i_base);
         const float *lrow0 = lsd + (i_base - qr0) * C::LP + (qc0 & 3) + uc;
         const uint32_t lane_addr = lane_q + x * kSlot;
-        if (fast)
-          chunk_rows<L, QP, true>(lane_addr, uc, tbl_row0, colterm, lrow0, pk, i_base, p.H, rows_here, Lh, sl2);
-        else
-          chunk_rows<L, QP, false>(lane_addr, uc, tbl_row0, colterm, lrow0, pk, i_base, p.H, rows_here, Lh, sl2);
+        // a quarter whose keys all lie past the map edge only feeds accumulator rows the TMA store
+        // clips, so its P / dS columns may hold anything
+        if (kc0 + 4 * quarter < p.W) {
+          if (fast)
+            chunk_rows<L, QP, true>(lane_addr, uc, tbl_row0, colterm, lrow0, pk, i_base, p.H, rows_here, Lh, sl2);
+          else
+            chunk_rows<L, QP, false>(lane_addr, uc, tbl_row0, colterm, lrow0, pk, i_base, p.H, rows_here, Lh, sl2);
+        }
         tc_wait_st();
         tc_fence_before();
         __syncwarp();

@@ -51,27 +51,43 @@ struct CfgQ {
   static constexpr int KV_ROWS = HR * kHCP;
   static constexpr int Q_BYTES = 128 * kRowBytes;
   static constexpr int KV_BYTES = KV_ROWS * kRowBytes;
-  static constexpr int STAGE_BYTES = 2 * Q_BYTES + 2 * KV_BYTES;  // Q, dO, K, V
+  static constexpr int TX_BYTES = 2 * Q_BYTES + 2 * KV_BYTES;     // Q, dO, K, V by TMA
+  static constexpr int LSE_OFF = TX_BYTES;                          // + the tile's 128 LSE (log2)
+  static constexpr int STAGE_BYTES = TX_BYTES + 1024;
   static_assert(STAGE_BYTES % 1024 == 0, "stages must stay 1 KB aligned (swizzled TMA / UMMA)");
   static constexpr int TT = 2 * L - 1;
   static constexpr int TBL_OFF = kStages * STAGE_BYTES;
-  static constexpr int DB_OFF = TBL_OFF + BiasTable<L>::FLOATS * 4;
-  static constexpr int BAR_OFF = DB_OFF + ((TT * TT * 4 + 255) / 256) * 256;
+  static constexpr int OUT_OFF = (TBL_OFF + BiasTable<L>::FLOATS * 4 + 1023) / 1024 * 1024;  // dQ staging
+  static constexpr int DB_OFF = OUT_OFF + 4 * 2048;
+  static constexpr int BAR_OFF = DB_OFF + ((8 * TT * TT * 4 + 255) / 256) * 256;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
+  static_assert(SMEM <= 232448, "shared memory");
 };
 
 __device__ __forceinline__ TileOrder::Tile decode(const BwdQParams &p, int t) { return p.order.decode(t); }
+// debug timeline: trace[4096 + (cta / 37 * 32 + tile) * 32 + ev] for CTAs 0, 37, 74, 111 (tile = CTA-local tile index;
+// the first 4096 slots belong to B2)
+__device__ __forceinline__ void qtrace_gt(const BwdQParams &p, int slot) {  // wall clock into tile row 0
+  if (p.trace && blockIdx.x % 37 == 0) {
+    uint64_t gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    p.trace[4096 + ((size_t)(blockIdx.x / 37) * 32) * 32 + slot] = (long long)gt;
+  }
+}
+__device__ __forceinline__ void qtrace(const BwdQParams &p, int it, int ev) {
+  if (p.trace && blockIdx.x % 37 == 0 && it < 32) p.trace[4096 + ((size_t)(blockIdx.x / 37) * 32 + it) * 32 + ev] = clock64();
+}
 
 template <int L>
 __global__ void __launch_bounds__(kThreads, 1)
     na2d_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                        const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
-                       const BwdQParams p) {
+                       const __grid_constant__ CUtensorMap tm_dq, const BwdQParams p) {
   using C = CfgQ<L>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   float *tbl = (float *)(smem + C::TBL_OFF);
-  float *s_db = (float *)(smem + C::DB_OFF);
+  float *s_db = (float *)(smem + C::DB_OFF);  // 8 private dRPB tables: (elementwise warp, half)
   uint64_t *bars = (uint64_t *)(smem + C::BAR_OFF);
   uint64_t *full = bars, *empty = bars + kStages;
   uint64_t *sp_full = bars + 2 * kStages, *ds_full = sp_full + 1, *dq_full = sp_full + 2, *tmem_free = sp_full + 3;
@@ -81,10 +97,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int t_begin = (int)((long)p.num_tiles * blockIdx.x / gridDim.x);
   const int t_end = (int)((long)p.num_tiles * (blockIdx.x + 1) / gridDim.x);
   const int q_end = p.q_row0 + p.q_rows;
+  if (threadIdx.x == 0) qtrace_gt(p, 16);
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], 1 + 32);  // expect_tx arrive + 32 lanes staging the tile's LSE
       mbar_init(&empty[s], 1);
     }
     mbar_init(sp_full, 1);
@@ -96,8 +113,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&tm_do);
     tma_prefetch(&tm_k);
     tma_prefetch(&tm_v);
+    tma_prefetch(&tm_dq);
   }
-  for (int c = threadIdx.x; c < C::TT * C::TT; c += kThreads) s_db[c] = 0.f;
+  for (int c = threadIdx.x; c < 8 * C::TT * C::TT; c += kThreads) s_db[c] = 0.f;
   if (warp == 0) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
@@ -105,16 +123,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    // ================= TMA producer
-    if (elect_one()) {
-      int it = 0;
-      for (int t = t_begin; t < t_end; ++t, ++it) {
-        const int s = it % kStages;
-        mbar_wait_sleep(&empty[s], ((it / kStages) & 1) ^ 1, 1024);
-        const TileOrder::Tile g = decode(p, t);
-        const int hr0 = wstart(g.i0, p.H, L), hc0 = wstart(g.j0, p.W, L);
-        uint8_t *st = smem + s * C::STAGE_BYTES;
-        mbar_expect_tx(&full[s], C::STAGE_BYTES);
+    // ================= producer: TMA (Q, dO 4x4 blocks; K, V halo) + the tile's LSE (log2 units)
+    int it = 0;
+    for (int t = t_begin; t < t_end; ++t, ++it) {
+      const int s = it % kStages;
+      mbar_wait_sleep(&empty[s], ((it / kStages) & 1) ^ 1, 1024);
+      const TileOrder::Tile g = decode(p, t);
+      const int hr0 = wstart(g.i0, p.H, L), hc0 = wstart(g.j0, p.W, L);
+      uint8_t *st = smem + s * C::STAGE_BYTES;
+      if (elect_one()) {
+        mbar_expect_tx(&full[s], C::TX_BYTES);
 #pragma unroll
         for (int sb = 0; sb < 2; ++sb)
 #pragma unroll
@@ -126,6 +144,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_4d(st + 2 * C::Q_BYTES, &tm_k, &full[s], 0, hc0, hr0 - p.kv_row0, g.bh);
         tma_load_4d(st + 2 * C::Q_BYTES + C::KV_BYTES, &tm_v, &full[s], 0, hc0, hr0 - p.kv_row0, g.bh);
       }
+      __syncwarp();
+      // LSE of query (half, quarter, r, c) at e = half*64 + quarter*16 + r*4 + c; 0 if outside
+      float *lse_s = (float *)(st + C::LSE_OFF);
+      float lv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = lane + 32 * u;
+        const int i = g.i0 + 4 * (e >> 6) + ((e >> 2) & 3), j = g.j0 + 4 * ((e >> 4) & 3) + (e & 3);
+        lv[u] = (i < q_end && j < p.W)
+                    ? __ldg(&p.lse[((size_t)g.bh * p.q_rows + (i - p.q_row0)) * p.W + j]) * 1.4426950408889634f
+                    : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) lse_s[lane + 32 * u] = lv[u];
+      mbar_arrive(&full[s]);
     }
   } else if (warp == 1) {
     // ================= MMA issuer
@@ -140,7 +173,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int rb0 = wstart(min(g.i0, q_end - 1), p.H, L) - hr0;
       const int rb1 = wstart(min(g.i0 + 4, q_end - 1), p.H, L) - hr0;
       mbar_wait_sleep(&full[s], (it / kStages) & 1, 64);
+      if (lane == 0) qtrace(p, it, 0);
+      if (lane == 0 && p.trace && blockIdx.x % 37 == 0 && it < 32) {  // wall clock beside the SM clock
+        uint64_t gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        p.trace[4096 + ((size_t)(blockIdx.x / 37) * 32 + it) * 32 + 15] = (long long)gt;
+      }
       mbar_wait_sleep(tmem_free, ph ^ 1, 64);
+      if (lane == 0) qtrace(p, it, 1);
       tc_fence_after();
       const uint32_t q_addr = smem_u32(smem + s * C::STAGE_BYTES);
       const uint32_t do_addr = q_addr + C::Q_BYTES;
@@ -161,7 +201,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_commit(sp_full);
       }
       __syncwarp();
+      if (lane == 0) qtrace(p, it, 2);
       mbar_wait_sleep(ds_full, ph, 64);
+      if (lane == 0) qtrace(p, it, 3);
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
@@ -177,6 +219,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_commit(&empty[s]);
       }
       __syncwarp();
+      if (lane == 0) qtrace(p, it, 4);
     }
   } else {
     // ================= elementwise + epilogue (warps 2..5 -> TMEM lane quarters 2,3,0,1)
@@ -186,38 +229,56 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int Lh = wlen(p.H, L), Lw = wlen(p.W, L);
     const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
     const float sl2 = p.scale * 1.4426950408889634f;
+    const float2 sl2x2 = make_float2(sl2, sl2);
+    // this (warp, half)'s private dRPB table: within one instruction the 16 lanes of a half touch
+    // distinct cells (no intra-instruction address conflicts, no other warp contending), but
+    // different (u, z) of different lanes do meet, so the adds stay atomic (RED to shared)
+    float *my_db = s_db + (quarter * 2 + half) * C::TT * C::TT;
+    uint8_t *ostage = smem + C::OUT_OFF + quarter * 2048;
     // dRPB accumulator in union coordinates for the current (class, head) and its geometry
-    float acc[C::UR][C::UCW];
+    float2 acc[C::UR][C::UCW / 2];
 #pragma unroll
     for (int u = 0; u < C::UR; ++u)
 #pragma unroll
-      for (int z = 0; z < C::UCW; ++z) acc[u][z] = 0.f;
+      for (int z = 0; z < C::UCW / 2; ++z) acc[u][z] = make_float2(0.f, 0.f);
     int cur_key = -1, cur_head = -1;
     int f_wr = 0, f_wc = 0, f_brow = 0, f_bcol = 0;  // geometry of the accumulated class
+    bool f_valid = false;  // own query inside the map / band (constant within a class)
     auto flush = [&]() {
-      // masked to this lane's window; cells (f_brow + u, f_bcol + z)
+      // masked to this lane's window; cells (f_brow + u, f_bcol + z).  Lanes of queries past the
+      // edge (clamped onto an edge query's cells, dS = 0) skip the adds.
 #pragma unroll
       for (int u = 0; u < C::UR; ++u)
 #pragma unroll
         for (int z = 0; z < C::UCW; ++z) {
-          if ((unsigned)(u - f_wr) < (unsigned)Lh && (unsigned)(z - f_wc) < (unsigned)Lw)
-            atomicAdd(&s_db[(f_brow + u) * C::TT + f_bcol + z], acc[u][z]);
-          acc[u][z] = 0.f;
+          const float v = (z & 1) ? acc[u][z / 2].y : acc[u][z / 2].x;
+          if (f_valid && (unsigned)(u - f_wr) < (unsigned)Lh && (unsigned)(z - f_wc) < (unsigned)Lw)
+            atomicAdd(&my_db[(f_brow + u) * C::TT + f_bcol + z], v);
         }
+#pragma unroll
+      for (int u = 0; u < C::UR; ++u)
+#pragma unroll
+        for (int z = 0; z < C::UCW / 2; ++z) acc[u][z] = make_float2(0.f, 0.f);
     };
-    auto commit_head = [&](int head) {  // per-CTA table -> partials[cta][head]; clear
+    auto commit_head = [&](int head) {  // sum of the 8 private tables -> partials[cta][head]; clear
       named_bar_sync(1, 128);
       if (head >= 0 && p.drpb_part)
         for (int e = gtid; e < C::TT * C::TT; e += 128) {
+          float v = 0.f;
+#pragma unroll
+          for (int w = 0; w < 8; ++w) {
+            v += s_db[w * C::TT * C::TT + e];
+            s_db[w * C::TT * C::TT + e] = 0.f;
+          }
           float *dst = &p.drpb_part[((size_t)blockIdx.x * p.heads + head) * C::TT * C::TT + e];
-          *dst += p.scale * s_db[e];
-          s_db[e] = 0.f;
+          *dst += p.scale * v;
         }
       named_bar_sync(1, 128);
     };
     int it = 0;
     for (int t = t_begin; t < t_end; ++t, ++it) {
       const uint32_t ph = it & 1;
+      const int stage = it % kStages;
       const TileOrder::Tile g = decode(p, t);
       const int h = g.bh % p.heads;
       const int key = g.cls * p.heads + h;
@@ -239,75 +300,86 @@ __global__ void __launch_bounds__(kThreads, 1)
           cur_head = h;
         }
         cur_key = key;
+        f_valid = i < q_end && j < p.W;
         f_wr = si - hr0 - rb;
         f_wc = sj - hc0 - uc;
         f_brow = brow0;
         f_bcol = bcol0;
       }
-      // own query: LSE (log2 units)
       const bool qvalid = i < q_end && j < p.W;
       const size_t qi = ((size_t)g.bh * p.q_rows + (ic - p.q_row0)) * p.W + jc;
-      const float lse2 = qvalid ? p.lse[qi] * 1.4426950408889634f : 0.f;
       const float *tcls = tbl + dc * BiasTable<L>::TROWS * kTblStride + kTblOff + bcol0;
+      const bool tq = quarter == 2 && lane == 0;
+      if (tq) qtrace(p, it, 8);
+      mbar_wait(&full[stage], (it / kStages) & 1);  // the tile's LSE staged
+      const float nlse2 = -((const float *)(smem + stage * C::STAGE_BYTES + C::LSE_OFF))[half * 64 + quarter * 16 + r * 4 + c];
+      const float2 nlse2x2 = make_float2(nlse2, nlse2);
       mbar_wait(sp_full, ph);
+      if (tq) qtrace(p, it, 9);
       tc_fence_after();
       // ---- pass 1: P = exp2(s*scale*log2e + B' - LSE*log2e) (fp32, written over S in place) and
-      // D = dO.O = sum_window P dP (exact in fp32: O = sum P V, so dO.O = sum P (dO.v))
+      // D = dO.O = sum_window P dP (exact in fp32: O = sum P V, so dO.O = sum P (dO.v)); element
+      // pairs in packed fp32x2 arithmetic
       float Dq = 0.f;
 #pragma unroll 1
       for (int u = 0; u < C::UR; u += 2) {
-        uint32_t sa[16], sb_[16], pa_[16], pb_[16];
+        uint32_t sa[C::UCW], sb_[C::UCW], pa_[C::UCW], pb_[C::UCW];
         const uint32_t ca = lane_addr + u * kHCP + uc;
-        tmem_ld16(ca, sa);
-        tmem_ld16(ca + kHCP, sb_);
-        tmem_ld16(ca + kDP_COL, pa_);
-        tmem_ld16(ca + kDP_COL + kHCP, pb_);
+        ld_row<C::UCW>(ca, sa);
+        ld_row<C::UCW>(ca + kHCP, sb_);
+        ld_row<C::UCW>(ca + kDP_COL, pa_);
+        ld_row<C::UCW>(ca + kDP_COL + kHCP, pb_);
         const int pr = hr0 + rb + u;
         const bool rva = (unsigned)(pr - si) < (unsigned)Lh, rvb = (unsigned)(pr + 1 - si) < (unsigned)Lh;
         const float *ta = tcls + (rva ? pr - ic + L - 1 : C::TT) * kTblStride;
         const float *tb = tcls + (rvb ? pr + 1 - ic + L - 1 : C::TT) * kTblStride;
         tc_wait_ld();
-        float da = 0.f, db = 0.f;
+        float2 da = make_float2(0.f, 0.f), db = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int z = 0; z < C::UCW; ++z) {
-          const float P0 = ex2(fmaf(__uint_as_float(sa[z]), sl2, ta[z]) - lse2);
-          const float P1 = ex2(fmaf(__uint_as_float(sb_[z]), sl2, tb[z]) - lse2);
-          da = fmaf(P0, __uint_as_float(pa_[z]), da);
-          db = fmaf(P1, __uint_as_float(pb_[z]), db);
-          sa[z] = __float_as_uint(P0);
-          sb_[z] = __float_as_uint(P1);
+        for (int z = 0; z < C::UCW; z += 2) {
+          const float2 xa = __fadd2_rn(__ffma2_rn(make_float2(__uint_as_float(sa[z]), __uint_as_float(sa[z + 1])),
+                                                  sl2x2, make_float2(ta[z], ta[z + 1])), nlse2x2);
+          const float2 xb = __fadd2_rn(__ffma2_rn(make_float2(__uint_as_float(sb_[z]), __uint_as_float(sb_[z + 1])),
+                                                  sl2x2, make_float2(tb[z], tb[z + 1])), nlse2x2);
+          const float2 Pa = make_float2(ex2(xa.x), ex2(xa.y)), Pb = make_float2(ex2(xb.x), ex2(xb.y));
+          da = __ffma2_rn(Pa, make_float2(__uint_as_float(pa_[z]), __uint_as_float(pa_[z + 1])), da);
+          db = __ffma2_rn(Pb, make_float2(__uint_as_float(pb_[z]), __uint_as_float(pb_[z + 1])), db);
+          sa[z] = __float_as_uint(Pa.x);
+          sa[z + 1] = __float_as_uint(Pa.y);
+          sb_[z] = __float_as_uint(Pb.x);
+          sb_[z + 1] = __float_as_uint(Pb.y);
         }
-        Dq += da + db;
-        tmem_st16(ca, sa);
-        tmem_st16(ca + kHCP, sb_);
+        Dq += (da.x + da.y) + (db.x + db.y);
+        st_row<C::UCW>(ca, sa);
+        st_row<C::UCW>(ca + kHCP, sb_);
       }
       if (qvalid) p.D[qi] = Dq;
+      if (tq) qtrace(p, it, 10);
       tc_wait_st();
       // ---- pass 2: dS = P (dP - D) -> dRPB accumulators (union coordinates) and bf16 pairs over
       // the consumed S/P columns (the dQ MMA's A operand)
       const int zb = uc >> 1;
+      const float2 nD = make_float2(-Dq, -Dq);
 #pragma unroll
       for (int u = 0; u < C::UR; u += 2) {
-        uint32_t sa[16], sb_[16], pa_[16], pb_[16];
+        uint32_t sa[C::UCW], sb_[C::UCW], pa_[C::UCW], pb_[C::UCW];
         const uint32_t ca = lane_addr + u * kHCP + uc;
-        tmem_ld16(ca, sa);
-        tmem_ld16(ca + kHCP, sb_);
-        tmem_ld16(ca + kDP_COL, pa_);
-        tmem_ld16(ca + kDP_COL + kHCP, pb_);
+        ld_row<C::UCW>(ca, sa);
+        ld_row<C::UCW>(ca + kHCP, sb_);
+        ld_row<C::UCW>(ca + kDP_COL, pa_);
+        ld_row<C::UCW>(ca + kDP_COL + kHCP, pb_);
         tc_wait_ld();
         uint32_t da[C::UCW / 2], db[C::UCW / 2];
 #pragma unroll
         for (int z = 0; z < C::UCW; z += 2) {
-          float d2[2][2];
-#pragma unroll
-          for (int y = 0; y < 2; ++y) {
-            d2[0][y] = __uint_as_float(sa[z + y]) * (__uint_as_float(pa_[z + y]) - Dq);
-            d2[1][y] = __uint_as_float(sb_[z + y]) * (__uint_as_float(pb_[z + y]) - Dq);
-            acc[u][z + y] += d2[0][y];
-            acc[u + 1][z + y] += d2[1][y];
-          }
-          da[z / 2] = pack_bf16_alu(d2[0][0], d2[0][1]);
-          db[z / 2] = pack_bf16_alu(d2[1][0], d2[1][1]);
+          const float2 dsa = __fmul2_rn(make_float2(__uint_as_float(sa[z]), __uint_as_float(sa[z + 1])),
+                                        __fadd2_rn(make_float2(__uint_as_float(pa_[z]), __uint_as_float(pa_[z + 1])), nD));
+          const float2 dsb = __fmul2_rn(make_float2(__uint_as_float(sb_[z]), __uint_as_float(sb_[z + 1])),
+                                        __fadd2_rn(make_float2(__uint_as_float(pb_[z]), __uint_as_float(pb_[z + 1])), nD));
+          acc[u][z / 2] = __fadd2_rn(acc[u][z / 2], dsa);
+          acc[u + 1][z / 2] = __fadd2_rn(acc[u + 1][z / 2], dsb);
+          da[z / 2] = pack_bf16(dsa.x, dsa.y);
+          db[z / 2] = pack_bf16(dsb.x, dsb.y);
         }
         const uint32_t prow = lane_addr + C::DS_COL + u * (kHCP / 2);
         st_zero12(prow);
@@ -319,42 +391,60 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(ds_full);
-      // ---- epilogue: dQ = scale * sum of partial accumulators -> bf16
+      if (tq) qtrace(p, it, 11);
+      // ---- epilogue: dQ = scale * sum of partial accumulators -> bf16, TMA-stored via smem
       mbar_wait(dq_full, ph);
+      if (tq) qtrace(p, it, 12);
       tc_fence_after();
-      uint32_t o[32];
-      {
-        uint32_t oa[kQAcc][32];
+      uint32_t o[32];  // partial accumulators summed one at a time (register pressure)
+      tmem_ld32(lane_addr + C::Q_COL, o);
+      tc_wait_ld();
 #pragma unroll
-        for (int a = 0; a < kQAcc; ++a) tmem_ld32(lane_addr + C::Q_COL + a * kD, oa[a]);
+      for (int a = 1; a < kQAcc; ++a) {
+        uint32_t oa[32];
+        tmem_ld32(lane_addr + C::Q_COL + a * kD, oa);
         tc_wait_ld();
 #pragma unroll
-        for (int z = 0; z < 32; ++z) {
-          float s = __uint_as_float(oa[0][z]);
-#pragma unroll
-          for (int a = 1; a < kQAcc; ++a) s += __uint_as_float(oa[a][z]);
-          o[z] = __float_as_uint(s * p.scale);
-        }
+        for (int z = 0; z < 32; ++z) o[z] = __float_as_uint(__uint_as_float(o[z]) + __uint_as_float(oa[z]));
       }
+#pragma unroll
+      for (int z = 0; z < 32; ++z) o[z] = __float_as_uint(__uint_as_float(o[z]) * p.scale);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tmem_free);
-      if (qvalid) {
-        uint4 *dst = (uint4 *)(p.dq + qi * kD);
+      if (tq) qtrace(p, it, 13);
+      if (lane == 0) bulk_wait_read0();  // this warp's previous store has left the staging
+      __syncwarp();
+      {
+        // query (r, c) of block `half` is row R of the 1 KB box; SW64: 16-byte chunk z at z ^ (R/2 % 4)
+        const int R = r * 4 + c;
+        uint8_t *row = ostage + half * 1024 + R * 64;
 #pragma unroll
-        for (int z = 0; z < kD; z += 8)
-          dst[z / 8] = make_uint4(pack_bf16(__uint_as_float(o[z]), __uint_as_float(o[z + 1])),
-                                  pack_bf16(__uint_as_float(o[z + 2]), __uint_as_float(o[z + 3])),
-                                  pack_bf16(__uint_as_float(o[z + 4]), __uint_as_float(o[z + 5])),
-                                  pack_bf16(__uint_as_float(o[z + 6]), __uint_as_float(o[z + 7])));
+        for (int z = 0; z < 4; ++z)
+          *(uint4 *)(row + 16 * ((z ^ (R >> 1)) & 3)) =
+              make_uint4(pack_bf16(__uint_as_float(o[8 * z]), __uint_as_float(o[8 * z + 1])),
+                         pack_bf16(__uint_as_float(o[8 * z + 2]), __uint_as_float(o[8 * z + 3])),
+                         pack_bf16(__uint_as_float(o[8 * z + 4]), __uint_as_float(o[8 * z + 5])),
+                         pack_bf16(__uint_as_float(o[8 * z + 6]), __uint_as_float(o[8 * z + 7])));
       }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {  // queries past the map / band edge are clipped by the TMA unit
+        tma_store_4d(&tm_dq, ostage, 0, g.j0 + 4 * quarter, g.i0 - p.q_row0, g.bh);
+        tma_store_4d(&tm_dq, ostage + 1024, 0, g.j0 + 4 * quarter, g.i0 - p.q_row0 + 4, g.bh);
+        bulk_commit();
+      }
+      if (tq) qtrace(p, it, 14);
     }
+    if (threadIdx.x == 64 + 64) qtrace_gt(p, 17);
     if (p.rpb) {
       if (cur_key >= 0) flush();
       commit_head(cur_head);
     }
+    if (lane == 0) bulk_wait0();
   }
   __syncthreads();
+  if (threadIdx.x == 0) qtrace_gt(p, 18);
   if (warp == 0) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
@@ -384,12 +474,13 @@ cudaError_t launch_dq(const Geo &g, const void *q, const void *k, const void *v,
     attr_err = cudaFuncSetAttribute(na2d_bwd_dq_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   });
   if (attr_err != cudaSuccess) return attr_err;
-  CUtensorMap tq, tdo, tk, tv;
+  CUtensorMap tq, tdo, tk, tv, tdq;
   const int BH = g.B * g.heads;
   if (!make_tmap_bf16_4d(&tq, q, kD, g.W, g.q_rows, BH, 4, 4) ||
       !make_tmap_bf16_4d(&tdo, dout, kD, g.W, g.q_rows, BH, 4, 4) ||
       !make_tmap_bf16_4d(&tk, k, kD, g.W, g.kv_rows, BH, kHCP, C::HR) ||
-      !make_tmap_bf16_4d(&tv, v, kD, g.W, g.kv_rows, BH, kHCP, C::HR))
+      !make_tmap_bf16_4d(&tv, v, kD, g.W, g.kv_rows, BH, kHCP, C::HR) ||
+      !make_tmap_bf16_4d(&tdq, dq, kD, g.W, g.q_rows, BH, 4, 4))
     return cudaErrorInvalidValue;
   BwdQParams p;
   p.heads = g.heads;
@@ -408,6 +499,7 @@ cudaError_t launch_dq(const Geo &g, const void *q, const void *k, const void *v,
   p.dq = (__nv_bfloat16 *)dq;
   p.D = D;
   p.drpb_part = rpb ? part : nullptr;
+  p.trace = (long long *)debug_trace_buffer();
   const int grid = dq_grid(g);
   const int TT = 2 * L - 1;
   cudaError_t e;
@@ -417,7 +509,7 @@ cudaError_t launch_dq(const Geo &g, const void *q, const void *k, const void *v,
   }
   {
     ProfScope ps("na2d_bwd_dq_tc", st);
-    na2d_bwd_dq_kernel<L><<<grid, kThreads, C::SMEM, st>>>(tq, tdo, tk, tv, p);
+    na2d_bwd_dq_kernel<L><<<grid, kThreads, C::SMEM, st>>>(tq, tdo, tk, tv, tdq, p);
   }
   e = cudaGetLastError();
   if (e != cudaSuccess || !rpb) return e;

@@ -56,6 +56,7 @@ struct BwdQParams {
   __nv_bfloat16 *dq;
   float *D;          // [B*heads*q_rows*W] written
   float *drpb_part;  // [grid][heads][TT*TT] partial tables (null if no rpb)
+  long long *trace;  // debug timeline (na2d_debug_set_trace) or null
 };
 
 int dq_grid(const Geo &g);
