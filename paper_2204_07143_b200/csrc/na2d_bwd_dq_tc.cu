@@ -34,9 +34,17 @@ using namespace sm100;
 using namespace tc;
 
 constexpr int kStages = 2;
-constexpr int kThreads = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 elementwise + epilogue
+constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-5 / 6-9 elementwise groups 0 / 1
 constexpr int kQAcc = 3;       // independent dQ accumulators
 constexpr int kDP_COL = 256;   // dP accumulator columns
+
+// Per-stage tile description, written by the producer before it arms full[stage] (the class-grouped
+// order's decode and the window origins, computed once instead of in every warp).
+struct TileInfoQ {
+  int bh, i0, j0, cls, hr0, hc0;
+  int rb[2];  // first union row of sub-tile / half h (relative to hr0)
+  int uc[4];  // even first union column of lane quarter q (relative to hc0)
+};
 
 template <int L>
 struct CfgQ {
@@ -44,10 +52,15 @@ struct CfgQ {
   static constexpr int UR = 4 + L - 1;
   static constexpr int NSUB = UR * kHCP;
   static constexpr int UCW = L + 5;
+  // union row pairs split between the two elementwise warps of a TMEM lane quarter; each group
+  // writes its dS rows over its own consumed S rows: row u at DS_COL + u*12 (+ DS_SHIFT for
+  // group 1's rows), so the dQ MMA's K-steps from DS_KS1 on read DS_SHIFT columns further
+  static constexpr int PAIRS = UR / 2, PA = (PAIRS + 1) / 2;
+  static constexpr int DS_SHIFT = PA * kHCP, DS_KS1 = 3 * PA;
+  static_assert(2 * PA * kHCP == 16 * DS_KS1, "group boundary on a K-step boundary");
   static constexpr int DS_COL = 0;         // dS (bf16 pairs) over consumed S columns
-  static constexpr int Q_COL = NSUB / 2;   // dQ partial accumulators in dead S columns
-  static_assert(Q_COL + kQAcc * kD <= kDP_COL, "TMEM budget");
-  static_assert(kDP_COL + NSUB <= 512, "TMEM budget");
+  static constexpr int Q_COL = kDP_COL;    // dQ partial accumulators in the dP columns (dead after pass 2)
+  static_assert(kDP_COL + NSUB <= 512 && Q_COL + kQAcc * kD <= 512, "TMEM budget");
   static constexpr int KV_ROWS = HR * kHCP;
   static constexpr int Q_BYTES = 128 * kRowBytes;
   static constexpr int KV_BYTES = KV_ROWS * kRowBytes;
@@ -59,7 +72,10 @@ struct CfgQ {
   static constexpr int TBL_OFF = kStages * STAGE_BYTES;
   static constexpr int OUT_OFF = (TBL_OFF + BiasTable<L>::FLOATS * 4 + 1023) / 1024 * 1024;  // dQ staging
   static constexpr int DB_OFF = OUT_OFF + 4 * 2048;
-  static constexpr int BAR_OFF = DB_OFF + ((8 * TT * TT * 4 + 255) / 256) * 256;
+  static constexpr int DP_OFF = DB_OFF + ((16 * TT * TT * 4 + 255) / 256) * 256;  // partial D exchange
+  static constexpr int TI_OFF = DP_OFF + 2 * 128 * 4;
+  static constexpr int BAR_OFF = TI_OFF + kStages * 64;
+  static_assert(sizeof(TileInfoQ) <= 64, "TileInfoQ");
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
   static_assert(SMEM <= 232448, "shared memory");
 };
@@ -87,7 +103,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   float *tbl = (float *)(smem + C::TBL_OFF);
-  float *s_db = (float *)(smem + C::DB_OFF);  // 8 private dRPB tables: (elementwise warp, half)
+  float *s_db = (float *)(smem + C::DB_OFF);  // 16 private dRPB tables: (elementwise warp, half)
+  TileInfoQ *tinfo = (TileInfoQ *)(smem + C::TI_OFF);
   uint64_t *bars = (uint64_t *)(smem + C::BAR_OFF);
   uint64_t *full = bars, *empty = bars + kStages;
   uint64_t *sp_full = bars + 2 * kStages, *ds_full = sp_full + 1, *dq_full = sp_full + 2, *tmem_free = sp_full + 3;
@@ -105,7 +122,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(sp_full, 1);
-    mbar_init(ds_full, 4);
+    mbar_init(ds_full, 8);
     mbar_init(dq_full, 1);
     mbar_init(tmem_free, 4);
     fence_barrier_init();
@@ -115,7 +132,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&tm_v);
     tma_prefetch(&tm_dq);
   }
-  for (int c = threadIdx.x; c < 8 * C::TT * C::TT; c += kThreads) s_db[c] = 0.f;
+  for (int c = threadIdx.x; c < 16 * C::TT * C::TT; c += kThreads) s_db[c] = 0.f;
   if (warp == 0) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
@@ -131,6 +148,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       const TileOrder::Tile g = decode(p, t);
       const int hr0 = wstart(g.i0, p.H, L), hc0 = wstart(g.j0, p.W, L);
       uint8_t *st = smem + s * C::STAGE_BYTES;
+      TileInfoQ *ti = tinfo + s;
+      if (lane < 2) ti->rb[lane] = wstart(min(g.i0 + 4 * lane, q_end - 1), p.H, L) - hr0;
+      if (lane < 4) ti->uc[lane] = (wstart(min(g.j0 + 4 * lane, p.W - 1), p.W, L) - hc0) & ~1;
+      if (lane == 0) {
+        ti->bh = g.bh;
+        ti->i0 = g.i0;
+        ti->j0 = g.j0;
+        ti->cls = g.cls;
+        ti->hr0 = hr0;
+        ti->hc0 = hc0;
+      }
+      __syncwarp();
       if (elect_one()) {
         mbar_expect_tx(&full[s], C::TX_BYTES);
 #pragma unroll
@@ -168,11 +197,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int t = t_begin; t < t_end; ++t, ++it) {
       const int s = it % kStages;
       const uint32_t ph = it & 1;
-      const TileOrder::Tile g = decode(p, t);
-      const int hr0 = wstart(g.i0, p.H, L);
-      const int rb0 = wstart(min(g.i0, q_end - 1), p.H, L) - hr0;
-      const int rb1 = wstart(min(g.i0 + 4, q_end - 1), p.H, L) - hr0;
       mbar_wait_sleep(&full[s], (it / kStages) & 1, 64);
+      const int rb0 = tinfo[s].rb[0], rb1 = tinfo[s].rb[1];
       if (lane == 0) qtrace(p, it, 0);
       if (lane == 0 && p.trace && blockIdx.x % 37 == 0 && it < 32) {  // wall clock beside the SM clock
         uint64_t gt;
@@ -212,7 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int sb = 0; sb < 2; ++sb) {
             const uint32_t base = tmem + ((uint32_t)(16 * sb) << 16);
             const int rb = sb ? rb1 : rb0;
-            mma_ts(base + C::Q_COL + (ks % kQAcc) * kD, base + C::DS_COL + ks * 8,
+            mma_ts(base + C::Q_COL + (ks % kQAcc) * kD, base + C::DS_COL + ks * 8 + (ks >= C::DS_KS1 ? C::DS_SHIFT : 0),
                    sdesc_sw64(k_addr + rb * kHCP * kRowBytes + ks * 16 * kRowBytes), idesc_q, ks >= kQAcc);
           }
         mma_commit(dq_full);
@@ -222,10 +248,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) qtrace(p, it, 4);
     }
   } else {
-    // ================= elementwise + epilogue (warps 2..5 -> TMEM lane quarters 2,3,0,1)
-    const int quarter = warp & 3;
+    // ================= elementwise (warps 2..5 / 6..9 -> TMEM lane quarters 2,3,0,1): group grp
+    // takes union row pairs [pr0, pr1) of every tile; group 0 also runs the epilogue
+    const int quarter = warp & 3, grp = (warp - 2) >> 2;
+    const int pr0 = grp ? C::PA : 0, pr1 = grp ? C::PAIRS : C::PA;
     const int half = lane >> 4, r = (lane >> 2) & 3, c = lane & 3;
     const int gtid = threadIdx.x - 64;
+    float *s_dpart = (float *)(smem + C::DP_OFF);
     const int Lh = wlen(p.H, L), Lw = wlen(p.W, L);
     const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
     const float sl2 = p.scale * 1.4426950408889634f;
@@ -233,70 +262,75 @@ __global__ void __launch_bounds__(kThreads, 1)
     // this (warp, half)'s private dRPB table: within one instruction the 16 lanes of a half touch
     // distinct cells (no intra-instruction address conflicts, no other warp contending), but
     // different (u, z) of different lanes do meet, so the adds stay atomic (RED to shared)
-    float *my_db = s_db + (quarter * 2 + half) * C::TT * C::TT;
+    float *my_db = s_db + ((grp * 4 + quarter) * 2 + half) * C::TT * C::TT;
     uint8_t *ostage = smem + C::OUT_OFF + quarter * 2048;
     // dRPB accumulator in union coordinates for the current (class, head) and its geometry
-    float2 acc[C::UR][C::UCW / 2];
+    float2 acc[2 * C::PA][C::UCW / 2];  // local rows: union row 2 * pr0 + u
 #pragma unroll
-    for (int u = 0; u < C::UR; ++u)
+    for (int u = 0; u < 2 * C::PA; ++u)
 #pragma unroll
       for (int z = 0; z < C::UCW / 2; ++z) acc[u][z] = make_float2(0.f, 0.f);
     int cur_key = -1, cur_head = -1;
     int f_wr = 0, f_wc = 0, f_brow = 0, f_bcol = 0;  // geometry of the accumulated class
     bool f_valid = false;  // own query inside the map / band (constant within a class)
     auto flush = [&]() {
-      // masked to this lane's window; cells (f_brow + u, f_bcol + z).  Lanes of queries past the
-      // edge (clamped onto an edge query's cells, dS = 0) skip the adds.
+      // masked to this lane's window; cells (f_brow + ug, f_bcol + z) for union row ug.  Lanes of
+      // queries past the edge (clamped onto an edge query's cells, dS = 0) skip the adds.
 #pragma unroll
-      for (int u = 0; u < C::UR; ++u)
+      for (int u = 0; u < 2 * C::PA; ++u) {
+        const int ug = 2 * pr0 + u;
+        if (ug >= 2 * pr1) break;
 #pragma unroll
         for (int z = 0; z < C::UCW; ++z) {
           const float v = (z & 1) ? acc[u][z / 2].y : acc[u][z / 2].x;
-          if (f_valid && (unsigned)(u - f_wr) < (unsigned)Lh && (unsigned)(z - f_wc) < (unsigned)Lw)
-            atomicAdd(&my_db[(f_brow + u) * C::TT + f_bcol + z], v);
+          if (f_valid && (unsigned)(ug - f_wr) < (unsigned)Lh && (unsigned)(z - f_wc) < (unsigned)Lw)
+            atomicAdd(&my_db[(f_brow + ug) * C::TT + f_bcol + z], v);
         }
+      }
 #pragma unroll
-      for (int u = 0; u < C::UR; ++u)
+      for (int u = 0; u < 2 * C::PA; ++u)
 #pragma unroll
         for (int z = 0; z < C::UCW / 2; ++z) acc[u][z] = make_float2(0.f, 0.f);
     };
-    auto commit_head = [&](int head) {  // sum of the 8 private tables -> partials[cta][head]; clear
-      named_bar_sync(1, 128);
+    auto commit_head = [&](int head) {  // sum of the 16 private tables -> partials[cta][head]; clear
+      named_bar_sync(1, 256);
       if (head >= 0 && p.drpb_part)
-        for (int e = gtid; e < C::TT * C::TT; e += 128) {
+        for (int e = gtid; e < C::TT * C::TT; e += 256) {
           float v = 0.f;
 #pragma unroll
-          for (int w = 0; w < 8; ++w) {
+          for (int w = 0; w < 16; ++w) {
             v += s_db[w * C::TT * C::TT + e];
             s_db[w * C::TT * C::TT + e] = 0.f;
           }
           float *dst = &p.drpb_part[((size_t)blockIdx.x * p.heads + head) * C::TT * C::TT + e];
           *dst += p.scale * v;
         }
-      named_bar_sync(1, 128);
+      named_bar_sync(1, 256);
     };
     int it = 0;
     for (int t = t_begin; t < t_end; ++t, ++it) {
       const uint32_t ph = it & 1;
       const int stage = it % kStages;
-      const TileOrder::Tile g = decode(p, t);
-      const int h = g.bh % p.heads;
-      const int key = g.cls * p.heads + h;
-      const int hr0 = wstart(g.i0, p.H, L), hc0 = wstart(g.j0, p.W, L);
-      const int i = g.i0 + 4 * half + r, j = g.j0 + 4 * quarter + c;
+      mbar_wait(&full[stage], (it / kStages) & 1);  // tile description and LSE staged
+      // copied to registers: the producer refills this stage once the tile's dQ MMAs complete,
+      // before the epilogue ends
+      const TileInfoQ &ti = tinfo[stage];
+      const int bh = ti.bh, i0 = ti.i0, j0 = ti.j0, hr0 = ti.hr0, hc0 = ti.hc0;
+      const int rb = ti.rb[half], uc = ti.uc[quarter];
+      const int h = bh % p.heads;
+      const int key = ti.cls * p.heads + h;
+      const int i = i0 + 4 * half + r, j = j0 + 4 * quarter + c;
       const int ic = min(i, q_end - 1), jc = min(j, p.W - 1);
       const int si = wstart(ic, p.H, L), sj = wstart(jc, p.W, L);
-      const int rb = wstart(min(g.i0 + 4 * half, q_end - 1), p.H, L) - hr0;
-      const int uc = (wstart(min(g.j0 + 4 * quarter, p.W - 1), p.W, L) - hc0) & ~1;
       const int dc = sj - jc + L - 1;
       const int brow0 = hr0 + rb - ic + L - 1, bcol0 = hc0 + uc - jc + L - 1;
       if (key != cur_key) {
         if (p.rpb && cur_key >= 0) flush();
         if (h != cur_head) {
           if (p.rpb) commit_head(cur_head);
-          named_bar_sync(1, 128);
-          BiasTable<L>::build(tbl, p.rpb, h, Lw, sl2, gtid, 128);
-          named_bar_sync(1, 128);
+          named_bar_sync(1, 256);
+          BiasTable<L>::build(tbl, p.rpb, h, Lw, sl2, gtid, 256);
+          named_bar_sync(1, 256);
           cur_head = h;
         }
         cur_key = key;
@@ -307,11 +341,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         f_bcol = bcol0;
       }
       const bool qvalid = i < q_end && j < p.W;
-      const size_t qi = ((size_t)g.bh * p.q_rows + (ic - p.q_row0)) * p.W + jc;
+      const size_t qi = ((size_t)bh * p.q_rows + (ic - p.q_row0)) * p.W + jc;
       const float *tcls = tbl + dc * BiasTable<L>::TROWS * kTblStride + kTblOff + bcol0;
-      const bool tq = quarter == 2 && lane == 0;
+      const bool tq = grp == 0 && quarter == 2 && lane == 0;
       if (tq) qtrace(p, it, 8);
-      mbar_wait(&full[stage], (it / kStages) & 1);  // the tile's LSE staged
       const float nlse2 = -((const float *)(smem + stage * C::STAGE_BYTES + C::LSE_OFF))[half * 64 + quarter * 16 + r * 4 + c];
       const float2 nlse2x2 = make_float2(nlse2, nlse2);
       mbar_wait(sp_full, ph);
@@ -322,7 +355,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // pairs in packed fp32x2 arithmetic
       float Dq = 0.f;
 #pragma unroll 1
-      for (int u = 0; u < C::UR; u += 2) {
+      for (int u = 2 * pr0; u < 2 * pr1; u += 2) {
         uint32_t sa[C::UCW], sb_[C::UCW], pa_[C::UCW], pb_[C::UCW];
         const uint32_t ca = lane_addr + u * kHCP + uc;
         ld_row<C::UCW>(ca, sa);
@@ -353,15 +386,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         st_row<C::UCW>(ca, sa);
         st_row<C::UCW>(ca + kHCP, sb_);
       }
-      if (qvalid) p.D[qi] = Dq;
+      // D over the whole window: the two groups' partial sums, added in a fixed order
+      s_dpart[grp * 128 + quarter * 32 + lane] = Dq;
+      named_bar_sync(2 + quarter, 64);
+      Dq = s_dpart[quarter * 32 + lane] + s_dpart[128 + quarter * 32 + lane];
+      if (qvalid && grp == 0) p.D[qi] = Dq;
       if (tq) qtrace(p, it, 10);
       tc_wait_st();
       // ---- pass 2: dS = P (dP - D) -> dRPB accumulators (union coordinates) and bf16 pairs over
       // the consumed S/P columns (the dQ MMA's A operand)
       const int zb = uc >> 1;
       const float2 nD = make_float2(-Dq, -Dq);
+      const uint32_t ds_base = lane_addr + C::DS_COL + (grp ? C::DS_SHIFT : 0);
 #pragma unroll
-      for (int u = 0; u < C::UR; u += 2) {
+      for (int lp = 0; lp < C::PA; ++lp) {
+        if (pr0 + lp >= pr1) break;
+        const int u = 2 * (pr0 + lp), ul = 2 * lp;  // union row, local accumulator row
         uint32_t sa[C::UCW], sb_[C::UCW], pa_[C::UCW], pb_[C::UCW];
         const uint32_t ca = lane_addr + u * kHCP + uc;
         ld_row<C::UCW>(ca, sa);
@@ -376,12 +416,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                                         __fadd2_rn(make_float2(__uint_as_float(pa_[z]), __uint_as_float(pa_[z + 1])), nD));
           const float2 dsb = __fmul2_rn(make_float2(__uint_as_float(sb_[z]), __uint_as_float(sb_[z + 1])),
                                         __fadd2_rn(make_float2(__uint_as_float(pb_[z]), __uint_as_float(pb_[z + 1])), nD));
-          acc[u][z / 2] = __fadd2_rn(acc[u][z / 2], dsa);
-          acc[u + 1][z / 2] = __fadd2_rn(acc[u + 1][z / 2], dsb);
+          acc[ul][z / 2] = __fadd2_rn(acc[ul][z / 2], dsa);
+          acc[ul + 1][z / 2] = __fadd2_rn(acc[ul + 1][z / 2], dsb);
           da[z / 2] = pack_bf16(dsa.x, dsa.y);
           db[z / 2] = pack_bf16(dsb.x, dsb.y);
         }
-        const uint32_t prow = lane_addr + C::DS_COL + u * (kHCP / 2);
+        const uint32_t prow = ds_base + u * (kHCP / 2);
         st_zero12(prow);
         st_zero12(prow + kHCP / 2);
         st_row<C::UCW / 2>(prow + zb, da);
@@ -392,7 +432,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(ds_full);
       if (tq) qtrace(p, it, 11);
-      // ---- epilogue: dQ = scale * sum of partial accumulators -> bf16, TMA-stored via smem
+      if (grp) continue;
+      // ---- epilogue (group 0): dQ = scale * sum of partial accumulators -> bf16, TMA stores
       mbar_wait(dq_full, ph);
       if (tq) qtrace(p, it, 12);
       tc_fence_after();
@@ -430,8 +471,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {  // queries past the map / band edge are clipped by the TMA unit
-        tma_store_4d(&tm_dq, ostage, 0, g.j0 + 4 * quarter, g.i0 - p.q_row0, g.bh);
-        tma_store_4d(&tm_dq, ostage + 1024, 0, g.j0 + 4 * quarter, g.i0 - p.q_row0 + 4, g.bh);
+        tma_store_4d(&tm_dq, ostage, 0, j0 + 4 * quarter, i0 - p.q_row0, bh);
+        tma_store_4d(&tm_dq, ostage + 1024, 0, j0 + 4 * quarter, i0 - p.q_row0 + 4, bh);
         bulk_commit();
       }
       if (tq) qtrace(p, it, 14);
