@@ -19,6 +19,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
+# development experiments only (e.g. NA2D_NVCC_EXTRA=-DNA2D_EXP=1); pair with build(force=True)
+FLAGS += os.environ.get("NA2D_NVCC_EXTRA", "").split()
 
 
 def _sources():

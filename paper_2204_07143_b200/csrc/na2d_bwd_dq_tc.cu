@@ -34,7 +34,8 @@ using namespace sm100;
 using namespace tc;
 
 constexpr int kStages = 2;
-constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-5 / 6-9 elementwise groups 0 / 1
+constexpr int kGroups = 3;     // elementwise warp groups (each covers the 4 TMEM lane quarters)
+constexpr int kThreads = 64 + kGroups * 128;  // warp 0 TMA, warp 1 MMA, warps 2.. elementwise
 constexpr int kQAcc = 3;       // independent dQ accumulators
 constexpr int kDP_COL = 256;   // dP accumulator columns
 
@@ -52,12 +53,19 @@ struct CfgQ {
   static constexpr int UR = 4 + L - 1;
   static constexpr int NSUB = UR * kHCP;
   static constexpr int UCW = L + 5;
-  // union row pairs split between the two elementwise warps of a TMEM lane quarter; each group
-  // writes its dS rows over its own consumed S rows: row u at DS_COL + u*12 (+ DS_SHIFT for
-  // group 1's rows), so the dQ MMA's K-steps from DS_KS1 on read DS_SHIFT columns further
-  static constexpr int PAIRS = UR / 2, PA = (PAIRS + 1) / 2;
-  static constexpr int DS_SHIFT = PA * kHCP, DS_KS1 = 3 * PA;
-  static_assert(2 * PA * kHCP == 16 * DS_KS1, "group boundary on a K-step boundary");
+  // union row pairs split between the kGroups elementwise warps of a TMEM lane quarter: group g
+  // takes pairs [pr0(g), pr0(g+1)).  Each group writes its dS rows over its own consumed S rows
+  // (row u at DS_COL + u*12 + shift(g), shift(g) = pr0(g)*24), so dQ MMA K-step ks (16 keys; a
+  // row pair is 3 K-steps) reads from column ks*8 + shift(group of pair ks/3)
+  static constexpr int PAIRS = UR / 2;
+  static constexpr int PA = (PAIRS + kGroups - 1) / kGroups;  // max pairs of a group
+  __host__ __device__ static constexpr int pr0(int g) { return g * PAIRS / kGroups; }
+  __host__ __device__ static constexpr int ds_shift_of_ks(int ks) {
+    int g = 0;
+    while (g + 1 < kGroups && pr0(g + 1) <= ks / 3) ++g;
+    return pr0(g) * kHCP;
+  }
+  static_assert(2 * kHCP == 3 * 16, "a row pair is 3 K-steps");
   static constexpr int DS_COL = 0;         // dS (bf16 pairs) over consumed S columns
   static constexpr int Q_COL = kDP_COL;    // dQ partial accumulators in the dP columns (dead after pass 2)
   static_assert(kDP_COL + NSUB <= 512 && Q_COL + kQAcc * kD <= 512, "TMEM budget");
@@ -72,8 +80,8 @@ struct CfgQ {
   static constexpr int TBL_OFF = kStages * STAGE_BYTES;
   static constexpr int OUT_OFF = (TBL_OFF + BiasTable<L>::FLOATS * 4 + 1023) / 1024 * 1024;  // dQ staging
   static constexpr int DB_OFF = OUT_OFF + 4 * 2048;
-  static constexpr int DP_OFF = DB_OFF + ((16 * TT * TT * 4 + 255) / 256) * 256;  // partial D exchange
-  static constexpr int TI_OFF = DP_OFF + 2 * 128 * 4;
+  static constexpr int DP_OFF = DB_OFF + ((8 * kGroups * TT * TT * 4 + 255) / 256) * 256;  // partial D
+  static constexpr int TI_OFF = DP_OFF + kGroups * 128 * 4;
   static constexpr int BAR_OFF = TI_OFF + kStages * 64;
   static_assert(sizeof(TileInfoQ) <= 64, "TileInfoQ");
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
@@ -122,7 +130,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(sp_full, 1);
-    mbar_init(ds_full, 8);
+    mbar_init(ds_full, 4 * kGroups);
     mbar_init(dq_full, 1);
     mbar_init(tmem_free, 4);
     fence_barrier_init();
@@ -132,7 +140,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&tm_v);
     tma_prefetch(&tm_dq);
   }
-  for (int c = threadIdx.x; c < 16 * C::TT * C::TT; c += kThreads) s_db[c] = 0.f;
+  for (int c = threadIdx.x; c < 8 * kGroups * C::TT * C::TT; c += kThreads) s_db[c] = 0.f;
   if (warp == 0) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
@@ -238,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int sb = 0; sb < 2; ++sb) {
             const uint32_t base = tmem + ((uint32_t)(16 * sb) << 16);
             const int rb = sb ? rb1 : rb0;
-            mma_ts(base + C::Q_COL + (ks % kQAcc) * kD, base + C::DS_COL + ks * 8 + (ks >= C::DS_KS1 ? C::DS_SHIFT : 0),
+            mma_ts(base + C::Q_COL + (ks % kQAcc) * kD, base + C::DS_COL + ks * 8 + C::ds_shift_of_ks(ks),
                    sdesc_sw64(k_addr + rb * kHCP * kRowBytes + ks * 16 * kRowBytes), idesc_q, ks >= kQAcc);
           }
         mma_commit(dq_full);
@@ -248,10 +256,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) qtrace(p, it, 4);
     }
   } else {
-    // ================= elementwise (warps 2..5 / 6..9 -> TMEM lane quarters 2,3,0,1): group grp
-    // takes union row pairs [pr0, pr1) of every tile; group 0 also runs the epilogue
+    // ================= elementwise (warps 2.. -> TMEM lane quarter warp % 4): group grp takes union
+    // row pairs [pr0, pr1) of every tile; group 0 also runs the epilogue
     const int quarter = warp & 3, grp = (warp - 2) >> 2;
-    const int pr0 = grp ? C::PA : 0, pr1 = grp ? C::PAIRS : C::PA;
+    const int pr0 = C::pr0(grp), pr1 = C::pr0(grp + 1);
     const int half = lane >> 4, r = (lane >> 2) & 3, c = lane & 3;
     const int gtid = threadIdx.x - 64;
     float *s_dpart = (float *)(smem + C::DP_OFF);
@@ -263,6 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // distinct cells (no intra-instruction address conflicts, no other warp contending), but
     // different (u, z) of different lanes do meet, so the adds stay atomic (RED to shared)
     float *my_db = s_db + ((grp * 4 + quarter) * 2 + half) * C::TT * C::TT;
+    constexpr int kEw = kGroups * 128;  // elementwise threads
     uint8_t *ostage = smem + C::OUT_OFF + quarter * 2048;
     // dRPB accumulator in union coordinates for the current (class, head) and its geometry
     float2 acc[2 * C::PA][C::UCW / 2];  // local rows: union row 2 * pr0 + u
@@ -292,20 +301,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int z = 0; z < C::UCW / 2; ++z) acc[u][z] = make_float2(0.f, 0.f);
     };
-    auto commit_head = [&](int head) {  // sum of the 16 private tables -> partials[cta][head]; clear
-      named_bar_sync(1, 256);
+    auto commit_head = [&](int head) {  // sum of the private tables -> partials[cta][head]; clear
+      named_bar_sync(1, kEw);
       if (head >= 0 && p.drpb_part)
-        for (int e = gtid; e < C::TT * C::TT; e += 256) {
+        for (int e = gtid; e < C::TT * C::TT; e += kEw) {
           float v = 0.f;
 #pragma unroll
-          for (int w = 0; w < 16; ++w) {
+          for (int w = 0; w < 8 * kGroups; ++w) {
             v += s_db[w * C::TT * C::TT + e];
             s_db[w * C::TT * C::TT + e] = 0.f;
           }
           float *dst = &p.drpb_part[((size_t)blockIdx.x * p.heads + head) * C::TT * C::TT + e];
           *dst += p.scale * v;
         }
-      named_bar_sync(1, 256);
+      named_bar_sync(1, kEw);
     };
     int it = 0;
     for (int t = t_begin; t < t_end; ++t, ++it) {
@@ -328,9 +337,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (p.rpb && cur_key >= 0) flush();
         if (h != cur_head) {
           if (p.rpb) commit_head(cur_head);
-          named_bar_sync(1, 256);
-          BiasTable<L>::build(tbl, p.rpb, h, Lw, sl2, gtid, 256);
-          named_bar_sync(1, 256);
+          named_bar_sync(1, kEw);
+          BiasTable<L>::build(tbl, p.rpb, h, Lw, sl2, gtid, kEw);
+          named_bar_sync(1, kEw);
           cur_head = h;
         }
         cur_key = key;
@@ -370,10 +379,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         float2 da = make_float2(0.f, 0.f), db = make_float2(0.f, 0.f);
 #pragma unroll
         for (int z = 0; z < C::UCW; z += 2) {
+          const float2 tta = make_float2(ta[z], ta[z + 1]), ttb = make_float2(tb[z], tb[z + 1]);
           const float2 xa = __fadd2_rn(__ffma2_rn(make_float2(__uint_as_float(sa[z]), __uint_as_float(sa[z + 1])),
-                                                  sl2x2, make_float2(ta[z], ta[z + 1])), nlse2x2);
+                                                  sl2x2, tta), nlse2x2);
           const float2 xb = __fadd2_rn(__ffma2_rn(make_float2(__uint_as_float(sb_[z]), __uint_as_float(sb_[z + 1])),
-                                                  sl2x2, make_float2(tb[z], tb[z + 1])), nlse2x2);
+                                                  sl2x2, ttb), nlse2x2);
           const float2 Pa = make_float2(ex2(xa.x), ex2(xa.y)), Pb = make_float2(ex2(xb.x), ex2(xb.y));
           da = __ffma2_rn(Pa, make_float2(__uint_as_float(pa_[z]), __uint_as_float(pa_[z + 1])), da);
           db = __ffma2_rn(Pb, make_float2(__uint_as_float(pb_[z]), __uint_as_float(pb_[z + 1])), db);
@@ -388,8 +398,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // D over the whole window: the two groups' partial sums, added in a fixed order
       s_dpart[grp * 128 + quarter * 32 + lane] = Dq;
-      named_bar_sync(2 + quarter, 64);
-      Dq = s_dpart[quarter * 32 + lane] + s_dpart[128 + quarter * 32 + lane];
+      named_bar_sync(2 + quarter, 32 * kGroups);
+      Dq = 0.f;
+#pragma unroll
+      for (int g2 = 0; g2 < kGroups; ++g2) Dq += s_dpart[g2 * 128 + quarter * 32 + lane];
       if (qvalid && grp == 0) p.D[qi] = Dq;
       if (tq) qtrace(p, it, 10);
       tc_wait_st();
@@ -397,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // the consumed S/P columns (the dQ MMA's A operand)
       const int zb = uc >> 1;
       const float2 nD = make_float2(-Dq, -Dq);
-      const uint32_t ds_base = lane_addr + C::DS_COL + (grp ? C::DS_SHIFT : 0);
+      const uint32_t ds_base = lane_addr + C::DS_COL + pr0 * kHCP;
 #pragma unroll
       for (int lp = 0; lp < C::PA; ++lp) {
         if (pr0 + lp >= pr1) break;
@@ -437,37 +449,43 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(dq_full, ph);
       if (tq) qtrace(p, it, 12);
       tc_fence_after();
-      uint32_t o[32];  // partial accumulators summed one at a time (register pressure)
-      tmem_ld32(lane_addr + C::Q_COL, o);
-      tc_wait_ld();
+      // dQ in two 16-column halves (register pressure): partial accumulators summed, scaled,
+      // packed into the SW64 staging row of query (r, c) of block `half` (row R of the 1 KB box;
+      // 16-byte chunk z at z ^ (R/2 % 4))
+      const int R = r * 4 + c;
+      uint8_t *orow = ostage + half * 1024 + R * 64;
+      uint32_t o[2][16];
 #pragma unroll
-      for (int a = 1; a < kQAcc; ++a) {
-        uint32_t oa[32];
-        tmem_ld32(lane_addr + C::Q_COL + a * kD, oa);
-        tc_wait_ld();
+      for (int hh = 0; hh < 2; ++hh) {
+        tmem_ld16(lane_addr + C::Q_COL + 16 * hh, o[hh]);
 #pragma unroll
-        for (int z = 0; z < 32; ++z) o[z] = __float_as_uint(__uint_as_float(o[z]) + __uint_as_float(oa[z]));
+        for (int a = 1; a < kQAcc; ++a) {
+          uint32_t oa[16];
+          tmem_ld16(lane_addr + C::Q_COL + a * kD + 16 * hh, oa);
+          tc_wait_ld();
+#pragma unroll
+          for (int z = 0; z < 16; ++z) o[hh][z] = __float_as_uint(__uint_as_float(o[hh][z]) + __uint_as_float(oa[z]));
+        }
       }
-#pragma unroll
-      for (int z = 0; z < 32; ++z) o[z] = __float_as_uint(__uint_as_float(o[z]) * p.scale);
+      tc_wait_ld();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tmem_free);
       if (tq) qtrace(p, it, 13);
       if (lane == 0) bulk_wait_read0();  // this warp's previous store has left the staging
       __syncwarp();
-      {
-        // query (r, c) of block `half` is row R of the 1 KB box; SW64: 16-byte chunk z at z ^ (R/2 % 4)
-        const int R = r * 4 + c;
-        uint8_t *row = ostage + half * 1024 + R * 64;
 #pragma unroll
-        for (int z = 0; z < 4; ++z)
-          *(uint4 *)(row + 16 * ((z ^ (R >> 1)) & 3)) =
-              make_uint4(pack_bf16(__uint_as_float(o[8 * z]), __uint_as_float(o[8 * z + 1])),
-                         pack_bf16(__uint_as_float(o[8 * z + 2]), __uint_as_float(o[8 * z + 3])),
-                         pack_bf16(__uint_as_float(o[8 * z + 4]), __uint_as_float(o[8 * z + 5])),
-                         pack_bf16(__uint_as_float(o[8 * z + 6]), __uint_as_float(o[8 * z + 7])));
-      }
+      for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+        for (int z2 = 0; z2 < 2; ++z2) {
+          const int z = 2 * hh + z2;
+          const uint32_t *v = o[hh] + 8 * z2;
+          *(uint4 *)(orow + 16 * ((z ^ (R >> 1)) & 3)) = make_uint4(
+              pack_bf16(__uint_as_float(v[0]) * p.scale, __uint_as_float(v[1]) * p.scale),
+              pack_bf16(__uint_as_float(v[2]) * p.scale, __uint_as_float(v[3]) * p.scale),
+              pack_bf16(__uint_as_float(v[4]) * p.scale, __uint_as_float(v[5]) * p.scale),
+              pack_bf16(__uint_as_float(v[6]) * p.scale, __uint_as_float(v[7]) * p.scale));
+        }
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {  // queries past the map / band edge are clipped by the TMA unit
