@@ -73,6 +73,7 @@ struct CfgK {
 struct BwdKParams {
   int B, heads, H, W, q_rows, q_row0, kv_rows, kv_row0;
   int tiles_h, tiles_w, num_tiles;
+  int shift_cols;  // last two key tile columns start at W-L-16 and W-16 (key_col0)
   int tma_lsd;  // LSE / D halos by TMA (W * 4 bytes 16-byte aligned) instead of lane loads
   float scale;
   const float *rpb, *lse, *D;
@@ -96,6 +97,15 @@ __device__ __forceinline__ int inv_hi(int p, int n, int L, int lo, int hi) {
   return (L >= n || p >= n - L) ? hi - 1 : min(hi - 1, p + ns);
 }
 
+// Column origin of key tile column tcol.  Normally 16 tcol; for L = 7 and W = 5, 6 mod 16 (>= 37) the
+// second-to-last tile would see a 25-column query halo (its last keys reach the right clamp zone),
+// so the last two tiles are moved to end at W-L-1 and W-1 (overlapping keys are computed twice,
+// identically).  The host (key_tile_cols) checks every tile's halo against the pitch.
+__device__ __forceinline__ int key_col0(const BwdKParams &p, int tcol, int L) {
+  if (p.shift_cols && tcol >= p.tiles_w - 2) return tcol == p.tiles_w - 1 ? p.W - kTQW : p.W - L - kTQW;
+  return tcol * kTQW;
+}
+
 struct KTile {
   int bh, kr0, kc0;   // key tile origin (global row, column)
   int qr0, qc0;       // query halo origin (global)
@@ -111,7 +121,7 @@ __device__ __forceinline__ KTile ktile(const BwdKParams &p, int t) {
   g.bh = t / per;
   const int rem = t - g.bh * per;
   g.kr0 = p.kv_row0 + (rem / p.tiles_w) * kTQH;
-  g.kc0 = (rem % p.tiles_w) * kTQW;
+  g.kc0 = key_col0(p, rem % p.tiles_w, L);
   const int q_end = p.q_row0 + p.q_rows, kv_end = p.kv_row0 + p.kv_rows;
   g.qr0 = inv_lo(min(g.kr0, kv_end - 1), p.H, L, p.q_row0, q_end);
   // even origin: (qc0 & 3) + uc is even, so LSE / D pairs are 8-byte aligned (LDS.64)
@@ -608,6 +618,8 @@ cudaError_t launch_dkdv_t(const Geo &g, const void *q, const void *k, const void
   p.tiles_h = (g.kv_rows + kTQH - 1) / kTQH;
   p.tiles_w = (g.W + kTQW - 1) / kTQW;
   p.num_tiles = BH * p.tiles_h * p.tiles_w;
+  p.shift_cols = 0;
+  if (max_query_halo_width(g, false) > QP) p.shift_cols = 1;
   p.scale = g.scale;
   p.rpb = rpb;
   p.lse = lse;
@@ -621,9 +633,12 @@ cudaError_t launch_dkdv_t(const Geo &g, const void *q, const void *k, const void
   return cudaGetLastError();
 }
 
-// widest query halo over the key tile columns (host replica of inv_lo / inv_hi)
-int max_query_halo_width(const Geo &g) {
-  const int L = g.L, W = g.W, len = wlen(W, L);
+}  // namespace
+
+// widest query halo over the key tile columns (host replica of inv_lo / inv_hi and key_col0), with
+// the standard (shift = false) or shifted (shift = true) column origins
+int max_query_halo_width(const Geo &g, bool shift) {
+  const int L = g.L, W = g.W, len = wlen(W, L), tw = (W + tc::kTQW - 1) / tc::kTQW;
   auto lo = [&](int p) {
     int i = p - L + 1 > 0 ? p - L + 1 : 0;
     while (i < W && wstart(i, W, L) + len - 1 < p) ++i;
@@ -635,7 +650,10 @@ int max_query_halo_width(const Geo &g) {
     return i;
   };
   int w = 0;
-  for (int c0 = 0; c0 < W; c0 += tc::kTQW) {
+  for (int t = 0; t < tw; ++t) {
+    int c0 = t * tc::kTQW;
+    if (shift && t >= tw - 2) c0 = t == tw - 1 ? W - tc::kTQW : W - L - tc::kTQW;
+    if (c0 < 0) return 1 << 20;
     const int c1 = c0 + tc::kTQW - 1 < W - 1 ? c0 + tc::kTQW - 1 : W - 1;
     const int ww = hi(c1) - (lo(c0) & ~1) + 1;  // the kernel rounds the halo origin down to even
     w = ww > w ? ww : w;
@@ -643,13 +661,17 @@ int max_query_halo_width(const Geo &g) {
   return w;
 }
 
-}  // namespace
+bool tc_dkdv_supported(const Geo &g) {
+  return max_query_halo_width(g, false) <= 24 || max_query_halo_width(g, true) <= 24;
+}
+
 
 cudaError_t tc_backward_dkdv(const Geo &g, const void *q, const void *k, const void *v, const float *rpb,
                              const float *lse, const void *dout, const float *D, void *dk, void *dv,
                              cudaStream_t st) {
-  // the query halo of a 16-column key tile is at most 16 + 2NS + 1 <= 23 columns for L <= 7
-  if (max_query_halo_width(g) > 24) return cudaErrorNotSupported;
+  // the query halo of a 16-column key tile is at most 16 + 2NS + 1 <= 23 columns away from the right
+  // clamp zone; tiles reaching it are shifted (key_col0)
+  if (!tc_dkdv_supported(g)) return cudaErrorNotSupported;
   switch (g.L) {
     case 3: return launch_dkdv_t<3, 24>(g, q, k, v, rpb, lse, dout, D, dk, dv, st);
     case 5: return launch_dkdv_t<5, 24>(g, q, k, v, rpb, lse, dout, D, dk, dv, st);

@@ -60,6 +60,8 @@ struct BwdQParams {
 };
 
 int dq_grid(const Geo &g);
+int max_query_halo_width(const Geo &g, bool shift);
+bool tc_dkdv_supported(const Geo &g);
 cudaError_t tc_backward_dkdv(const Geo &g, const void *q, const void *k, const void *v, const float *rpb,
                              const float *lse, const void *dout, const float *D, void *dk, void *dv,
                              cudaStream_t st);

@@ -40,6 +40,8 @@ SMALL = [
     Shape("wide3x70k3", 1, 1, 3, 70, 32, 3),
     Shape("sa7x7k7", 4, 4, 7, 7, 32, 7),         # NAT-Tiny stage-4 geometry (k = map: full SA)
     Shape("tall61x9k7", 1, 1, 61, 9, 32, 7),
+    Shape("w37k7", 2, 2, 11, 37, 32, 7),         # W = 5 mod 16: shifted key tile columns (B2)
+    Shape("w54k7", 1, 2, 9, 54, 32, 7),          # W = 6 mod 16
 ]
 
 
