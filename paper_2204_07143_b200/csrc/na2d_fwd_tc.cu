@@ -13,15 +13,20 @@
 //     O_s = P_s V[rb_s..]     (M=64, N=32, K=NSUB)   tcgen05.mma TS (P from TMEM)
 // Softmax.  TMEM lane quarter q holds the 4 x 4 query block at tile columns [4q, 4q+4) of both
 // sub-tiles; the union of its windows is (4+L-1) rows x (4+L-1) columns of S (loaded as L+5
-// even-aligned columns).  Per element: x = s*scale*log2e + T[cell] where T is a shared-memory
-// table of the head's relative positional bias B[h][p-i+L-1][q-j+L-1] pre-multiplied by
-// scale*log2e, with -inf outside the query's own window (one table per column-clamp class, plus
-// an all -inf row for rows outside the window).  Exact single-pass softmax (the whole window
-// sits in one tile): pass 1 max (x written back in place), pass 2 P = exp2(x - max) packed to
-// bf16 into TMEM, aliased over S columns already consumed.  O lands in dead S columns.
-// Pipeline.  Persistent CTAs (one per SM), contiguous tile ranges.  Warp 0: TMA (3-stage ring);
-// warp 1: MMA issue, software-pipelined one tile ahead; warps 2-5 and 6-9: two softmax +
-// epilogue groups that ping-pong between two TMEM slots of 256 columns.
+// even-aligned columns; the exponentials skip the two outside the union).  Per element pair, in
+// packed fp32x2 arithmetic: x = s*scale*log2e + T[cell], T a shared-memory table of the head's
+// relative positional bias B[h][p-i+L-1][q-j+L-1] pre-multiplied by scale*log2e, with
+// -inf outside the query's own window (one table per column-clamp class, plus an all -inf row for
+// rows outside the window; two copies shifted by one column so every lane reads 8-byte aligned
+// pairs).  Exact two-pass softmax (the whole window sits in one tile): pass 1 computes x and the
+// row max (FMNMX3) and stores x compacted to 12 columns per union row over consumed S columns;
+// pass 2 writes P = exp2(x - max) as bf16 pairs in place, one union row pair at a time, each pair
+// released at once to the PV MMAs (which accumulate O in the columns the compaction freed), so
+// PV overlaps pass 2.
+// Pipeline.  Persistent CTAs (one per SM), contiguous head-major tile ranges.  Warp 0: tile
+// descriptions + TMA (3-stage ring); warp 1: MMA issue (QK of tile t, then PV of tile t-1 pair by
+// pair); warps 2-5 and 6-9: two softmax + epilogue groups that ping-pong between two TMEM slots
+// of 256 columns.
 #include <math.h>
 
 #include <mutex>
@@ -47,11 +52,12 @@ template <int L>
 struct Cfg {
   static constexpr int HR = kTQH + L - 1;      // halo rows
   static constexpr int UR = 4 + L - 1;         // union rows per sub-tile
+  static constexpr int PAIRS = UR / 2;         // union row pairs (3 PV K-steps each)
   static constexpr int NSUB = UR * kHCP;       // S columns per sub-tile (keys)
-  static constexpr int UCW = L + 5;            // union columns loaded (even)
   static constexpr int P_COL = 0;              // P (bf16 pairs) aliased over consumed S
-  static constexpr int O_COL = NSUB / 2;       // O partial accumulators in dead S columns
+  static constexpr int O_COL = NSUB / 2;       // O partial accumulators past the compacted x / P
   static_assert(O_COL + kOAcc * kD <= 256, "slot budget");
+  static_assert(2 * kHCP == 3 * 16, "a union row pair is 3 PV K-steps");
   static constexpr int KV_ROWS = HR * kHCP;
   static constexpr int Q_BYTES = 128 * kRowBytes;
   static constexpr int KV_BYTES = KV_ROWS * kRowBytes;
@@ -59,42 +65,62 @@ struct Cfg {
   static_assert(STAGE_BYTES % 1024 == 0, "stages must stay 1 KB aligned (swizzled TMA / UMMA)");
   static constexpr int TT = 2 * L - 1;
   static constexpr int TROWS = TT + 1;                             // + all -inf row
-  static constexpr int TBL_FLOATS = L * TROWS * kTblStride;        // one table set (per group)
-  static constexpr int TBL_OFF = kStages * STAGE_BYTES;
-  static constexpr int BAR_OFF = TBL_OFF + 2 * TBL_FLOATS * 4;
+  static constexpr int TBL_FLOATS = L * TROWS * kTblStride;        // one table copy
+  static constexpr int TBL_OFF = kStages * STAGE_BYTES;            // 2 groups x 2 parity copies
+  static constexpr int TI_OFF = TBL_OFF + 4 * TBL_FLOATS * 4;
+  static constexpr int BAR_OFF = TI_OFF + kStages * 64;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
+  static_assert(SMEM <= 232448, "shared memory");
 };
 
 struct FwdParams {
-  int heads, H, W, q_rows, q_row0, kv_row0;
+  int B, heads, H, W, q_rows, q_row0, kv_row0;
   int tiles_h, tiles_w, num_tiles;
   float scale_log2;  // scale * log2(e)
   const float *rpb;  // [heads][TT][TT] or null
   __nv_bfloat16 *out;
   float *lse;
-  long long *trace;  // debug timeline (na2d_debug_set_trace) or null
+  long long *trace;  // debug timeline (na2d_debug_set_trace, builds with -DNA2D_TRACE) or null
 };
 
+// Per-stage tile description, written by the producer before it arms full[stage].
+struct FTile {
+  int bh, head, i0, j0, hr0, hc0;
+  int rb[2];  // first halo row of sub-tile s (relative to hr0)
+  int uc[4];  // union origin of lane quarter q: bit 0 = first needed column odd, rest = even column
+};
+static_assert(sizeof(FTile) <= 64, "FTile");
+
+#ifdef NA2D_TRACE
 // Debug timeline: trace[(cta * kTraceTiles + it) * kTraceEv + ev] = clock64() for CTAs < 4.
 constexpr int kTraceTiles = 32, kTraceEv = 16;
 __device__ __forceinline__ void trace_ev(const FwdParams &p, int it, int ev) {
   if (p.trace && blockIdx.x < 4 && it < kTraceTiles)
     p.trace[((size_t)blockIdx.x * kTraceTiles + it) * kTraceEv + ev] = clock64();
 }
+#else
+__device__ __forceinline__ void trace_ev(const FwdParams &, int, int) {}
+#endif
 
-struct TileGeo {
-  int bh, i0, j0, hr0, hc0;
-};
-__device__ __forceinline__ TileGeo tile_geo(const FwdParams &p, int t, int L) {
-  TileGeo g;
-  const int per = p.tiles_h * p.tiles_w;
-  g.bh = t / per;
-  const int rem = t - g.bh * per;
-  g.i0 = p.q_row0 + (rem / p.tiles_w) * kTQH;
-  g.j0 = (rem % p.tiles_w) * kTQW;
-  g.hr0 = wstart(g.i0, p.H, L);
-  g.hc0 = wstart(g.j0, p.W, L);
-  return g;
+// Pass 2 of one union row: P = exp2(x - max) for the needed columns of the row's 12 loaded union
+// columns (ODD: columns 1..10, else 0..9; the others are outside every lane's window), bf16 pairs.
+template <bool ODD>
+__device__ __forceinline__ void p_row(const uint32_t (&x)[12], float mx, float2 &sum, uint32_t (&pp)[6]) {
+  const float2 nm = make_float2(-mx, -mx);
+#pragma unroll
+  for (int z = 0; z < 6; ++z) {
+    const float2 a = __fadd2_rn(make_float2(__uint_as_float(x[2 * z]), __uint_as_float(x[2 * z + 1])), nm);
+    float2 e;
+    if (ODD) {
+      e.x = z == 0 ? 0.f : ex2(a.x);
+      e.y = z == 5 ? 0.f : ex2(a.y);
+    } else {
+      e.x = z == 5 ? 0.f : ex2(a.x);
+      e.y = z == 5 ? 0.f : ex2(a.y);
+    }
+    sum = __fadd2_rn(sum, e);
+    pp[z] = pack_bf16(e.x, e.y);
+  }
 }
 
 template <int L>
@@ -105,10 +131,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   float *tables = (float *)(smem + C::TBL_OFF);
+  FTile *tinfo = (FTile *)(smem + C::TI_OFF);
   uint64_t *bars = (uint64_t *)(smem + C::BAR_OFF);
   uint64_t *full = bars, *empty = bars + kStages;
-  uint64_t *s_full = bars + 2 * kStages, *p_full = s_full + 2, *o_full = s_full + 4, *tmem_free = s_full + 6;
-  uint32_t *tmem_slot = (uint32_t *)(bars + 2 * kStages + 8);
+  uint64_t *s_full = bars + 2 * kStages, *o_full = s_full + 2, *tmem_free = s_full + 4;
+  uint64_t *p_pair = s_full + 6;  // [slot][pair]: union row pair of P written by the 4 warps
+  uint32_t *tmem_slot = (uint32_t *)(p_pair + 2 * C::PAIRS);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int t_begin = (int)((long)p.num_tiles * blockIdx.x / gridDim.x);
@@ -122,9 +150,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&s_full[s], 1);
-      mbar_init(&p_full[s], 4);
       mbar_init(&o_full[s], 1);
       mbar_init(&tmem_free[s], 4);
+      for (int k = 0; k < C::PAIRS; ++k) mbar_init(&p_pair[s * C::PAIRS + k], 4);
     }
     fence_barrier_init();
     tma_prefetch(&tm_q);
@@ -138,14 +166,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    // ================= TMA producer
-    if (elect_one()) {
-      int it = 0;
-      for (int t = t_begin; t < t_end; ++t, ++it) {
-        const int s = it % kStages;
-        mbar_wait_sleep(&empty[s], ((it / kStages) & 1) ^ 1, 1024);
-        trace_ev(p, it, 0);
-        const TileGeo g = tile_geo(p, t, L);
+    // ================= producer: tile description + TMA (Q 4x4 blocks, K / V halo)
+    int it = 0;
+    const int per = p.tiles_h * p.tiles_w;
+    for (int t = t_begin; t < t_end; ++t, ++it) {
+      const int s = it % kStages;
+      mbar_wait_sleep(&empty[s], ((it / kStages) & 1) ^ 1, 1024);
+      if (lane == 0) trace_ev(p, it, 0);
+      // head-major tile order: consecutive tiles share the head (bias table rebuilds are rare)
+      const int u = t / per, rem = t - u * per;
+      const int h = u / p.B, b = u - h * p.B;
+      const int bh = b * p.heads + h;
+      const int i0 = p.q_row0 + (rem / p.tiles_w) * kTQH, j0 = (rem % p.tiles_w) * kTQW;
+      const int hr0 = wstart(i0, p.H, L), hc0 = wstart(j0, p.W, L);
+      FTile *ti = tinfo + s;
+      if (lane < 2) ti->rb[lane] = wstart(min(i0 + 4 * lane, q_end - 1), p.H, L) - hr0;
+      if (lane < 4) ti->uc[lane] = wstart(min(j0 + 4 * lane, p.W - 1), p.W, L) - hc0;
+      if (lane == 0) {
+        ti->bh = bh;
+        ti->head = h;
+        ti->i0 = i0;
+        ti->j0 = j0;
+        ti->hr0 = hr0;
+        ti->hc0 = hc0;
+      }
+      __syncwarp();
+      if (elect_one()) {
         uint8_t *st = smem + s * C::STAGE_BYTES;
         mbar_expect_tx(&full[s], C::STAGE_BYTES);
         // Q: sub-tile sb, quarter qb -> 16 rows = 4x4 block (rows i0+4sb.., cols j0+4qb..)
@@ -153,31 +199,33 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int sb = 0; sb < 2; ++sb)
 #pragma unroll
           for (int qb = 0; qb < 4; ++qb)
-            tma_load_4d(st + (64 * sb + 16 * qb) * kRowBytes, &tm_q, &full[s], 0, g.j0 + 4 * qb,
-                        g.i0 - p.q_row0 + 4 * sb, g.bh);
-        tma_load_4d(st + C::Q_BYTES, &tm_k, &full[s], 0, g.hc0, g.hr0 - p.kv_row0, g.bh);
-        tma_load_4d(st + C::Q_BYTES + C::KV_BYTES, &tm_v, &full[s], 0, g.hc0, g.hr0 - p.kv_row0, g.bh);
+            tma_load_4d(st + (64 * sb + 16 * qb) * kRowBytes, &tm_q, &full[s], 0, j0 + 4 * qb, i0 - p.q_row0 + 4 * sb, bh);
+        tma_load_4d(st + C::Q_BYTES, &tm_k, &full[s], 0, hc0, hr0 - p.kv_row0, bh);
+        tma_load_4d(st + C::Q_BYTES + C::KV_BYTES, &tm_v, &full[s], 0, hc0, hr0 - p.kv_row0, bh);
       }
+      __syncwarp();
     }
   } else if (warp == 1) {
-    // ================= MMA issuer (QK of tile it, then PV of tile it-1)
+    // ================= MMA issuer: QK of tile it, then PV of tile it-1 one union row pair at a
+    // time as the elementwise warps release it (the PV overlaps pass 2)
     constexpr uint32_t idesc_qk = idesc_bf16(64, C::NSUB, false);
     constexpr uint32_t idesc_pv = idesc_bf16(64, kD, true);
     const int n = t_end - t_begin;
+    int prb0 = 0, prb1 = 0;
     for (int it = 0; it <= n; ++it) {
+      int rb0 = 0, rb1 = 0;
       if (it < n) {
         const int s = it % kStages, slot = it & 1;
-        const TileGeo g = tile_geo(p, t_begin + it, L);
-        mbar_wait_sleep(&full[s], (it / kStages) & 1, 64);
+        mbar_wait(&full[s], (it / kStages) & 1);
+        rb0 = tinfo[s].rb[0];
+        rb1 = tinfo[s].rb[1];
         if (lane == 0) trace_ev(p, it, 1);
-        mbar_wait_sleep(&tmem_free[slot], ((it >> 1) & 1) ^ 1, 64);
+        mbar_wait(&tmem_free[slot], ((it >> 1) & 1) ^ 1);
         if (lane == 0) trace_ev(p, it, 2);
         tc_fence_after();
         const uint32_t q_addr = smem_u32(smem + s * C::STAGE_BYTES);
         const uint32_t k_addr = q_addr + C::Q_BYTES;
         if (elect_one()) {
-          const int rb0 = wstart(min(g.i0, q_end - 1), p.H, L) - g.hr0;
-          const int rb1 = wstart(min(g.i0 + 4, q_end - 1), p.H, L) - g.hr0;
 #pragma unroll
           for (int k = 0; k < kD / 16; ++k)
 #pragma unroll
@@ -190,59 +238,77 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (it > 0) {
         const int pi = it - 1, s = pi % kStages, slot = pi & 1;
-        const TileGeo g = tile_geo(p, t_begin + pi, L);
-        mbar_wait_sleep(&p_full[slot], (pi >> 1) & 1, 64);
-        if (lane == 0) trace_ev(p, pi, 3);
-        tc_fence_after();
         const uint32_t v_addr = smem_u32(smem + s * C::STAGE_BYTES) + C::Q_BYTES + C::KV_BYTES;
-        if (elect_one()) {
-          const int rb0 = wstart(min(g.i0, q_end - 1), p.H, L) - g.hr0;
-          const int rb1 = wstart(min(g.i0 + 4, q_end - 1), p.H, L) - g.hr0;
-          // 2 sub-tiles x kOAcc partial accumulators = independent MMA chains, interleaved
+#pragma unroll 1
+        for (int k = 0; k < C::PAIRS; ++k) {
+          mbar_wait(&p_pair[slot * C::PAIRS + k], (pi >> 1) & 1);
+          tc_fence_after();
+          if (elect_one()) {
+            // 2 sub-tiles x kOAcc partial accumulators = independent MMA chains, interleaved
 #pragma unroll
-          for (int ks = 0; ks < C::NSUB / 16; ++ks)
+            for (int k3 = 0; k3 < 3; ++k3)
 #pragma unroll
-            for (int sb = 0; sb < 2; ++sb) {
-              const uint32_t base = tmem + ((uint32_t)(16 * sb) << 16) + slot * 256;
-              mma_ts(base + C::O_COL + (ks % kOAcc) * kD, base + C::P_COL + ks * 8,
-                     sdesc_sw64(v_addr + (sb ? rb1 : rb0) * kHCP * kRowBytes + ks * 16 * kRowBytes), idesc_pv,
-                     ks >= kOAcc);
+              for (int sb = 0; sb < 2; ++sb) {
+                const int ks = 3 * k + k3;
+                const uint32_t base = tmem + ((uint32_t)(16 * sb) << 16) + slot * 256;
+                mma_ts(base + C::O_COL + k3 * kD, base + C::P_COL + ks * 8,
+                       sdesc_sw64(v_addr + (sb ? prb1 : prb0) * kHCP * kRowBytes + ks * 16 * kRowBytes), idesc_pv,
+                       k > 0);
+              }
+            if (k == C::PAIRS - 1) {
+              mma_commit(&o_full[slot]);
+              mma_commit(&empty[s]);
             }
-          mma_commit(&o_full[slot]);
-          mma_commit(&empty[s]);
+          }
+          __syncwarp();
         }
-        __syncwarp();
+        if (lane == 0) trace_ev(p, pi, 3);
       }
+      prb0 = rb0;
+      prb1 = rb1;
     }
   } else {
-    // ================= softmax + epilogue groups
+    // ================= softmax + epilogue groups (ping-pong between the two TMEM slots)
     const int grp = (warp - 2) >> 2;  // 0: warps 2-5, 1: warps 6-9
     const int quarter = warp & 3;
     const int half = lane >> 4, r = (lane >> 2) & 3, c = lane & 3;
-    float *tbl = tables + grp * C::TBL_FLOATS;
+    float *tbl = tables + grp * 2 * C::TBL_FLOATS;  // this group's two parity copies
     const int gtid = threadIdx.x - 64 - grp * 128;  // 0..127 within the group
     const int Lh = wlen(p.H, L), Lw = wlen(p.W, L);
+    const float2 sl2x2 = make_float2(p.scale_log2, p.scale_log2);
     int cur_head = -1;
     for (int it = grp; it < t_end - t_begin; it += 2) {
-      const int slot = it & 1;
+      const int slot = it & 1, stage = it % kStages;
       const uint32_t ph = (it >> 1) & 1;
-      const TileGeo g = tile_geo(p, t_begin + it, L);
-      const int h = g.bh % p.heads;
-      if (h != cur_head) {  // (re)build this group's masked, pre-scaled bias tables
+      mbar_wait(&full[stage], (it / kStages) & 1);  // tile description
+      const FTile &ti = tinfo[stage];
+      const int bh = ti.bh, h = ti.head, i0 = ti.i0, j0 = ti.j0, hr0 = ti.hr0, hc0 = ti.hc0;
+      const int rb = ti.rb[half], ucr = ti.uc[quarter];
+      if (h != cur_head) {  // (re)build this group's masked, pre-scaled bias tables (two parity copies:
+        // copy x holds column b at kTblOff + x + b, so every lane's row start is 8-byte aligned)
         named_bar_sync(1 + grp, 128);
-        BiasTable<L>::build(tbl, p.rpb, h, Lw, p.scale_log2, gtid, 128);
+        for (int e = gtid; e < 2 * C::TBL_FLOATS; e += 128) {
+          const int x = e >= C::TBL_FLOATS, e2 = e - x * C::TBL_FLOATS;
+          const int dc = e2 / (C::TROWS * kTblStride);
+          const int rr = (e2 / kTblStride) % C::TROWS;
+          const int cb = e2 % kTblStride - kTblOff - x;
+          float v = -INFINITY;
+          if (rr < C::TT && cb >= dc && cb < dc + Lw) v = p.rpb ? __ldg(&p.rpb[(h * C::TT + rr) * C::TT + cb]) * p.scale_log2 : 0.f;
+          tbl[e] = v;
+        }
         named_bar_sync(1 + grp, 128);
         cur_head = h;
       }
       // this thread's query and window geometry
-      const int i = g.i0 + 4 * half + r, j = g.j0 + 4 * quarter + c;
+      const int i = i0 + 4 * half + r, j = j0 + 4 * quarter + c;
       const int ic = min(i, q_end - 1), jc = min(j, p.W - 1);
       const int si = wstart(ic, p.H, L), sj = wstart(jc, p.W, L);
-      const int rb = wstart(min(g.i0 + 4 * half, q_end - 1), p.H, L) - g.hr0;
-      const int uc = (wstart(min(g.j0 + 4 * quarter, p.W - 1), p.W, L) - g.hc0) & ~1;  // warp-uniform
+      const bool odd = ucr & 1;                                      // warp-uniform
+      const int uc = ucr & ~1;
       const int dc = sj - jc + L - 1;                                // column-clamp class
-      const int bcol0 = g.hc0 + uc - jc + L - 1;                     // bias column of union col 0
-      const float *tcls = tbl + dc * C::TROWS * kTblStride + kTblOff + bcol0;
+      const int bcol0 = hc0 + uc - jc + L - 1;                       // bias column of union col 0
+      const int cp = bcol0 & 1;                                      // parity copy: aligned row start
+      const float *tcls = tbl + cp * C::TBL_FLOATS + dc * C::TROWS * kTblStride + kTblOff + cp + bcol0;
       const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16) + slot * 256;
 
       const bool tr = quarter == 2 && lane == 0;
@@ -250,10 +316,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&s_full[slot], ph);
       if (tr) trace_ev(p, it, 5);
       tc_fence_after();
-      const float sl2 = p.scale_log2;
-      // ---- pass 1 (rolled, two union rows per iteration: both x16 TMEM loads in flight):
-      // x = s*scale*log2e + T (masked, pre-scaled bias); row max; x written back in place (the 4
-      // extra columns of each x16 store are outside this lane's union; TMEM lanes are private)
+      // ---- pass 1 (two union rows per iteration, both x16 TMEM loads in flight):
+      // x = s*scale*log2e + T (masked, pre-scaled bias) in packed fp32x2; row max; x written back
+      // in place (the 4 extra columns of each x16 store are rewritten unchanged)
       float mx = -INFINITY;
 #pragma unroll 1
       for (int u = 0; u < C::UR; u += 2) {
@@ -261,65 +326,82 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t ca = lane_addr + u * kHCP + uc;
         tmem_ld16(ca, ra);
         tmem_ld16(ca + kHCP, rbv);
-        const int pr = g.hr0 + rb + u;  // key row of union row u
+        const int pr = hr0 + rb + u;  // key row of union row u
         const bool rva = (unsigned)(pr - si) < (unsigned)Lh, rvb = (unsigned)(pr + 1 - si) < (unsigned)Lh;
-        const float *ta = tcls + (rva ? pr - ic + L - 1 : C::TT) * kTblStride;
-        const float *tb = tcls + (rvb ? pr + 1 - ic + L - 1 : C::TT) * kTblStride;
+        const float2 *ta = (const float2 *)(tcls + (rva ? pr - ic + L - 1 : C::TT) * kTblStride);
+        const float2 *tb = (const float2 *)(tcls + (rvb ? pr + 1 - ic + L - 1 : C::TT) * kTblStride);
+        float2 ba[6], bb[6];
+#pragma unroll
+        for (int z = 0; z < 6; ++z) {
+          ba[z] = ta[z];
+          bb[z] = tb[z];
+        }
         tc_wait_ld();
-        float xa[C::UCW], xb[C::UCW];
+        float2 xa[6], xb[6];
 #pragma unroll
-        for (int z = 0; z < C::UCW; ++z) {
-          xa[z] = fmaf(__uint_as_float(ra[z]), sl2, ta[z]);
-          xb[z] = fmaf(__uint_as_float(rbv[z]), sl2, tb[z]);
+        for (int z = 0; z < 6; ++z) {
+          xa[z] = __ffma2_rn(make_float2(__uint_as_float(ra[2 * z]), __uint_as_float(ra[2 * z + 1])), sl2x2, ba[z]);
+          xb[z] = __ffma2_rn(make_float2(__uint_as_float(rbv[2 * z]), __uint_as_float(rbv[2 * z + 1])), sl2x2, bb[z]);
         }
-        mx = fmaxf(mx, fmaxf(tree_max<C::UCW>(xa), tree_max<C::UCW>(xb)));
+        float m[8];
 #pragma unroll
-        for (int z = 0; z < C::UCW; ++z) {
-          ra[z] = __float_as_uint(xa[z]);
-          rbv[z] = __float_as_uint(xb[z]);
+        for (int z = 0; z < 3; ++z) {
+          m[z] = fmax3(xa[2 * z].x, xa[2 * z].y, xa[2 * z + 1].x);
+          m[3 + z] = fmax3(xa[2 * z + 1].y, xb[2 * z].x, xb[2 * z].y);
         }
-        tmem_st16(ca, ra);
-        tmem_st16(ca + kHCP, rbv);
+        m[6] = fmax3(xb[1].x, xb[1].y, xb[3].x);
+        m[7] = fmax3(xb[3].y, xb[5].x, xb[5].y);
+        mx = fmax3(mx, fmax3(m[0], m[1], m[2]), fmax3(fmax3(m[3], m[4], m[5]), m[6], m[7]));
+        // compact store: x of union row u at columns [12u, 12u+12) -- over S rows <= u/2, already
+        // consumed -- so columns [NSUB/2, 256) are free for the O accumulators during pass 2
+        uint32_t xs[24];
+#pragma unroll
+        for (int z = 0; z < 6; ++z) {
+          xs[2 * z] = __float_as_uint(xa[z].x);
+          xs[2 * z + 1] = __float_as_uint(xa[z].y);
+          xs[12 + 2 * z] = __float_as_uint(xb[z].x);
+          xs[13 + 2 * z] = __float_as_uint(xb[z].y);
+        }
+        st_row<24>(lane_addr + u * 12, xs);
       }
       tc_wait_st();
       if (tr) trace_ev(p, it, 6);
-      // ---- pass 2 (rolled, two rows per iteration): P = exp2(x - max) -> bf16 pairs over the
-      // consumed S columns.  Each halo row of P is first zeroed, then the union span written.
-      float sum = 0.f;
+      // ---- pass 2 (two rows per iteration): P = exp2(x - max) -> bf16 pairs over the consumed S
+      // columns (each halo row of P zeroed, then the union span written); after each row pair the
+      // warp releases it to the PV MMAs
+      float2 sum2 = make_float2(0.f, 0.f);
       const int zb = uc >> 1;  // packed column where the union span starts (warp-uniform)
 #pragma unroll 1
       for (int u = 0; u < C::UR; u += 2) {
-        uint32_t ra[16], rbv[16];
-        const uint32_t ca = lane_addr + u * kHCP + uc;
-        tmem_ld16(ca, ra);
-        tmem_ld16(ca + kHCP, rbv);
+        uint32_t xs[24];
+        ld_row<24>(lane_addr + u * 12, xs);
         tc_wait_ld();
-        uint32_t pa[C::UCW / 2], pb[C::UCW / 2];
-        float ea[C::UCW], eb[C::UCW];
+        uint32_t ra[12], rbv[12];
 #pragma unroll
-        for (int z = 0; z < C::UCW; ++z) {
-          ea[z] = ex2(__uint_as_float(ra[z]) - mx);
-          eb[z] = ex2(__uint_as_float(rbv[z]) - mx);
+        for (int z = 0; z < 12; ++z) {
+          ra[z] = xs[z];
+          rbv[z] = xs[12 + z];
         }
-#pragma unroll
-        for (int z = 0; z < C::UCW; z += 2) {
-          pa[z / 2] = pack_bf16_alu(ea[z], ea[z + 1]);
-          pb[z / 2] = pack_bf16_alu(eb[z], eb[z + 1]);
+        uint32_t pa[6], pb[6];
+        if (odd) {
+          p_row<true>(ra, mx, sum2, pa);
+          p_row<true>(rbv, mx, sum2, pb);
+        } else {
+          p_row<false>(ra, mx, sum2, pa);
+          p_row<false>(rbv, mx, sum2, pb);
         }
-        sum += tree_sum<C::UCW>(ea) + tree_sum<C::UCW>(eb);
         const uint32_t prow = lane_addr + C::P_COL + u * (kHCP / 2);
         st_zero12(prow);
         st_zero12(prow + kHCP / 2);
-        st_row<C::UCW / 2>(prow + zb, pa);
-        st_row<C::UCW / 2>(prow + kHCP / 2 + zb, pb);
+        st_row<6>(prow + zb, pa);
+        st_row<6>(prow + kHCP / 2 + zb, pb);
+        tc_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_pair[slot * C::PAIRS + u / 2]);
       }
-      tc_wait_st();
-      if (tr) trace_ev(p, it, 14);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[slot]);
+      const float sum = sum2.x + sum2.y;
       if (tr) trace_ev(p, it, 7);
-      if (lane == 0) trace_ev(p, it, 10 + quarter);
       // ---- epilogue: O / sum -> bf16, LSE
       mbar_wait(&o_full[slot], ph);
       if (tr) trace_ev(p, it, 8);
@@ -343,7 +425,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(&tmem_free[slot]);
       if (i < q_end && j < p.W) {
         const float inv = 1.f / sum;
-        const size_t qi = ((size_t)g.bh * p.q_rows + (i - p.q_row0)) * p.W + j;
+        const size_t qi = ((size_t)bh * p.q_rows + (i - p.q_row0)) * p.W + j;
         uint4 *dst = (uint4 *)(p.out + qi * kD);
 #pragma unroll
         for (int z = 0; z < kD; z += 8)
@@ -380,6 +462,7 @@ cudaError_t launch_fwd(const Geo &g, const void *q, const void *k, const void *v
       !make_tmap_bf16_4d(&tv, v, kD, g.W, g.kv_rows, BH, kHCP, C::HR))
     return cudaErrorInvalidValue;
   FwdParams p;
+  p.B = g.B;
   p.heads = g.heads;
   p.H = g.H;
   p.W = g.W;

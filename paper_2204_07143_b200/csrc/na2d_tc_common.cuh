@@ -41,52 +41,69 @@ struct BiasTable {
   }
 };
 
-// N consecutive TMEM columns of this warp's 32 lanes -> registers (N in {4,5,6,8,10,12})
+// N consecutive TMEM columns of this warp's 32 lanes -> registers (N = 16a + 8b + 4c + 2d, the
+// loads all issued before the caller's tcgen05.wait::ld)
 template <int N>
 __device__ __forceinline__ void ld_row(uint32_t addr, uint32_t (&v)[N]) {
-  uint32_t a8[8];
-  if constexpr (N >= 8) {
-    tmem_ld8(addr, a8);
+  int o = 0;
 #pragma unroll
-    for (int z = 0; z < 8; ++z) v[z] = a8[z];
-  }
-  constexpr int R = N >= 8 ? N - 8 : N;
-  constexpr int B = N >= 8 ? 8 : 0;
-  if constexpr (R == 4) {
-    uint32_t a4[4];
-    tmem_ld4(addr + B, a4);
+  for (; o + 16 <= N; o += 16) {
+    uint32_t a[16];
+    tmem_ld16(addr + o, a);
 #pragma unroll
-    for (int z = 0; z < 4; ++z) v[B + z] = a4[z];
-  } else if constexpr (R == 2) {
-    uint32_t a2[2];
-    tmem_ld2(addr + B, a2);
-    v[B] = a2[0];
-    v[B + 1] = a2[1];
-  } else {
-    static_assert(R == 0, "row width");
+    for (int z = 0; z < 16; ++z) v[o + z] = a[z];
   }
+  if constexpr (N % 16 >= 8) {
+    constexpr int B = N / 16 * 16;
+    uint32_t a[8];
+    tmem_ld8(addr + B, a);
+#pragma unroll
+    for (int z = 0; z < 8; ++z) v[B + z] = a[z];
+  }
+  if constexpr (N % 8 >= 4) {
+    constexpr int B = N / 8 * 8;
+    uint32_t a[4];
+    tmem_ld4(addr + B, a);
+#pragma unroll
+    for (int z = 0; z < 4; ++z) v[B + z] = a[z];
+  }
+  if constexpr (N % 4 >= 2) {
+    constexpr int B = N / 4 * 4;
+    uint32_t a[2];
+    tmem_ld2(addr + B, a);
+    v[B] = a[0];
+    v[B + 1] = a[1];
+  }
+  static_assert(N % 2 == 0, "row width");
 }
 template <int N>
 __device__ __forceinline__ void st_row(uint32_t addr, const uint32_t (&v)[N]) {
-  if constexpr (N >= 8) {
-    uint32_t a8[8];
+  int o = 0;
 #pragma unroll
-    for (int z = 0; z < 8; ++z) a8[z] = v[z];
-    tmem_st8(addr, a8);
+  for (; o + 16 <= N; o += 16) {
+    uint32_t a[16];
+#pragma unroll
+    for (int z = 0; z < 16; ++z) a[z] = v[o + z];
+    tmem_st16(addr + o, a);
   }
-  constexpr int B = N >= 8 ? 8 : 0;
-  constexpr int R = N - B;
-  if constexpr (R >= 4) {
-    uint32_t a4[4] = {v[B], v[B + 1], v[B + 2], v[B + 3]};
-    tmem_st4(addr + B, a4);
+  if constexpr (N % 16 >= 8) {
+    constexpr int B = N / 16 * 16;
+    uint32_t a[8];
+#pragma unroll
+    for (int z = 0; z < 8; ++z) a[z] = v[B + z];
+    tmem_st8(addr + B, a);
   }
-  constexpr int B2 = B + (R >= 4 ? 4 : 0);
-  constexpr int R2 = N - B2;
-  if constexpr (R2 >= 2) {
-    uint32_t a2[2] = {v[B2], v[B2 + 1]};
-    tmem_st2(addr + B2, a2);
+  if constexpr (N % 8 >= 4) {
+    constexpr int B = N / 8 * 8;
+    uint32_t a[4] = {v[B], v[B + 1], v[B + 2], v[B + 3]};
+    tmem_st4(addr + B, a);
   }
-  if constexpr ((R2 & 1) == 1) tmem_st1(addr + N - 1, v[N - 1]);
+  if constexpr (N % 4 >= 2) {
+    constexpr int B = N / 4 * 4;
+    uint32_t a[2] = {v[B], v[B + 1]};
+    tmem_st2(addr + B, a);
+  }
+  if constexpr (N % 2 == 1) tmem_st1(addr + N - 1, v[N - 1]);
 }
 __device__ __forceinline__ void st_zero12(uint32_t addr) {
   const uint32_t z8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
