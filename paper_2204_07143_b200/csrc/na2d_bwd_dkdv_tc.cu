@@ -82,7 +82,9 @@ struct BwdKParams {
 };
 // debug timeline: trace[(cta * 32 + chunk) * 32 + ev] for CTAs < 4 (chunk = CTA-global chunk index)
 __device__ __forceinline__ void ktrace(const BwdKParams &p, int c, int ev) {
+#ifdef NA2D_TRACE
   if (p.trace && blockIdx.x < 4 && c < 32) p.trace[((size_t)blockIdx.x * 32 + c) * 32 + ev] = clock64();
+#endif
 }
 
 // first / last query row (column) in [lo, hi) whose clamped window holds key row (column) p.

@@ -92,6 +92,9 @@ __device__ __forceinline__ TileOrder::Tile decode(const BwdQParams &p, int t) { 
 // debug timeline: trace[4096 + (cta / 37 * 32 + tile) * 32 + ev] for CTAs 0, 37, 74, 111 (tile = CTA-local tile index;
 // the first 4096 slots belong to B2)
 __device__ __forceinline__ void qtrace_gt(const BwdQParams &p, int slot) {  // wall clock into tile row 0
+#ifndef NA2D_TRACE
+  return;
+#endif
   if (p.trace && blockIdx.x % 37 == 0) {
     uint64_t gt;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
@@ -99,6 +102,9 @@ __device__ __forceinline__ void qtrace_gt(const BwdQParams &p, int slot) {  // w
   }
 }
 __device__ __forceinline__ void qtrace(const BwdQParams &p, int it, int ev) {
+#ifndef NA2D_TRACE
+  return;
+#endif
   if (p.trace && blockIdx.x % 37 == 0 && it < 32) p.trace[4096 + ((size_t)(blockIdx.x / 37) * 32 + it) * 32 + ev] = clock64();
 }
 
@@ -208,11 +214,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait_sleep(&full[s], (it / kStages) & 1, 64);
       const int rb0 = tinfo[s].rb[0], rb1 = tinfo[s].rb[1];
       if (lane == 0) qtrace(p, it, 0);
+#ifdef NA2D_TRACE
       if (lane == 0 && p.trace && blockIdx.x % 37 == 0 && it < 32) {  // wall clock beside the SM clock
         uint64_t gt;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
         p.trace[4096 + ((size_t)(blockIdx.x / 37) * 32 + it) * 32 + 15] = (long long)gt;
       }
+#endif
       mbar_wait_sleep(tmem_free, ph ^ 1, 64);
       if (lane == 0) qtrace(p, it, 1);
       tc_fence_after();

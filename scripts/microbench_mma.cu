@@ -152,7 +152,7 @@ void run_chunk(const char *name) {
          cudaGetErrorString(e));
 }
 
-int main() {
+int main_old() {
   run_chunk<1>("B2 chunk: S/dP only");
   run_chunk<2>("B2 chunk: dV/dK only");
   run_chunk<3>("B2 chunk: S/dP + dV/dK");
@@ -167,5 +167,101 @@ int main() {
   run<128, 32, true, 4>("TS M=128 N=32 (4 chains)");
   run<128, 64, true, 4>("TS M=128 N=64 (4 chains)");
   run<64, 64, true, 4>("TS M=64 N=64 (4 chains)");
+  run<64, 32, false, 4>("SS M=64 N=32 (4 chains)");
+  run<128, 32, false, 4>("SS M=128 N=32 (4 chains)");
+  run<64, 48, false, 4>("SS M=64 N=48 (4 chains)");
+  run<128, 96, false, 2>("SS M=128 N=96 (2 chains)");
+  run<64, 96, false, 2>("SS M=64 N=96 (2 chains)");
+  return 0;
+}
+
+// TS M=64 N=32 MMA stream (warp 0, 3 chains, like the forward's PV) while NLD other warps hammer
+// TMEM with tcgen05.ld/st x16 on disjoint columns (like the softmax warps of the other group).
+template <int NLD, bool ST>
+__global__ void contention_bench(int iters, long long *cyc) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint64_t &bar = *(uint64_t *)(smem + 80 * 1024);
+  uint32_t &slot = *(uint32_t *)(smem + 80 * 1024 + 8);
+  volatile int &done = *(volatile int *)(smem + 80 * 1024 + 16);
+  const int warp = threadIdx.x / 32;
+  for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) ((uint32_t *)smem)[i] = 0x3c003c00u;
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+    done = 0;
+  }
+  if (warp == 0) tmem_alloc<512>(&slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (warp == 0) {
+    constexpr uint32_t id = idesc_bf16(64, 32, true);
+    const uint32_t b = smem_u32(smem + 16384);
+    long long t0 = clock64();
+    if (elect_one()) {
+      for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int c = 0; c < 6; ++c)
+          mma_ts(tmem + ((uint32_t)(16 * (c & 1)) << 16) + 128 + (c >> 1) * 32,
+                 tmem + ((uint32_t)(16 * (c & 1)) << 16) + (it % 8) * 8,
+                 sdesc_sw64(b + (it % 8) * 1024), id, it > 0);
+      }
+      mma_commit(&bar);
+    }
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+    done = 1;
+  } else if (warp >= 4 && warp < 4 + NLD) {
+    const uint32_t la = tmem + ((uint32_t)((warp & 3) * 32) << 16) + 256 + (warp >= 8 ? 128 : 0);
+    uint32_t r[16];
+    float acc = 0.f;
+    while (!done) {
+#pragma unroll 1
+      for (int k = 0; k < 8; ++k) {
+        tmem_ld16(la + k * 16, r);
+        tc_wait_ld();
+        acc += __uint_as_float(r[3]);
+        if (ST) {
+          tmem_st16(la + k * 16, r);
+        }
+      }
+      if (ST) tc_wait_st();
+    }
+    if (acc == 1234.5f) cyc[1000] = 1;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+template <int NLD, bool ST>
+void run_cont(const char *name) {
+  long long *cyc = nullptr, host[4] = {0, 0, 0, 0};
+  cudaError_t e0 = cudaMalloc(&cyc, 2000 * 8);
+  auto k = contention_bench<NLD, ST>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  const int iters = 2000;
+  k<<<148, 384, 100 * 1024>>>(iters, cyc);
+  cudaError_t e = cudaDeviceSynchronize();
+  cudaMemcpy(host, cyc, 8, cudaMemcpyDeviceToHost);
+  printf("%-34s %7.1f cyc/MMA (%s / %s)\n", name, (double)host[0] / (iters * 6), cudaGetErrorString(e0),
+         cudaGetErrorString(e));
+  cudaFree(cyc);
+}
+
+int main() {
+  run_cont<0, false>("TS M=64 N=32 x6 chains, idle");
+  run_cont<4, false>("... + 4 warps tcgen05.ld");
+  run_cont<8, false>("... + 8 warps tcgen05.ld");
+  run_cont<4, true>("... + 4 warps ld+st");
+  run_cont<8, true>("... + 8 warps ld+st");
   return 0;
 }
