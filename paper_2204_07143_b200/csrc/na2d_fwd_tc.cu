@@ -38,9 +38,6 @@
 #include "na2d_tc_common.cuh"
 #include "na2d_tmap.cuh"
 
-#ifndef NA2D_EXP
-#define NA2D_EXP 0
-#endif
 
 namespace na2d {
 namespace {
@@ -51,11 +48,11 @@ using namespace tc;
 constexpr int kStagesQK = 3;      // Q + K halo ring (released when the QK MMAs complete)
 constexpr int kStagesV = 3;       // V halo ring (released when the PV MMAs complete)
 constexpr int kTInfo = 8;         // tile-description ring (>= 5: see the producer)
-constexpr int kThreads = 352;     // 11 warps
+constexpr int kThreads = 384;     // 12 warps
 // The SM sub-partition scheduler favours the highest warp id among eligible warps: the producer and
 // MMA-issue warps take the two highest ids so the busy elementwise warps sharing their
 // sub-partitions (warp % 4) never delay a TMA or MMA issue.
-constexpr int kProducerWarp = 8, kMmaWarp = 9, kProducerVWarp = 10;
+constexpr int kProducerWarp = 8, kMmaWarp = 9, kProducerVWarp = 10, kPvWarp = 11;
 constexpr int kOAcc = 3;           // independent PV accumulators (summed in the epilogue)
 
 template <int L>
@@ -79,7 +76,8 @@ struct Cfg {
   static constexpr int TBL_FLOATS = L * TROWS * kTblStride;        // one table copy
   static constexpr int TBL_OFF = V_OFF + kStagesV * KV_BYTES;      // 2 groups x 2 parity copies
   static constexpr int TI_OFF = TBL_OFF + 4 * TBL_FLOATS * 4;
-  static constexpr int BAR_OFF = TI_OFF + kTInfo * 64;
+  static constexpr int VI_OFF = TI_OFF + kTInfo * 64;                // V ring: halo row offsets
+  static constexpr int BAR_OFF = VI_OFF + kStagesV * 16;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
   static_assert(SMEM <= 232448, "shared memory");
 };
@@ -122,12 +120,7 @@ __device__ __forceinline__ void p_row(const uint32_t (&x)[12], float mx, float2 
   for (int z = 0; z < 6; ++z) {
     const float2 a = __fadd2_rn(make_float2(__uint_as_float(x[2 * z]), __uint_as_float(x[2 * z + 1])), nm);
     float2 e;
-#if NA2D_EXP == 2
-    e = a;
-    if (0) {
-#else
     if (ODD) {
-#endif
       e.x = z == 0 ? 0.f : ex2(a.x);
       e.y = z == 5 ? 0.f : ex2(a.y);
     } else {
@@ -148,6 +141,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   float *tables = (float *)(smem + C::TBL_OFF);
   FTile *tinfo = (FTile *)(smem + C::TI_OFF);
+  int *vinfo = (int *)(smem + C::VI_OFF);  // [V slot][2]: rb of the two sub-tiles
   uint64_t *bars = (uint64_t *)(smem + C::BAR_OFF);
   uint64_t *full = bars, *empty = bars + kStagesQK;                     // Q/K ring
   uint64_t *full_v = bars + 2 * kStagesQK, *empty_v = full_v + kStagesV;  // V ring
@@ -248,6 +242,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int bh = b * p.heads + h;
       const int i0 = p.q_row0 + tr * kTQH, j0 = tcol * kTQW;
       if (elect_one()) {
+        const int hr0 = wstart(i0, p.H, L);
+        vinfo[2 * s] = wstart(min(i0, q_end - 1), p.H, L) - hr0;
+        vinfo[2 * s + 1] = wstart(min(i0 + 4, q_end - 1), p.H, L) - hr0;
         mbar_expect_tx(&full_v[s], C::KV_BYTES);
         tma_load_4d(smem + C::V_OFF + s * C::KV_BYTES, &tm_v, &full_v[s], 0, wstart(j0, p.W, L),
                     wstart(i0, p.H, L) - p.kv_row0, bh);
@@ -265,71 +262,70 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == kMmaWarp) {
-    // ================= MMA issuer (whole warp converged, one elected thread issues): QK of tile
-    // it, then PV of tile it-1 one union row pair at a time as the elementwise warps release it
-    // (the PV overlaps pass 2).  Shared-memory descriptors are built once per stage and advanced by
+    // ================= QK issuer (whole warp converged, one elected thread issues): S of tile it
+    // into TMEM slot it & 1 once its Q / K have landed and the slot's previous epilogue has read O.
+    // The PV MMAs have their own issuing warp, so neither stream waits behind the other's
+    // dependencies.  Shared-memory descriptors are built once per stage and advanced by
     // (byte offset >> 4).
     constexpr uint32_t idesc_qk = idesc_bf16(64, C::NSUB, false);
+    for (int it = 0; it < t_end - t_begin; ++it) {
+      const int s = it % kStagesQK, slot = it & 1;
+      mbar_wait(&full[s], (it / kStagesQK) & 1);
+      const int rb0 = tinfo[it % kTInfo].rb[0], rb1 = tinfo[it % kTInfo].rb[1];
+      if (lane == 0) trace_ev(p, it, 1);
+      mbar_wait(&tmem_free[slot], ((it >> 1) & 1) ^ 1);
+      if (lane == 0) trace_ev(p, it, 2);
+      tc_fence_after();
+      const uint64_t dq = sdesc_sw64(smem_u32(smem + s * C::QK_BYTES));
+      const uint64_t dk = dq + (C::Q_BYTES >> 4);
+      const uint64_t dk0 = dk + ((rb0 * kHCP * kRowBytes) >> 4), dk1 = dk + ((rb1 * kHCP * kRowBytes) >> 4);
+      const uint32_t d0 = tmem + slot * 256, d1 = d0 + ((uint32_t)16 << 16);
+      if (elect_one()) {  // two independent accumulation chains (sub-tiles) interleaved
+        mma_ss(d0, dq, dk0, idesc_qk, 0);
+        mma_ss(d1, dq + (4096 >> 4), dk1, idesc_qk, 0);
+        mma_ss(d0, dq + (32 >> 4), dk0 + (32 >> 4), idesc_qk, 1);
+        mma_ss(d1, dq + ((4096 + 32) >> 4), dk1 + (32 >> 4), idesc_qk, 1);
+        mma_commit(&s_full[slot]);
+        mma_commit(&empty[s]);
+      }
+      __syncwarp();
+    }
+  } else if (warp == kPvWarp) {
+    // ================= PV issuer: O of tile it (slot it & 1) one union row pair at a time as the
+    // elementwise warps release it (the PV overlaps pass 2)
     constexpr uint32_t idesc_pv = idesc_bf16(64, kD, true);
-    const int n = t_end - t_begin;
-    int prb0 = 0, prb1 = 0;
-    for (int it = 0; it <= n; ++it) {
-      int rb0 = 0, rb1 = 0;
-      if (it < n) {
-        const int s = it % kStagesQK, slot = it & 1;
-        mbar_wait(&full[s], (it / kStagesQK) & 1);
-        rb0 = tinfo[it % kTInfo].rb[0];
-        rb1 = tinfo[it % kTInfo].rb[1];
-        if (lane == 0) trace_ev(p, it, 1);
-        mbar_wait(&tmem_free[slot], ((it >> 1) & 1) ^ 1);
-        if (lane == 0) trace_ev(p, it, 2);
+    for (int it = 0; it < t_end - t_begin; ++it) {
+      const int s = it % kStagesV, slot = it & 1;
+      mbar_wait(&full_v[s], (it / kStagesV) & 1);
+      const int rb0 = vinfo[2 * s], rb1 = vinfo[2 * s + 1];
+      const uint64_t dv = sdesc_sw64(smem_u32(smem + C::V_OFF + s * C::KV_BYTES));
+      const uint64_t dv0 = dv + ((rb0 * kHCP * kRowBytes) >> 4), dv1 = dv + ((rb1 * kHCP * kRowBytes) >> 4);
+      const uint32_t b0 = tmem + slot * 256, b1 = b0 + ((uint32_t)16 << 16);
+      // fully unrolled: every descriptor / TMEM address below is the tile's base + an immediate, so
+      // each pair's issue is a short independent burst (no dependent address chain per pair)
+#pragma unroll
+      for (int k = 0; k < C::PAIRS; ++k) {
+        mbar_wait(&p_pair[slot * C::PAIRS + k], (it >> 1) & 1);
+        if (lane == 0) trace_ev(p, it, 19 + k);
         tc_fence_after();
-        const uint64_t dq = sdesc_sw64(smem_u32(smem + s * C::QK_BYTES));
-        const uint64_t dk = dq + (C::Q_BYTES >> 4);
-        const uint64_t dk0 = dk + ((rb0 * kHCP * kRowBytes) >> 4), dk1 = dk + ((rb1 * kHCP * kRowBytes) >> 4);
-        const uint32_t d0 = tmem + slot * 256, d1 = d0 + ((uint32_t)16 << 16);
-        if (elect_one()) {  // two independent accumulation chains (sub-tiles) interleaved
-          mma_ss(d0, dq, dk0, idesc_qk, 0);
-          mma_ss(d1, dq + (4096 >> 4), dk1, idesc_qk, 0);
-          mma_ss(d0, dq + (32 >> 4), dk0 + (32 >> 4), idesc_qk, 1);
-          mma_ss(d1, dq + ((4096 + 32) >> 4), dk1 + (32 >> 4), idesc_qk, 1);
-          mma_commit(&s_full[slot]);
-          mma_commit(&empty[s]);
+        // 2 sub-tiles x kOAcc partial accumulators = independent MMA chains, interleaved
+        constexpr uint32_t acc = 1;
+        if (elect_one()) {
+#pragma unroll
+          for (int k3 = 0; k3 < 3; ++k3) {
+            const int ks = 3 * k + k3;
+            const uint32_t voff = (ks * 16 * kRowBytes) >> 4;
+            mma_ts(b0 + C::O_COL + k3 * kD, b0 + C::P_COL + ks * 8, dv0 + voff, idesc_pv, k > 0 ? acc : 0u);
+            mma_ts(b1 + C::O_COL + k3 * kD, b1 + C::P_COL + ks * 8, dv1 + voff, idesc_pv, k > 0 ? acc : 0u);
+          }
+          if (k == C::PAIRS - 1) {
+            mma_commit(&o_full[slot]);
+            mma_commit(&empty_v[s]);
+          }
         }
         __syncwarp();
       }
-      if (it > 0) {
-        const int pi = it - 1, s = pi % kStagesV, slot = pi & 1;
-        mbar_wait(&full_v[s], (pi / kStagesV) & 1);
-        const uint64_t dv = sdesc_sw64(smem_u32(smem + C::V_OFF + s * C::KV_BYTES));
-        const uint64_t dv0 = dv + ((prb0 * kHCP * kRowBytes) >> 4), dv1 = dv + ((prb1 * kHCP * kRowBytes) >> 4);
-        const uint32_t b0 = tmem + slot * 256, b1 = b0 + ((uint32_t)16 << 16);
-#pragma unroll 1
-        for (int k = 0; k < C::PAIRS; ++k) {
-          mbar_wait(&p_pair[slot * C::PAIRS + k], (pi >> 1) & 1);
-          if (lane == 0) trace_ev(p, pi, 19 + k);
-          tc_fence_after();
-          // 2 sub-tiles x kOAcc partial accumulators = independent MMA chains, interleaved
-          const uint32_t acc = k > 0;
-          if (elect_one()) {
-#pragma unroll
-            for (int k3 = 0; k3 < 3; ++k3) {
-              const int ks = 3 * k + k3;
-              const uint32_t voff = (ks * 16 * kRowBytes) >> 4;
-              mma_ts(b0 + C::O_COL + k3 * kD, b0 + C::P_COL + ks * 8, dv0 + voff, idesc_pv, acc);
-              mma_ts(b1 + C::O_COL + k3 * kD, b1 + C::P_COL + ks * 8, dv1 + voff, idesc_pv, acc);
-            }
-            if (k == C::PAIRS - 1) {
-              mma_commit(&o_full[slot]);
-              mma_commit(&empty_v[s]);
-            }
-          }
-          __syncwarp();
-        }
-        if (lane == 0) trace_ev(p, pi, 3);
-      }
-      prb0 = rb0;
-      prb1 = rb1;
+      if (lane == 0) trace_ev(p, it, 3);
     }
   } else {
     // ================= softmax + epilogue groups (ping-pong between the two TMEM slots)
@@ -394,24 +390,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float2 *tb = (const float2 *)(tcls + (rvb ? pr + 1 - ic + L - 1 : C::TT) * kTblStride);
 #pragma unroll
           for (int z = 0; z < 6; ++z) {
-#if NA2D_EXP == 1
-            t[z] = make_float2(0.f, 0.f);
-            t[6 + z] = make_float2((float)(size_t)ta, (float)(size_t)tb);
-#else
             t[z] = ta[z];
             t[6 + z] = tb[z];
-#endif
           }
         };
-#if NA2D_EXP == 6
-#pragma unroll
-        for (int z = 0; z < 32; ++z) S[0][z] = S[1][z] = __float_as_uint((float)(z + lane));
-#define tmem_ld16_exp(a, b) ((void)0)
-#else
-#define tmem_ld16_exp(a, b) tmem_ld16(a, b)
-#endif
-        tmem_ld16_exp(lane_addr + uc, *reinterpret_cast<uint32_t(*)[16]>(&S[0][0]));
-        tmem_ld16_exp(lane_addr + kHCP + uc, *reinterpret_cast<uint32_t(*)[16]>(&S[0][16]));
+        tmem_ld16(lane_addr + uc, *reinterpret_cast<uint32_t(*)[16]>(&S[0][0]));
+        tmem_ld16(lane_addr + kHCP + uc, *reinterpret_cast<uint32_t(*)[16]>(&S[0][16]));
         load_tbl(0, T[0]);
 #pragma unroll
         for (int k = 0; k < C::PAIRS; ++k) {
@@ -421,8 +405,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_wait_ld();
           if (k + 1 < C::PAIRS) {
             const uint32_t cn = lane_addr + (u + 2) * kHCP + uc;
-            tmem_ld16_exp(cn, *reinterpret_cast<uint32_t(*)[16]>(&S[(k + 1) & 1][0]));
-            tmem_ld16_exp(cn + kHCP, *reinterpret_cast<uint32_t(*)[16]>(&S[(k + 1) & 1][16]));
+            tmem_ld16(cn, *reinterpret_cast<uint32_t(*)[16]>(&S[(k + 1) & 1][0]));
+            tmem_ld16(cn + kHCP, *reinterpret_cast<uint32_t(*)[16]>(&S[(k + 1) & 1][16]));
             load_tbl(u + 2, T[(k + 1) & 1]);
           }
           float2 xa[6], xb[6];
@@ -451,11 +435,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             xs[12 + 2 * z] = __float_as_uint(xb[z].x);
             xs[13 + 2 * z] = __float_as_uint(xb[z].y);
           }
-#if NA2D_EXP != 3
           st_row<24>(lane_addr + u * 12, xs);
-#else
-          if (xs[3] == 0x12345) st_row<24>(lane_addr + u * 12, xs);
-#endif
         }
       }
       tc_wait_st();
@@ -468,19 +448,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int zb = uc >> 1;  // packed column where the union span starts (warp-uniform)
       {
         uint32_t X[2][24];
-#if NA2D_EXP == 4
-#pragma unroll
-        for (int z = 0; z < 24; ++z) X[0][z] = X[1][z] = __float_as_uint(mx - (float)z);
-#define ld_row_exp(a, b) ((void)0)
-#else
-#define ld_row_exp(a, b) ld_row<24>(a, b)
-#endif
-        ld_row_exp(lane_addr, X[0]);
+        ld_row<24>(lane_addr, X[0]);
 #pragma unroll
         for (int k = 0; k < C::PAIRS; ++k) {
           const int u = 2 * k;
           tc_wait_ld();
-          if (k + 1 < C::PAIRS) ld_row_exp(lane_addr + (u + 2) * 12, X[(k + 1) & 1]);
+          if (k + 1 < C::PAIRS) ld_row<24>(lane_addr + (u + 2) * 12, X[(k + 1) & 1]);
           uint32_t ra[12], rbv[12];
 #pragma unroll
           for (int z = 0; z < 12; ++z) {
@@ -503,16 +476,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0 && quarter == 0) trace_ev(p, it, 24 + k - 1);
           }
           const uint32_t prow = lane_addr + C::P_COL + u * (kHCP / 2);
-#if NA2D_EXP == 5
-          if (pa[0] == 0x1234567 && pb[1] == 0x7654321) {
-#else
-          {
-#endif
           st_zero12(prow);
           st_zero12(prow + kHCP / 2);
           st_row<6>(prow + zb, pa);
           st_row<6>(prow + kHCP / 2 + zb, pb);
-          }
         }
         tc_wait_st();
         tc_fence_before();

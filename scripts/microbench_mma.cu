@@ -257,11 +257,124 @@ void run_cont(const char *name) {
   cudaFree(cyc);
 }
 
-int main() {
+int main_old2() {
   run_cont<0, false>("TS M=64 N=32 x6 chains, idle");
   run_cont<4, false>("... + 4 warps tcgen05.ld");
   run_cont<8, false>("... + 8 warps tcgen05.ld");
   run_cont<4, true>("... + 4 warps ld+st");
   run_cont<8, true>("... + 8 warps ld+st");
+  return 0;
+}
+
+// The forward's per-tile tensor sequence: QK (4 SS, M=64 N=240, sub-tiles at lane offsets 0/16)
+// into slot t&1, then PV of the previous tile (30 TS, M=64 N=32, A = P at slot (t-1)&1 columns
+// [0,120), D at [120,216) in 3 chains x 2 sub-tiles).  NLD other warps do TMEM ld/st.
+template <int NLD, bool QK, bool PV, bool MODE_ST = true>
+__global__ void fwd_seq_bench(int iters, long long *cyc) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint64_t &bar = *(uint64_t *)(smem + 90 * 1024);
+  uint32_t &slot = *(uint32_t *)(smem + 90 * 1024 + 8);
+  volatile int &done = *(volatile int *)(smem + 90 * 1024 + 16);
+  const int warp = threadIdx.x / 32;
+  for (int i = threadIdx.x; i < 88 * 1024 / 4; i += blockDim.x) {  // random bf16 pairs in [-2, 2)
+    uint32_t x = (uint32_t)i * 2654435761u + blockIdx.x * 40503u;
+    x ^= x >> 13; x *= 0x5bd1e995u; x ^= x >> 15;
+    ((uint32_t *)smem)[i] = (x & 0x807f807fu) | 0x3f003f00u;
+  }
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+    done = 0;
+  }
+  if (warp == 0) tmem_alloc<512>(&slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (warp == 0) {
+    constexpr uint32_t iqk = idesc_bf16(64, 240, false), ipv = idesc_bf16(64, 32, true);
+    const uint32_t q = smem_u32(smem), k = q + 8192, v = q + 8192 + 21504;
+    long long t0 = clock64();
+    if (elect_one()) {
+      for (int it = 0; it < iters; ++it) {
+        const uint32_t s0 = tmem + (it & 1) * 256, p0 = tmem + ((it + 1) & 1) * 256;
+        if (QK) {
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk)
+#pragma unroll
+            for (int sb = 0; sb < 2; ++sb)
+              mma_ss(s0 + ((uint32_t)(16 * sb) << 16), sdesc_sw64(q + sb * 4096 + kk * 32),
+                     sdesc_sw64(k + sb * 4 * 1536 + kk * 32), iqk, kk);
+        }
+        if (PV) {
+#pragma unroll
+          for (int ks = 0; ks < 15; ++ks)
+#pragma unroll
+            for (int sb = 0; sb < 2; ++sb) {
+              const uint32_t b = p0 + ((uint32_t)(16 * sb) << 16);
+              mma_ts(b + 120 + (ks % 3) * 32, b + ks * 8, sdesc_sw64(v + sb * 4 * 1536 + ks * 1024), ipv, ks >= 3);
+            }
+        }
+      }
+      mma_commit(&bar);
+    }
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+    done = 1;
+  } else if (warp >= 4 && warp < 4 + NLD) {
+    // like the softmax passes: both slots' lanes, two x16 loads in flight, a x16 + x8 store
+    const uint32_t la = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (warp >= 8 ? 256 : 0);
+    uint32_t r[16], r2[16];
+    float acc = 0.f;
+    while (!done) {
+#pragma unroll 1
+      for (int kk = 0; kk < 5; ++kk) {
+        tmem_ld16(la + kk * 24, r);
+        tmem_ld16(la + kk * 24 + 24, r2);
+        tc_wait_ld();
+        acc += __uint_as_float(r[3]) + __uint_as_float(r2[5]);
+        if (MODE_ST) {
+          tmem_st16(la + kk * 16 + 120, r);
+          uint32_t r8[8] = {r2[0], r2[1], r2[2], r2[3], r2[4], r2[5], r2[6], r2[7]};
+          tmem_st8(la + kk * 16 + 136, r8);
+        }
+      }
+      tc_wait_st();
+    }
+    if (acc == 1234.5f) cyc[1000] = 1;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+template <int NLD, bool QK, bool PV, bool MODE_ST = true>
+void run_seq(const char *name) {
+  long long *cyc = nullptr, host[4] = {0, 0, 0, 0};
+  cudaMalloc(&cyc, 2000 * 8);
+  auto k = fwd_seq_bench<NLD, QK, PV, MODE_ST>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  const int iters = 500;
+  k<<<148, 384, 100 * 1024>>>(iters, cyc);
+  cudaError_t e = cudaDeviceSynchronize();
+  cudaMemcpy(host, cyc, 8, cudaMemcpyDeviceToHost);
+  printf("%-40s %7.1f cyc/tile (%s)\n", name, (double)host[0] / iters, cudaGetErrorString(e));
+  cudaFree(cyc);
+}
+
+int main() {
+  run_seq<0, true, false>("fwd seq: QK only");
+  run_seq<0, false, true>("fwd seq: PV only");
+  run_seq<0, true, true>("fwd seq: QK + PV");
+  run_seq<8, true, true, false>("fwd seq: QK + PV, 8 ld warps");
+  run_seq<8, true, true>("fwd seq: QK + PV, 8 ld/st warps");
+  run_seq<4, true, true>("fwd seq: QK + PV, 4 ld/st warps");
   return 0;
 }
