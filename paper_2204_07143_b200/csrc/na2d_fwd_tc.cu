@@ -78,7 +78,7 @@ struct Cfg {
   static constexpr int TI_OFF = TBL_OFF + 4 * TBL_FLOATS * 4;
   static constexpr int VI_OFF = TI_OFF + kTInfo * 64;                // V ring: halo row offsets
   static constexpr int BAR_OFF = VI_OFF + kStagesV * 16;
-  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+  static constexpr int SMEM = BAR_OFF + 320 + 1024;
   static_assert(SMEM <= 232448, "shared memory");
 };
 
@@ -147,7 +147,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t *full_v = bars + 2 * kStagesQK, *empty_v = full_v + kStagesV;  // V ring
   uint64_t *s_full = full_v + 2 * kStagesV, *o_full = s_full + 2, *tmem_free = s_full + 4;
   uint64_t *p_pair = s_full + 6;  // [slot][pair]: union row pair of P written by the 4 warps
-  uint32_t *tmem_slot = (uint32_t *)(p_pair + 2 * C::PAIRS);
+  // tile description it % kTInfo written (the elementwise warps must not wait on full[]: by the time
+  // a slow group gets there, full[] may already have completed the next phase of its stage)
+  uint64_t *ti_full = p_pair + 2 * C::PAIRS;
+  uint32_t *tmem_slot = (uint32_t *)(ti_full + kTInfo);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int t_begin = (int)((long)p.num_tiles * blockIdx.x / gridDim.x);
@@ -159,6 +162,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
+    for (int s = 0; s < kTInfo; ++s) mbar_init(&ti_full[s], 1);
     for (int s = 0; s < kStagesV; ++s) {
       mbar_init(&full_v[s], 1);
       mbar_init(&empty_v[s], 1);
@@ -208,6 +212,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ti->rb[1] = wstart(min(i0 + 4, q_end - 1), p.H, L) - hr0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) ti->uc[q] = wstart(min(j0 + 4 * q, p.W - 1), p.W, L) - hc0;
+        mbar_arrive(&ti_full[it % kTInfo]);  // release: the description above is visible to its waiters
         uint8_t *st = smem + s * C::QK_BYTES;
         mbar_expect_tx(&full[s], C::QK_BYTES);
         // Q: sub-tile sb, quarter qb -> 16 rows = 4x4 block (rows i0+4sb.., cols j0+4qb..)
@@ -338,9 +343,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float2 sl2x2 = make_float2(p.scale_log2, p.scale_log2);
     int cur_head = -1;
     for (int it = grp; it < t_end - t_begin; it += 2) {
-      const int slot = it & 1, stage = it % kStagesQK;
+      const int slot = it & 1;
       const uint32_t ph = (it >> 1) & 1;
-      mbar_wait(&full[stage], (it / kStagesQK) & 1);  // tile description (Q/K of tile it arrived)
+      // tile description of tile it: its ring slot is rewritten (tile it + 8) only after QK(it + 5),
+      // which needs the epilogue of tile it + 3, whose PV is issued after PV(it + 2), i.e. after this
+      // group has read the description of tile it (and processed tile it + 2)
+      mbar_wait(&ti_full[it % kTInfo], (it / kTInfo) & 1);
       const FTile &ti = tinfo[it % kTInfo];
       const int bh = ti.bh, h = ti.head, i0 = ti.i0, j0 = ti.j0, hr0 = ti.hr0, hc0 = ti.hc0;
       const int rb = ti.rb[half], ucr = ti.uc[quarter];

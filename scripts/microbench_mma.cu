@@ -325,6 +325,21 @@ __global__ void fwd_seq_bench(int iters, long long *cyc) {
     long long t1 = clock64();
     if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
     done = 1;
+  } else if (warp >= 4 && warp < 4 + NLD && MODE_ST == false && QK == false) {
+  } else if (warp >= 4 && warp < 4 + NLD && NLD == 7) {
+    // pure ALU / MUFU / LDS load (no TMEM): FFMA2 + ex2 + LDS like the softmax warps
+    float2 a = make_float2(threadIdx.x * 1e-3f, 0.5f), b2 = make_float2(1.0001f, 0.9999f);
+    float e0 = 0.f, e1 = 0.f;
+    const float *sp = (const float *)(smem + (threadIdx.x % 64) * 16);
+    while (!done) {
+#pragma unroll 8
+      for (int kk = 0; kk < 64; ++kk) {
+        a = __ffma2_rn(a, b2, make_float2(sp[kk & 7], sp[(kk + 3) & 7]));
+        e0 += ex2(a.x * 1e-3f);
+        e1 += ex2(a.y * 1e-3f);
+      }
+    }
+    if (e0 + e1 == 1234.5f) cyc[1000] = 1;
   } else if (warp >= 4 && warp < 4 + NLD) {
     // like the softmax passes: both slots' lanes, two x16 loads in flight, a x16 + x8 store
     const uint32_t la = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (warp >= 8 ? 256 : 0);
@@ -376,5 +391,6 @@ int main() {
   run_seq<8, true, true, false>("fwd seq: QK + PV, 8 ld warps");
   run_seq<8, true, true>("fwd seq: QK + PV, 8 ld/st warps");
   run_seq<4, true, true>("fwd seq: QK + PV, 4 ld/st warps");
+  run_seq<7, true, true>("fwd seq: QK + PV, 7 ALU/MUFU/LDS warps");
   return 0;
 }
