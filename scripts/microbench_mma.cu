@@ -326,6 +326,16 @@ __global__ void fwd_seq_bench(int iters, long long *cyc) {
     if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
     done = 1;
   } else if (warp >= 4 && warp < 4 + NLD && MODE_ST == false && QK == false) {
+  } else if (warp >= 4 && warp < 4 + NLD && (NLD == 6 || NLD == 5)) {
+    // LDS with bank conflicts (NLD == 6: lanes stride 40 floats, 8-way; NLD == 5: stride 32, 32-way)
+    const int stride = NLD == 6 ? 40 : 32;
+    const float *sp = (const float *)(smem + 60 * 1024) + (threadIdx.x % 32) * stride;
+    float acc2 = 0.f;
+    while (!done) {
+#pragma unroll 8
+      for (int kk = 0; kk < 64; ++kk) acc2 += sp[kk & 15];
+    }
+    if (acc2 == 1234.5f) cyc[1000] = 1;
   } else if (warp >= 4 && warp < 4 + NLD && NLD == 7) {
     // pure ALU / MUFU / LDS load (no TMEM): FFMA2 + ex2 + LDS like the softmax warps
     float2 a = make_float2(threadIdx.x * 1e-3f, 0.5f), b2 = make_float2(1.0001f, 0.9999f);
@@ -384,7 +394,7 @@ void run_seq(const char *name) {
   cudaFree(cyc);
 }
 
-int main() {
+int main_old4() {
   run_seq<0, true, false>("fwd seq: QK only");
   run_seq<0, false, true>("fwd seq: PV only");
   run_seq<0, true, true>("fwd seq: QK + PV");
@@ -392,5 +402,130 @@ int main() {
   run_seq<8, true, true>("fwd seq: QK + PV, 8 ld/st warps");
   run_seq<4, true, true>("fwd seq: QK + PV, 4 ld/st warps");
   run_seq<7, true, true>("fwd seq: QK + PV, 7 ALU/MUFU/LDS warps");
+  run_seq<6, true, true>("fwd seq: QK + PV, 6 LDS 8-way-conflict warps");
+  run_seq<5, true, true>("fwd seq: QK + PV, 5 LDS 32-way-conflict warps");
+  return 0;
+}
+
+// Issue mechanics: the forward's per-tile MMAs (4 QK + 30 PV) issued as
+//   V=0: one elect block per tile;  V=1: QK block + 5 PV blocks of 6 (elect + syncwarp each);
+//   V=2: V=1 + a tcgen05.commit after every block;  V=3: V=1 + mbarrier wait (already complete)
+//   + tcgen05.fence::after_thread_sync before every block;  V=4: V=1 with precomputed descriptors.
+template <int V>
+__global__ void issue_bench(int iters, long long *cyc) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint64_t &bar = *(uint64_t *)(smem + 90 * 1024);
+  uint64_t &bar2 = *(uint64_t *)(smem + 90 * 1024 + 8);
+  uint64_t &done_bar = *(uint64_t *)(smem + 90 * 1024 + 16);
+  uint32_t &slot = *(uint32_t *)(smem + 90 * 1024 + 24);
+  const int warp = threadIdx.x / 32;
+  for (int i = threadIdx.x; i < 88 * 1024 / 4; i += blockDim.x) ((uint32_t *)smem)[i] = 0x3c003c00u;
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_init(&bar2, 1);
+    mbar_init(&done_bar, 1);
+    fence_barrier_init();
+    mbar_arrive(&done_bar);
+  }
+  if (warp == 0) tmem_alloc<512>(&slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (warp == 0) {
+    constexpr uint32_t iqk = idesc_bf16(64, 240, false), ipv = idesc_bf16(64, 32, true);
+    const uint32_t q = smem_u32(smem), k = q + 8192, v = q + 8192 + 21504;
+    const uint64_t dv = sdesc_sw64(v);
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      const uint32_t s0 = tmem + (it & 1) * 256, p0 = tmem + ((it + 1) & 1) * 256, p1 = p0 + ((uint32_t)16 << 16);
+      if (V == 0) {
+        if (elect_one()) {
+          for (int kk = 0; kk < 2; ++kk)
+            for (int sb = 0; sb < 2; ++sb)
+              mma_ss(s0 + ((uint32_t)(16 * sb) << 16), sdesc_sw64(q + sb * 4096 + kk * 32),
+                     sdesc_sw64(k + sb * 4 * 1536 + kk * 32), iqk, kk);
+#pragma unroll
+          for (int ks = 0; ks < 15; ++ks)
+#pragma unroll
+            for (int sb = 0; sb < 2; ++sb) {
+              const uint32_t b = p0 + ((uint32_t)(16 * sb) << 16);
+              mma_ts(b + 120 + (ks % 3) * 32, b + ks * 8, sdesc_sw64(v + sb * 4 * 1536 + ks * 1024), ipv, ks >= 3);
+            }
+        }
+        __syncwarp();
+      } else {
+        if (elect_one()) {
+          for (int kk = 0; kk < 2; ++kk)
+            for (int sb = 0; sb < 2; ++sb)
+              mma_ss(s0 + ((uint32_t)(16 * sb) << 16), sdesc_sw64(q + sb * 4096 + kk * 32),
+                     sdesc_sw64(k + sb * 4 * 1536 + kk * 32), iqk, kk);
+          if (V == 2) mma_commit(&bar2);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int pk = 0; pk < 5; ++pk) {
+          if (V == 3) {
+            mbar_wait(&done_bar, 0);
+            tc_fence_after();
+          }
+          if (elect_one()) {
+#pragma unroll
+            for (int k3 = 0; k3 < 3; ++k3) {
+              const int ks = 3 * pk + k3;
+              if (V == 4) {
+                const uint32_t vo = (ks * 1024) >> 4;
+                mma_ts(p0 + 120 + k3 * 32, p0 + ks * 8, dv + vo, ipv, pk > 0);
+                mma_ts(p1 + 120 + k3 * 32, p1 + ks * 8, dv + (6144 >> 4) + vo, ipv, pk > 0);
+              } else {
+#pragma unroll
+                for (int sb = 0; sb < 2; ++sb) {
+                  const uint32_t b = p0 + ((uint32_t)(16 * sb) << 16);
+                  mma_ts(b + 120 + k3 * 32, b + ks * 8, sdesc_sw64(v + sb * 4 * 1536 + ks * 1024), ipv, pk > 0);
+                }
+              }
+            }
+            if (V == 2) mma_commit(&bar2);
+          }
+          __syncwarp();
+        }
+      }
+    }
+    if (elect_one()) mma_commit(&bar);
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+template <int V>
+void run_issue(const char *name) {
+  long long *cyc = nullptr, host[4] = {0, 0, 0, 0};
+  cudaMalloc(&cyc, 2000 * 8);
+  auto k = issue_bench<V>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  const int iters = 500;
+  k<<<148, 128, 100 * 1024>>>(iters, cyc);
+  cudaError_t e = cudaDeviceSynchronize();
+  cudaMemcpy(host, cyc, 8, cudaMemcpyDeviceToHost);
+  printf("%-50s %7.1f cyc/tile (%s)\n", name, (double)host[0] / iters, cudaGetErrorString(e));
+  cudaFree(cyc);
+}
+
+int main() {
+  run_issue<0>("issue: one elect block per tile");
+  run_issue<1>("issue: QK block + 5 PV blocks of 6");
+  run_issue<2>("issue: ... + commit per block");
+  run_issue<3>("issue: ... + mbar wait + fence per block");
+  run_issue<4>("issue: 5 PV blocks, precomputed descriptors");
   return 0;
 }
