@@ -39,8 +39,6 @@ constexpr int kThreads = 64 + kGroups * 128;  // warps 0.. elementwise, then the
 // (the sub-partition scheduler favours the highest warp id: the producer / MMA warps never wait for
 // the elementwise warps sharing their sub-partitions)
 constexpr int kProducerWarp = 4 * kGroups, kMmaWarp = 4 * kGroups + 1;
-constexpr int kQAcc = 3;       // independent dQ accumulators
-constexpr int kDP_COL = 256;   // dP accumulator columns
 
 // Per-stage tile description, written by the producer before it arms full[stage] (the class-grouped
 // order's decode and the window origins, computed once instead of in every warp).
@@ -70,8 +68,13 @@ struct CfgQ {
   }
   static_assert(2 * kHCP == 3 * 16, "a row pair is 3 K-steps");
   static constexpr int DS_COL = 0;         // dS (bf16 pairs) over consumed S columns
-  static constexpr int Q_COL = kDP_COL;    // dQ partial accumulators in the dP columns (dead after pass 2)
-  static_assert(kDP_COL + NSUB <= 512 && Q_COL + kQAcc * kD <= 512, "TMEM budget");
+  // TMEM: S [0, NSUB), dP [NSUB, 2 NSUB), dQ partial accumulators [2 NSUB, +QACC*32).  dQ lives
+  // outside S / dP, so S / dP of the next tile are issued right behind this tile's dQ MMAs and the
+  // dQ read-out (epilogue) leaves the critical path.
+  static constexpr int DP_COL = NSUB;
+  static constexpr int Q_COL = 2 * NSUB;
+  static constexpr int QACC = (512 - Q_COL) / kD < 3 ? (512 - Q_COL) / kD : 3;  // independent dQ chains
+  static_assert(QACC >= 1, "TMEM budget");
   static constexpr int KV_ROWS = HR * kHCP;
   static constexpr int Q_BYTES = 128 * kRowBytes;
   static constexpr int KV_BYTES = KV_ROWS * kRowBytes;
@@ -124,7 +127,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   TileInfoQ *tinfo = (TileInfoQ *)(smem + C::TI_OFF);
   uint64_t *bars = (uint64_t *)(smem + C::BAR_OFF);
   uint64_t *full = bars, *empty = bars + kStages;
-  uint64_t *sp_full = bars + 2 * kStages, *ds_full = sp_full + 1, *dq_full = sp_full + 2, *tmem_free = sp_full + 3;
+  uint64_t *sp_full = bars + 2 * kStages, *ds_full = sp_full + 1, *dq_full = sp_full + 2, *dq_free = sp_full + 3;
   uint32_t *tmem_slot = (uint32_t *)(bars + 2 * kStages + 4);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -141,7 +144,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(sp_full, 1);
     mbar_init(ds_full, 4 * kGroups);
     mbar_init(dq_full, 1);
-    mbar_init(tmem_free, 4);
+    mbar_init(dq_free, 4);
     fence_barrier_init();
     tma_prefetch(&tm_q);
     tma_prefetch(&tm_do);
@@ -207,60 +210,64 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(&full[s]);
     }
   } else if (warp == kMmaWarp) {
-    // ================= MMA issuer
+    // ================= MMA issuer: S / dP of tile 0; then per tile: (wait dS) dQ of tile it, then
+    // S / dP of tile it + 1 straight behind it (the in-order tensor pipe finishes reading dS and the
+    // K tile before S / dP overwrite their columns), so the elementwise warps start the next tile
+    // while the epilogue reads dQ.
     constexpr uint32_t idesc_s = idesc_bf16(64, C::NSUB, false);
     constexpr uint32_t idesc_q = idesc_bf16(64, kD, true);
-    int it = 0;
-    for (int t = t_begin; t < t_end; ++t, ++it) {
+    const int n = t_end - t_begin;
+    const uint32_t t0 = tmem, t1 = tmem + ((uint32_t)16 << 16);
+    auto issue_sdp = [&](int it) {
       const int s = it % kStages;
-      const uint32_t ph = it & 1;
       mbar_wait(&full[s], (it / kStages) & 1);
-      const int rb0 = tinfo[s].rb[0], rb1 = tinfo[s].rb[1];
       if (lane == 0) qtrace(p, it, 0);
-#ifdef NA2D_TRACE
-      if (lane == 0 && p.trace && blockIdx.x % 37 == 0 && it < 32) {  // wall clock beside the SM clock
-        uint64_t gt;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-        p.trace[4096 + ((size_t)(blockIdx.x / 37) * 32 + it) * 32 + 15] = (long long)gt;
-      }
-#endif
-      mbar_wait(tmem_free, ph ^ 1);
-      if (lane == 0) qtrace(p, it, 1);
+      const int rb0 = tinfo[s].rb[0], rb1 = tinfo[s].rb[1];
       tc_fence_after();
       // descriptors: per-stage bases + immediate offsets (short issue bursts, no per-MMA chains)
       const uint64_t dqs = sdesc_sw64(smem_u32(smem + s * C::STAGE_BYTES));
       const uint64_t dk0 = dqs + ((2 * C::Q_BYTES + rb0 * kHCP * kRowBytes) >> 4);
       const uint64_t dk1 = dqs + ((2 * C::Q_BYTES + rb1 * kHCP * kRowBytes) >> 4);
-      const uint32_t t0 = tmem, t1 = tmem + ((uint32_t)16 << 16);
       if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < kD / 16; ++k) {
           const uint32_t ko = (k * 32) >> 4;
           mma_ss(t0, dqs + ko, dk0 + ko, idesc_s, k);
-          mma_ss(t0 + kDP_COL, dqs + (C::Q_BYTES >> 4) + ko, dk0 + (C::KV_BYTES >> 4) + ko, idesc_s, k);
+          mma_ss(t0 + C::DP_COL, dqs + (C::Q_BYTES >> 4) + ko, dk0 + (C::KV_BYTES >> 4) + ko, idesc_s, k);
           mma_ss(t1, dqs + (4096 >> 4) + ko, dk1 + ko, idesc_s, k);
-          mma_ss(t1 + kDP_COL, dqs + ((C::Q_BYTES + 4096) >> 4) + ko, dk1 + (C::KV_BYTES >> 4) + ko, idesc_s, k);
+          mma_ss(t1 + C::DP_COL, dqs + ((C::Q_BYTES + 4096) >> 4) + ko, dk1 + (C::KV_BYTES >> 4) + ko, idesc_s, k);
         }
         mma_commit(sp_full);
       }
       __syncwarp();
       if (lane == 0) qtrace(p, it, 2);
+    };
+    if (n > 0) issue_sdp(0);
+    for (int it = 0; it < n; ++it) {
+      const int s = it % kStages;
+      const uint32_t ph = it & 1;
       mbar_wait(ds_full, ph);
       if (lane == 0) qtrace(p, it, 3);
+      mbar_wait(dq_free, ph ^ 1);  // the epilogue of tile it - 1 has read its dQ
+      if (lane == 0) qtrace(p, it, 1);
       tc_fence_after();
+      const int rb0 = tinfo[s].rb[0], rb1 = tinfo[s].rb[1];
+      const uint64_t dk0 = sdesc_sw64(smem_u32(smem + s * C::STAGE_BYTES) + 2 * C::Q_BYTES + rb0 * kHCP * kRowBytes);
+      const uint64_t dk1 = dk0 + (((rb1 - rb0) * kHCP * kRowBytes) >> 4);
       if (elect_one()) {
 #pragma unroll
         for (int ks = 0; ks < C::NSUB / 16; ++ks) {
           const uint32_t ko = (ks * 16 * kRowBytes) >> 4;
-          const uint32_t ao = C::DS_COL + ks * 8 + C::ds_shift_of_ks(ks), qo = C::Q_COL + (ks % kQAcc) * kD;
-          mma_ts(t0 + qo, t0 + ao, dk0 + ko, idesc_q, ks >= kQAcc);
-          mma_ts(t1 + qo, t1 + ao, dk1 + ko, idesc_q, ks >= kQAcc);
+          const uint32_t ao = C::DS_COL + ks * 8 + C::ds_shift_of_ks(ks), qo = C::Q_COL + (ks % C::QACC) * kD;
+          mma_ts(t0 + qo, t0 + ao, dk0 + ko, idesc_q, ks >= C::QACC);
+          mma_ts(t1 + qo, t1 + ao, dk1 + ko, idesc_q, ks >= C::QACC);
         }
         mma_commit(dq_full);
         mma_commit(&empty[s]);
       }
       __syncwarp();
       if (lane == 0) qtrace(p, it, 4);
+      if (it + 1 < n) issue_sdp(it + 1);
     }
   } else {
     // ================= elementwise (warps 2.. -> TMEM lane quarter warp % 4): group grp takes union
@@ -376,8 +383,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t ca = lane_addr + u * kHCP + uc;
         ld_row<C::UCW>(ca, sa);
         ld_row<C::UCW>(ca + kHCP, sb_);
-        ld_row<C::UCW>(ca + kDP_COL, pa_);
-        ld_row<C::UCW>(ca + kDP_COL + kHCP, pb_);
+        ld_row<C::UCW>(ca + C::DP_COL, pa_);
+        ld_row<C::UCW>(ca + C::DP_COL + kHCP, pb_);
         const int pr = hr0 + rb + u;
         const bool rva = (unsigned)(pr - si) < (unsigned)Lh, rvb = (unsigned)(pr + 1 - si) < (unsigned)Lh;
         const float *ta = tcls + (rva ? pr - ic + L - 1 : C::TT) * kTblStride;
@@ -425,8 +432,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t ca = lane_addr + u * kHCP + uc;
         ld_row<C::UCW>(ca, sa);
         ld_row<C::UCW>(ca + kHCP, sb_);
-        ld_row<C::UCW>(ca + kDP_COL, pa_);
-        ld_row<C::UCW>(ca + kDP_COL + kHCP, pb_);
+        ld_row<C::UCW>(ca + C::DP_COL, pa_);
+        ld_row<C::UCW>(ca + C::DP_COL + kHCP, pb_);
         tc_wait_ld();
         uint32_t da[C::UCW / 2], db[C::UCW / 2];
 #pragma unroll
@@ -466,7 +473,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int hh = 0; hh < 2; ++hh) {
         tmem_ld16(lane_addr + C::Q_COL + 16 * hh, o[hh]);
 #pragma unroll
-        for (int a = 1; a < kQAcc; ++a) {
+        for (int a = 1; a < C::QACC; ++a) {
           uint32_t oa[16];
           tmem_ld16(lane_addr + C::Q_COL + a * kD + 16 * hh, oa);
           tc_wait_ld();
@@ -477,7 +484,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_wait_ld();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tmem_free);
+      if (lane == 0) mbar_arrive(dq_free);
       if (tq) qtrace(p, it, 13);
       if (lane == 0) bulk_wait_read0();  // this warp's previous store has left the staging
       __syncwarp();
