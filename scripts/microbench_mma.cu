@@ -270,7 +270,7 @@ int main_old2() {
 // into slot t&1, then PV of the previous tile (30 TS, M=64 N=32, A = P at slot (t-1)&1 columns
 // [0,120), D at [120,216) in 3 chains x 2 sub-tiles).  NLD other warps do TMEM ld/st.
 template <int NLD, bool QK, bool PV, bool MODE_ST = true>
-__global__ void fwd_seq_bench(int iters, long long *cyc) {
+__global__ void fwd_seq_bench(int iters, long long *cyc, const uint8_t *gsrc) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t &bar = *(uint64_t *)(smem + 90 * 1024);
@@ -309,6 +309,7 @@ __global__ void fwd_seq_bench(int iters, long long *cyc) {
                      sdesc_sw64(k + sb * 4 * 1536 + kk * 32), iqk, kk);
         }
         if (PV) {
+          if (NLD >= 100) tc_fence_after();
 #pragma unroll
           for (int ks = 0; ks < 15; ++ks)
 #pragma unroll
@@ -326,6 +327,26 @@ __global__ void fwd_seq_bench(int iters, long long *cyc) {
     if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
     done = 1;
   } else if (warp >= 4 && warp < 4 + NLD && MODE_ST == false && QK == false) {
+  } else if (warp == 4 && NLD == 1) {
+    const int lane = threadIdx.x % 32;
+    // bulk-copy producer: 2 x 16 KB global -> smem [60 KB, 92 KB) per round, like the TMA halo loads
+    uint64_t &tb = *(uint64_t *)(smem + 90 * 1024 + 32);
+    if (lane == 0) {
+      mbar_init(&tb, 1);
+      fence_barrier_init();
+      uint32_t ph = 0;
+      size_t off = blockIdx.x * 65536;
+      while (!done) {
+        mbar_expect_tx(&tb, 32768);
+        for (int h = 0; h < 2; ++h)
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                       ::"r"(smem_u32(smem + 52 * 1024 + h * 16384)), "l"(gsrc + off + h * 16384), "r"(16384),
+                       "r"(smem_u32(&tb)) : "memory");
+        mbar_wait(&tb, ph);
+        ph ^= 1;
+        off = (off + 32768) % (size_t)(148 * 65536 * 16);
+      }
+    }
   } else if (warp >= 4 && warp < 4 + NLD && (NLD == 6 || NLD == 5)) {
     // LDS with bank conflicts (NLD == 6: lanes stride 40 floats, 8-way; NLD == 5: stride 32, 32-way)
     const int stride = NLD == 6 ? 40 : 32;
@@ -350,7 +371,7 @@ __global__ void fwd_seq_bench(int iters, long long *cyc) {
       }
     }
     if (e0 + e1 == 1234.5f) cyc[1000] = 1;
-  } else if (warp >= 4 && warp < 4 + NLD) {
+  } else if (warp >= 4 && warp < 4 + (NLD >= 100 ? NLD - 100 : NLD)) {
     // like the softmax passes: both slots' lanes, two x16 loads in flight, a x16 + x8 store
     const uint32_t la = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (warp >= 8 ? 256 : 0);
     uint32_t r[16], r2[16];
@@ -387,10 +408,13 @@ void run_seq(const char *name) {
   auto k = fwd_seq_bench<NLD, QK, PV, MODE_ST>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   const int iters = 500;
-  k<<<148, 384, 100 * 1024>>>(iters, cyc);
+  static uint8_t *gsrc = nullptr;
+  if (!gsrc) cudaMalloc(&gsrc, (size_t)148 * 65536 * 16 + 65536);
+  k<<<148, 384, 100 * 1024>>>(iters, cyc, gsrc);
   cudaError_t e = cudaDeviceSynchronize();
   cudaMemcpy(host, cyc, 8, cudaMemcpyDeviceToHost);
   printf("%-40s %7.1f cyc/tile (%s)\n", name, (double)host[0] / iters, cudaGetErrorString(e));
+  fflush(stdout);
   cudaFree(cyc);
 }
 
@@ -521,11 +545,18 @@ void run_issue(const char *name) {
   cudaFree(cyc);
 }
 
-int main() {
+int main_old5() {
   run_issue<0>("issue: one elect block per tile");
   run_issue<1>("issue: QK block + 5 PV blocks of 6");
   run_issue<2>("issue: ... + commit per block");
   run_issue<3>("issue: ... + mbar wait + fence per block");
   run_issue<4>("issue: 5 PV blocks, precomputed descriptors");
+  return 0;
+}
+
+int main() {
+  run_seq<8, true, true>("fwd seq: QK + PV, 8 ld/st warps");
+  run_seq<108, true, true>("fwd seq: ... + fence::after_thread_sync per PV block");
+  run_seq<100, true, true>("fwd seq: fence, no ld/st warps");
   return 0;
 }
