@@ -37,7 +37,9 @@
  * Streams and synchronisation: every call validates its arguments synchronously (on error
  * nothing is launched and no output is touched), then enqueues all work on `stream` (a
  * cudaStream_t, NULL = legacy default stream) and returns without synchronising.
- * Asynchronous device faults surface at the caller's next synchronisation.  The library
+ * Asynchronous device faults surface at the caller's next synchronisation.  A non-sticky CUDA
+ * error left pending on the calling thread by an earlier, unrelated runtime call is cleared on
+ * entry (NA2D_ERR_CUDA reports only errors of this call's own launches).  The library
  * allocates no device memory and keeps no per-call state; it is thread-safe.
  *
  * Precision: NA2D_BF16 = bf16 in/out, fp32 accumulation (tcgen05 tensor cores), fp32 LSE and

@@ -117,6 +117,7 @@ na2d_status na2d_forward(const na2d_problem *p, const void *q, const void *k, co
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(out) || !aligned16(lse) || !aligned16(rpb))
     return NA2D_ERR_ALIGNMENT;
   cudaStream_t st = (cudaStream_t)stream;
+  (void)cudaGetLastError();  // a non-sticky error left by an unrelated earlier runtime call is not ours
   if (use_tc(g, 0)) return cuda_status(tc_forward(g, q, k, v, rpb, out, lse, st));
   return cuda_status(simt_forward(g, q, k, v, rpb, out, lse, st));
 }
@@ -142,6 +143,7 @@ na2d_status na2d_backward(const na2d_problem *p, const void *q, const void *k, c
   for (const void *ptr : ptrs)
     if (!aligned16(ptr)) return NA2D_ERR_ALIGNMENT;
   cudaStream_t st = (cudaStream_t)stream;
+  (void)cudaGetLastError();  // a non-sticky error left by an unrelated earlier runtime call is not ours
   float *D = (float *)workspace;
   if (use_tc(g, 1)) {
     void *scratch = (char *)workspace + align_up(n_query(g) * sizeof(float));
@@ -173,6 +175,7 @@ na2d_status na2d_step_host(const na2d_problem *p, const void *q, const void *k, 
   if (workspace_bytes < need) return NA2D_ERR_WORKSPACE;
   if (!aligned16(device_workspace)) return NA2D_ERR_ALIGNMENT;
   cudaStream_t st = (cudaStream_t)stream;
+  (void)cudaGetLastError();  // a non-sticky error left by an unrelated earlier runtime call is not ours
   const size_t bytes = n_query(g) * g.d * elem_size(g);
   const size_t t = align_up(bytes);
   const size_t TT = 2 * g.L - 1;

@@ -473,68 +473,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     // output staging of this warp (dV, dK: two 4x4-key blocks each, SW64 layout of the TMA store)
     uint8_t *ostage = smem + C::OUT_OFF + (grp * 4 + quarter) * 4096;
     const bool trq = quarter == 2 && lane == 0;
-    int cur_head = -1;
-    int c = 0;
-    for (int t = t_begin; t < t_end; ++t) {
-      const int it = t - t_begin, stage = it % kStages;
-      mbar_wait(&full[stage], (it / kStages) & 1);  // tile description, LSE / D staged
-      if (trq) ktrace(p, c, 16 + 4 * grp);
-      const TileInfo &ti = tinfo[stage];
-      const int h = ti.head, bh = ti.bh, kr0 = ti.kr0, kc0 = ti.kc0, qr0 = ti.qr0, qc0 = ti.qc0;
-      const int nch = ti.nchunks, qs_lo = ti.qs_lo[half], qs_n = ti.qs_n[half];
-      const int uc = ti.uc[quarter];
-      const bool fast = ti.fast[quarter];
-      int colterm[C::UCW];
-#pragma unroll
-      for (int z = 0; z < C::UCW; ++z) colterm[z] = ti.colterm[quarter][z];
-      if (h != cur_head) {  // both groups rebuild the shared table: sync all 256 threads
-        named_bar_sync(1, 256);
-        const int tid256 = threadIdx.x;
-        BiasTable<L>::build(tbl, p.rpb, h, Lw, sl2, tid256, 256);
-        for (int e = BiasTable<L>::FLOATS + tid256; e < C::TBL_FLOATS; e += 256) tbl[e] = -INFINITY;
-        named_bar_sync(1, 256);
-        cur_head = h;
-      }
-      // this thread's key
-      const int pk = kr0 + 4 * half + r, qk = kc0 + 4 * quarter + cc;
-      const float *lsd = (const float *)(smem + stage * C::STAGE_BYTES + 2 * C::Q_BYTES + 2 * C::KT_BYTES);
-      const float *tbl_row0 = tbl + kTblOff + qk + L - 1 + (fast ? C::NS * C::TROWS * kTblStride - (qc0 + uc) : 0);
-      if (trq) ktrace(p, c, 17 + 4 * grp);
-      bool last_mine = false;
-      for (int k = 0; k < nch; ++k, ++c) {
-        if ((c & 1) != grp) continue;
-        const int x = c & 1;
-        if (trq) ktrace(p, c, 4);
-        mbar_wait(&s_full[x], (c >> 1) & 1);
-        if (trq) ktrace(p, c, 5);
-        tc_fence_after();
-        const int i_base = qs_lo + C::CR * k;  // query row of chunk row 0 (this half)
-        const int rows_here = min(qs_n - C::CR * k, q_end - i_base);
-        const float *lrow0 = lsd + (i_base - qr0) * C::LP + (qc0 & 3) + uc;
-        const uint32_t lane_addr = lane_q + x * kSlot;
-        // a quarter whose keys all lie past the map edge only feeds accumulator rows the TMA store
-        // clips, so its P / dS columns may hold anything
-        if (kc0 + 4 * quarter < p.W) {
-          if (fast)
-            chunk_rows<L, QP, true>(lane_addr, uc, tbl_row0, colterm, lrow0, pk, i_base, p.H, rows_here, Lh, sl2);
-          else
-            chunk_rows<L, QP, false>(lane_addr, uc, tbl_row0, colterm, lrow0, pk, i_base, p.H, rows_here, Lh, sl2);
-        }
-        tc_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&ds_full[x]);
-        if (trq) ktrace(p, c, 6);
-        if (lane == 0) ktrace(p, c, 10 + quarter);
-        last_mine = k == nch - 1;
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[stage]);  // done with this stage's LSE / D and TileInfo
-      if (last_mine) {
-        // ---- epilogue of the tile: dV, dK (scale) from accumulator buffer b, TMA-stored via smem
-        const int b = it & 1, cl = c - 1;
-        mbar_wait(&acc_full[b], (it >> 1) & 1);
-        if (trq) ktrace(p, cl, 7);
+    // ---- epilogue of a tile: dV, dK (scale) from accumulator buffer (tile & 1), TMA-stored via
+    // smem.  Deferred until the group has processed its next chunk, so it never waits for the
+    // tile's last dV/dK MMAs (the MMA warp needs the buffer again only two tiles later).
+    auto epilogue = [&](int eit, int bh, int kr0, int kc0) {
+        const int b = eit & 1;
+        mbar_wait(&acc_full[b], (eit >> 1) & 1);
         tc_fence_after();
         uint32_t a0[32], a1[32];
         tmem_ld32(lane_q + kACC_COL + b * 2 * kD, a0);
@@ -543,7 +487,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_free[b]);
-        if (trq) ktrace(p, cl, 8);
         if (lane == 0) bulk_wait_read0();  // this warp's previous stores have left the staging
         __syncwarp();
         // key (r, cc) of block `half` is row R of the 1 KB box; SW64: 16-byte chunk z at z ^ (R/2 % 4)
@@ -573,9 +516,75 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           bulk_commit();
         }
-        if (trq) ktrace(p, cl, 9);
+    };
+    int cur_head = -1;
+    int c = 0;
+    int pend_it = -1, pend_bh = 0, pend_kr0 = 0, pend_kc0 = 0;  // deferred epilogue
+    for (int t = t_begin; t < t_end; ++t) {
+      const int it = t - t_begin, stage = it % kStages;
+      mbar_wait(&full[stage], (it / kStages) & 1);  // tile description, LSE / D staged
+      if (trq) ktrace(p, c, 16 + 4 * grp);
+      const TileInfo &ti = tinfo[stage];
+      const int h = ti.head, bh = ti.bh, kr0 = ti.kr0, kc0 = ti.kc0, qr0 = ti.qr0, qc0 = ti.qc0;
+      const int nch = ti.nchunks, qs_lo = ti.qs_lo[half], qs_n = ti.qs_n[half];
+      const int uc = ti.uc[quarter];
+      const bool fast = ti.fast[quarter];
+      int colterm[C::UCW];
+#pragma unroll
+      for (int z = 0; z < C::UCW; ++z) colterm[z] = ti.colterm[quarter][z];
+      if (h != cur_head) {  // both groups rebuild the shared table: sync all 256 threads
+        named_bar_sync(1, 256);
+        const int tid256 = threadIdx.x;
+        BiasTable<L>::build(tbl, p.rpb, h, Lw, sl2, tid256, 256);
+        for (int e = BiasTable<L>::FLOATS + tid256; e < C::TBL_FLOATS; e += 256) tbl[e] = -INFINITY;
+        named_bar_sync(1, 256);
+        cur_head = h;
       }
+      // this thread's key
+      const int pk = kr0 + 4 * half + r, qk = kc0 + 4 * quarter + cc;
+      const float *lsd = (const float *)(smem + stage * C::STAGE_BYTES + 2 * C::Q_BYTES + 2 * C::KT_BYTES);
+      const float *tbl_row0 = tbl + kTblOff + qk + L - 1 + (fast ? C::NS * C::TROWS * kTblStride - (qc0 + uc) : 0);
+      if (trq) ktrace(p, c, 17 + 4 * grp);
+      for (int k = 0; k < nch; ++k, ++c) {
+        if ((c & 1) != grp) continue;
+        const int x = c & 1;
+        if (trq) ktrace(p, c, 4);
+        mbar_wait(&s_full[x], (c >> 1) & 1);
+        if (trq) ktrace(p, c, 5);
+        tc_fence_after();
+        const int i_base = qs_lo + C::CR * k;  // query row of chunk row 0 (this half)
+        const int rows_here = min(qs_n - C::CR * k, q_end - i_base);
+        const float *lrow0 = lsd + (i_base - qr0) * C::LP + (qc0 & 3) + uc;
+        const uint32_t lane_addr = lane_q + x * kSlot;
+        // a quarter whose keys all lie past the map edge only feeds accumulator rows the TMA store
+        // clips, so its P / dS columns may hold anything
+        if (kc0 + 4 * quarter < p.W) {
+          if (fast)
+            chunk_rows<L, QP, true>(lane_addr, uc, tbl_row0, colterm, lrow0, pk, i_base, p.H, rows_here, Lh, sl2);
+          else
+            chunk_rows<L, QP, false>(lane_addr, uc, tbl_row0, colterm, lrow0, pk, i_base, p.H, rows_here, Lh, sl2);
+        }
+        tc_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ds_full[x]);
+        if (trq) ktrace(p, c, 6);
+        if (lane == 0) ktrace(p, c, 10 + quarter);
+        if (pend_it >= 0) {
+          epilogue(pend_it, pend_bh, pend_kr0, pend_kc0);
+          pend_it = -1;
+        }
+        if (k == nch - 1) {
+          pend_it = it;
+          pend_bh = bh;
+          pend_kr0 = kr0;
+          pend_kc0 = kc0;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);  // done with this stage's LSE / D and TileInfo
     }
+    if (pend_it >= 0) epilogue(pend_it, pend_bh, pend_kr0, pend_kc0);
     if (lane == 0) bulk_wait0();
   }
   __syncthreads();

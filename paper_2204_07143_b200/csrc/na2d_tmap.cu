@@ -25,6 +25,12 @@ EncodeFn encode_fn() {
   return fn;
 }
 
+// cuTensorMapEncodeTiled (driver API) needs a current context.  A host thread that has made no
+// runtime call that binds one yet (e.g. torch's autograd worker thread, when the kernels'
+// one-time attribute setup already ran on another thread) gets CUDA_ERROR_INVALID_CONTEXT:
+// bind the primary context of the thread's current device (cudaFree(nullptr) does exactly that).
+bool bind_context() { return cudaFree(nullptr) == cudaSuccess; }
+
 }  // namespace
 
 bool tmap_available() { return encode_fn() != nullptr; }
@@ -36,9 +42,13 @@ bool make_tmap_bf16_4d(CUtensorMap *m, const void *base, int dim, int W, int row
   const cuuint64_t gstride[3] = {(cuuint64_t)dim * 2, (cuuint64_t)W * dim * 2, (cuuint64_t)rows * W * dim * 2};
   const cuuint32_t box[4] = {(cuuint32_t)dim, (cuuint32_t)box_w, (cuuint32_t)box_h, 1};
   const cuuint32_t estride[4] = {1, 1, 1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(base), gdim, gstride, box, estride,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  auto encode = [&] {
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(base), gdim, gstride, box, estride,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  };
+  CUresult r = encode();
+  if (r == CUDA_ERROR_INVALID_CONTEXT && bind_context()) r = encode();
   return r == CUDA_SUCCESS;
 }
 
@@ -49,9 +59,13 @@ bool make_tmap_f32_3d(CUtensorMap *m, const void *base, int W, int rows, int out
   const cuuint64_t gstride[2] = {(cuuint64_t)W * 4, (cuuint64_t)rows * W * 4};
   const cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)box_h, 1};
   const cuuint32_t estride[3] = {1, 1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void *>(base), gdim, gstride, box, estride,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  auto encode = [&] {
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void *>(base), gdim, gstride, box, estride,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  };
+  CUresult r = encode();
+  if (r == CUDA_ERROR_INVALID_CONTEXT && bind_context()) r = encode();
   return r == CUDA_SUCCESS;
 }
 
