@@ -48,11 +48,11 @@ using namespace tc;
 constexpr int kStagesQK = 3;      // Q + K halo ring (released when the QK MMAs complete)
 constexpr int kStagesV = 3;       // V halo ring (released when the PV MMAs complete)
 constexpr int kTInfo = 8;         // tile-description ring (>= 5: see the producer)
-constexpr int kThreads = 384;     // 12 warps
+constexpr int kThreads = 640;     // 20 warps
 // The SM sub-partition scheduler favours the highest warp id among eligible warps: the producer and
 // MMA-issue warps take the two highest ids so the busy elementwise warps sharing their
 // sub-partitions (warp % 4) never delay a TMA or MMA issue.
-constexpr int kProducerWarp = 8, kMmaWarp = 9, kProducerVWarp = 10, kPvWarp = 11;
+constexpr int kProducerWarp = 16, kMmaWarp = 17, kProducerVWarp = 18, kPvWarp = 19;
 constexpr int kOAcc = 3;           // independent PV accumulators (summed in the epilogue)
 
 template <int L>
@@ -111,27 +111,6 @@ __device__ __forceinline__ void trace_ev(const FwdParams &p, int it, int ev) {
 __device__ __forceinline__ void trace_ev(const FwdParams &, int, int) {}
 #endif
 
-// Pass 2 of one union row: P = exp2(x - max) for the needed columns of the row's 12 loaded union
-// columns (ODD: columns 1..10, else 0..9; the others are outside every lane's window), bf16 pairs.
-template <bool ODD>
-__device__ __forceinline__ void p_row(const uint32_t (&x)[12], float mx, float2 &sum, uint32_t (&pp)[6]) {
-  const float2 nm = make_float2(-mx, -mx);
-#pragma unroll
-  for (int z = 0; z < 6; ++z) {
-    const float2 a = __fadd2_rn(make_float2(__uint_as_float(x[2 * z]), __uint_as_float(x[2 * z + 1])), nm);
-    float2 e;
-    if (ODD) {
-      e.x = z == 0 ? 0.f : ex2(a.x);
-      e.y = z == 5 ? 0.f : ex2(a.y);
-    } else {
-      e.x = z == 5 ? 0.f : ex2(a.x);
-      e.y = z == 5 ? 0.f : ex2(a.y);
-    }
-    sum = __fadd2_rn(sum, e);
-    pp[z] = pack_bf16(e.x, e.y);
-  }
-}
-
 template <int L>
 __global__ void __launch_bounds__(kThreads, 1)
     na2d_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -170,8 +149,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&s_full[s], 1);
       mbar_init(&o_full[s], 1);
-      mbar_init(&tmem_free[s], 4);
-      for (int k = 0; k < C::PAIRS; ++k) mbar_init(&p_pair[s * C::PAIRS + k], 4);
+      mbar_init(&tmem_free[s], 8);  // both lane-half groups of the slot
+      for (int k = 0; k < C::PAIRS; ++k) mbar_init(&p_pair[s * C::PAIRS + k], 8);
     }
     fence_barrier_init();
     tma_prefetch(&tm_q);
@@ -333,17 +312,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) trace_ev(p, it, 3);
     }
   } else {
-    // ================= softmax + epilogue groups (ping-pong between the two TMEM slots)
-    const int grp = warp >> 2;  // 0: warps 0-3, 1: warps 4-7
+    // ================= softmax + epilogue: 4 groups of 4 warps.  Group g works on TMEM slot g >> 1
+    // (tiles it with it & 1 == slot) and on sub-tile / TMEM lane half h = g & 1 of those tiles; its
+    // warp of lane quarter q reads the 16 lanes [32q + 16h, +16) with the .16x32bx2 shapes, so two
+    // threads share a query: thread t handles query (t & 15) and union columns [6 (t >> 4), +6).
+    const int grp = warp >> 2, slot = grp >> 1, hh = grp & 1;
     const int quarter = warp & 3;
-    const int half = lane >> 4, r = (lane >> 2) & 3, c = lane & 3;
-    float *tbl = tables + grp * 2 * C::TBL_FLOATS;  // this group's two parity copies
-    const int gtid = threadIdx.x - grp * 128;  // 0..127 within the group
+    const int hf = lane >> 4, ql = lane & 15, r = ql >> 2, c = ql & 3;
+    float *tbl = tables + slot * 2 * C::TBL_FLOATS;  // the slot's two parity copies (both halves share)
+    const int stid = threadIdx.x - slot * 256;       // 0..255 within the slot's two groups
     const int Lh = wlen(p.H, L), Lw = wlen(p.W, L);
     const float2 sl2x2 = make_float2(p.scale_log2, p.scale_log2);
+    const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32 + 16 * hh) << 16) + slot * 256;
     int cur_head = -1;
-    for (int it = grp; it < t_end - t_begin; it += 2) {
-      const int slot = it & 1;
+    for (int it = slot; it < t_end - t_begin; it += 2) {
       const uint32_t ph = (it >> 1) & 1;
       // tile description of tile it: its ring slot is rewritten (tile it + 8) only after QK(it + 5),
       // which needs the epilogue of tile it + 3, whose PV is issued after PV(it + 2), i.e. after this
@@ -351,11 +333,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&ti_full[it % kTInfo], (it / kTInfo) & 1);
       const FTile &ti = tinfo[it % kTInfo];
       const int bh = ti.bh, h = ti.head, i0 = ti.i0, j0 = ti.j0, hr0 = ti.hr0, hc0 = ti.hc0;
-      const int rb = ti.rb[half], ucr = ti.uc[quarter];
-      if (h != cur_head) {  // (re)build this group's masked, pre-scaled bias tables (two parity copies:
-        // copy x holds column b at kTblOff + x + b, so every lane's row start is 8-byte aligned)
-        named_bar_sync(1 + grp, 128);
-        for (int e = gtid; e < 2 * C::TBL_FLOATS; e += 128) {
+      const int rb = ti.rb[hh], ucr = ti.uc[quarter];
+      if (h != cur_head) {  // (re)build the slot's masked, pre-scaled bias tables (two parity copies:
+        // copy x holds column b at kTblOff + x + b, so every thread's row start is 8-byte aligned)
+        named_bar_sync(1 + slot, 256);
+        for (int e = stid; e < 2 * C::TBL_FLOATS; e += 256) {
           const int x = e >= C::TBL_FLOATS, e2 = e - x * C::TBL_FLOATS;
           const int dc = e2 / (C::TROWS * kTblStride);
           const int rr = (e2 / kTblStride) % C::TROWS;
@@ -364,156 +346,156 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (rr < C::TT && cb >= dc && cb < dc + Lw) v = p.rpb ? __ldg(&p.rpb[(h * C::TT + rr) * C::TT + cb]) * p.scale_log2 : 0.f;
           tbl[e] = v;
         }
-        named_bar_sync(1 + grp, 128);
+        named_bar_sync(1 + slot, 256);
         cur_head = h;
       }
       // this thread's query and window geometry
-      const int i = i0 + 4 * half + r, j = j0 + 4 * quarter + c;
+      const int i = i0 + 4 * hh + r, j = j0 + 4 * quarter + c;
       const int ic = min(i, q_end - 1), jc = min(j, p.W - 1);
       const int si = wstart(ic, p.H, L), sj = wstart(jc, p.W, L);
-      const bool odd = ucr & 1;                                      // warp-uniform
-      const int uc = ucr & ~1;
+      const int uc = ucr & ~1;                                       // even union origin (warp-uniform)
       const int dc = sj - jc + L - 1;                                // column-clamp class
       const int bcol0 = hc0 + uc - jc + L - 1;                       // bias column of union col 0
       const int cp = bcol0 & 1;                                      // parity copy: aligned row start
-      const float *tcls = tbl + cp * C::TBL_FLOATS + dc * C::TROWS * kTblStride + kTblOff + cp + bcol0;
-      const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16) + slot * 256;
+      const float *tcls = tbl + cp * C::TBL_FLOATS + dc * C::TROWS * kTblStride + kTblOff + cp + bcol0 + 6 * hf;
 
-      const bool tr = quarter == 2 && lane == 0;
+      const bool tr = grp == 0 && quarter == 2 && lane == 0;
       if (tr) trace_ev(p, it, 4);
       mbar_wait(&s_full[slot], ph);
       if (tr) trace_ev(p, it, 5);
       tc_fence_after();
-      // ---- pass 1 (union row pair k per step, software-pipelined: pair k+1's two x16 TMEM loads are
-      // in flight while pair k is computed): x = s*scale*log2e + T (masked, pre-scaled bias) in
-      // packed fp32x2; row max (FMNMX3); x stored compacted (below)
+      // ---- pass 1 (union row pair k per step, software-pipelined): x = s*scale*log2e + T in packed
+      // fp32x2 over this thread's 6 columns; row max (FMNMX3); x stored compacted: union row u at
+      // columns [12u, 12u+12) over consumed S columns, freeing [NSUB/2, 256) for O during pass 2
       float mx = -INFINITY;
       {
-        uint32_t S[2][32];
-        float2 T[2][12];  // bias pairs of the two rows of a union row pair (prefetched one pair ahead)
-        auto load_tbl = [&](int u, float2(&t)[12]) {
+        uint32_t S[2][16];  // [buffer][row a: 0-7 | row b: 8-15] (columns 6, 7 of each row unused)
+        float2 T[2][6];     // bias pairs: row a 0-2, row b 3-5
+        auto load_tbl = [&](int u, float2(&t)[6]) {
           const int pr = hr0 + rb + u;  // key row of union row u
           const bool rva = (unsigned)(pr - si) < (unsigned)Lh, rvb = (unsigned)(pr + 1 - si) < (unsigned)Lh;
           const float2 *ta = (const float2 *)(tcls + (rva ? pr - ic + L - 1 : C::TT) * kTblStride);
           const float2 *tb = (const float2 *)(tcls + (rvb ? pr + 1 - ic + L - 1 : C::TT) * kTblStride);
 #pragma unroll
-          for (int z = 0; z < 6; ++z) {
+          for (int z = 0; z < 3; ++z) {
             t[z] = ta[z];
-            t[6 + z] = tb[z];
+            t[3 + z] = tb[z];
           }
         };
-        tmem_ld16(lane_addr + uc, *reinterpret_cast<uint32_t(*)[16]>(&S[0][0]));
-        tmem_ld16(lane_addr + kHCP + uc, *reinterpret_cast<uint32_t(*)[16]>(&S[0][16]));
+        auto load_s = [&](int u, uint32_t(&d)[16]) {
+          tmem_ld_h8<6>(lane_addr + u * kHCP + uc, *reinterpret_cast<uint32_t(*)[8]>(&d[0]));
+          tmem_ld_h8<6>(lane_addr + (u + 1) * kHCP + uc, *reinterpret_cast<uint32_t(*)[8]>(&d[8]));
+        };
+        load_s(0, S[0]);
         load_tbl(0, T[0]);
 #pragma unroll
         for (int k = 0; k < C::PAIRS; ++k) {
           const int u = 2 * k;
-          uint32_t(&cur)[32] = S[k & 1];
-          const float2(&tc)[12] = T[k & 1];
+          uint32_t(&cur)[16] = S[k & 1];
+          const float2(&tc)[6] = T[k & 1];
           tc_wait_ld();
           if (k + 1 < C::PAIRS) {
-            const uint32_t cn = lane_addr + (u + 2) * kHCP + uc;
-            tmem_ld16(cn, *reinterpret_cast<uint32_t(*)[16]>(&S[(k + 1) & 1][0]));
-            tmem_ld16(cn + kHCP, *reinterpret_cast<uint32_t(*)[16]>(&S[(k + 1) & 1][16]));
+            load_s(u + 2, S[(k + 1) & 1]);
             load_tbl(u + 2, T[(k + 1) & 1]);
           }
-          float2 xa[6], xb[6];
-#pragma unroll
-          for (int z = 0; z < 6; ++z) {
-            xa[z] = __ffma2_rn(make_float2(__uint_as_float(cur[2 * z]), __uint_as_float(cur[2 * z + 1])), sl2x2, tc[z]);
-            xb[z] = __ffma2_rn(make_float2(__uint_as_float(cur[16 + 2 * z]), __uint_as_float(cur[17 + 2 * z])), sl2x2,
-                               tc[6 + z]);
-          }
-          float m[8];
+          float2 x[6];
 #pragma unroll
           for (int z = 0; z < 3; ++z) {
-            m[z] = fmax3(xa[2 * z].x, xa[2 * z].y, xa[2 * z + 1].x);
-            m[3 + z] = fmax3(xa[2 * z + 1].y, xb[2 * z].x, xb[2 * z].y);
+            x[z] = __ffma2_rn(make_float2(__uint_as_float(cur[2 * z]), __uint_as_float(cur[2 * z + 1])), sl2x2, tc[z]);
+            x[3 + z] = __ffma2_rn(make_float2(__uint_as_float(cur[8 + 2 * z]), __uint_as_float(cur[9 + 2 * z])), sl2x2,
+                                  tc[3 + z]);
           }
-          m[6] = fmax3(xb[1].x, xb[1].y, xb[3].x);
-          m[7] = fmax3(xb[3].y, xb[5].x, xb[5].y);
-          mx = fmax3(mx, fmax3(m[0], m[1], m[2]), fmax3(fmax3(m[3], m[4], m[5]), m[6], m[7]));
-          // compact store: x of union row u at columns [12u, 12u+12) -- over S rows <= u/2, already
-          // consumed -- so columns [NSUB/2, 256) are free for the O accumulators during pass 2
-          uint32_t xs[24];
-#pragma unroll
-          for (int z = 0; z < 6; ++z) {
-            xs[2 * z] = __float_as_uint(xa[z].x);
-            xs[2 * z + 1] = __float_as_uint(xa[z].y);
-            xs[12 + 2 * z] = __float_as_uint(xb[z].x);
-            xs[13 + 2 * z] = __float_as_uint(xb[z].y);
-          }
-          st_row<24>(lane_addr + u * 12, xs);
+          mx = fmax3(mx, fmax3(fmax3(x[0].x, x[0].y, x[1].x), fmax3(x[1].y, x[2].x, x[2].y),
+                               fmax3(x[3].x, x[3].y, x[4].x)),
+                     fmax3(x[4].y, x[5].x, x[5].y));
+          const uint32_t xa4[4] = {__float_as_uint(x[0].x), __float_as_uint(x[0].y), __float_as_uint(x[1].x),
+                                   __float_as_uint(x[1].y)};
+          const uint32_t xa2[2] = {__float_as_uint(x[2].x), __float_as_uint(x[2].y)};
+          const uint32_t xb4[4] = {__float_as_uint(x[3].x), __float_as_uint(x[3].y), __float_as_uint(x[4].x),
+                                   __float_as_uint(x[4].y)};
+          const uint32_t xb2[2] = {__float_as_uint(x[5].x), __float_as_uint(x[5].y)};
+          tmem_st_h4<6>(lane_addr + u * 12, xa4);
+          tmem_st_h2<6>(lane_addr + u * 12 + 4, xa2);
+          tmem_st_h4<6>(lane_addr + u * 12 + 12, xb4);
+          tmem_st_h2<6>(lane_addr + u * 12 + 16, xb2);
         }
       }
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));  // the query's other 6 columns
       tc_wait_st();
       if (tr) trace_ev(p, it, 6);
-      if (lane == 0) trace_ev(p, it, 14 + quarter);
-      // ---- pass 2 (row pair k per step, pipelined like pass 1): P = exp2(x - max) -> bf16 pairs in
-      // place (each halo row of P zeroed, then the union span written); pair k-1 is released to the
-      // PV MMAs once pair k is computed (its stores have drained by then)
+      // ---- pass 2 (row pair k per step, pipelined): P = exp2(x - max) -> bf16 pairs in place (each
+      // halo row of P zeroed, then the union span written); pair k-1 is released to the PV MMAs once
+      // pair k is computed (its stores have drained by then)
       float2 sum2 = make_float2(0.f, 0.f);
       const int zb = uc >> 1;  // packed column where the union span starts (warp-uniform)
       {
-        uint32_t X[2][24];
-        ld_row<24>(lane_addr, X[0]);
+        uint32_t X[2][12];  // [buffer][row a: 0-5 | row b: 6-11]
+        auto load_x = [&](int u, uint32_t(&d)[12]) {
+          tmem_ld_h4<6>(lane_addr + u * 12, *reinterpret_cast<uint32_t(*)[4]>(&d[0]));
+          tmem_ld_h2<6>(lane_addr + u * 12 + 4, *reinterpret_cast<uint32_t(*)[2]>(&d[4]));
+          tmem_ld_h4<6>(lane_addr + u * 12 + 12, *reinterpret_cast<uint32_t(*)[4]>(&d[6]));
+          tmem_ld_h2<6>(lane_addr + u * 12 + 16, *reinterpret_cast<uint32_t(*)[2]>(&d[10]));
+        };
+        load_x(0, X[0]);
+        const float2 nm = make_float2(-mx, -mx);
+        const uint32_t z4[4] = {0u, 0u, 0u, 0u}, z2[2] = {0u, 0u};
 #pragma unroll
         for (int k = 0; k < C::PAIRS; ++k) {
           const int u = 2 * k;
+          uint32_t(&cur)[12] = X[k & 1];
           tc_wait_ld();
-          if (k + 1 < C::PAIRS) ld_row<24>(lane_addr + (u + 2) * 12, X[(k + 1) & 1]);
-          uint32_t ra[12], rbv[12];
+          if (k + 1 < C::PAIRS) load_x(u + 2, X[(k + 1) & 1]);
+          uint32_t pk[6];
 #pragma unroll
-          for (int z = 0; z < 12; ++z) {
-            ra[z] = X[k & 1][z];
-            rbv[z] = X[k & 1][12 + z];
-          }
-          uint32_t pa[6], pb[6];
-          if (odd) {
-            p_row<true>(ra, mx, sum2, pa);
-            p_row<true>(rbv, mx, sum2, pb);
-          } else {
-            p_row<false>(ra, mx, sum2, pa);
-            p_row<false>(rbv, mx, sum2, pb);
+          for (int z = 0; z < 6; ++z) {
+            const float2 a = __fadd2_rn(make_float2(__uint_as_float(cur[2 * z]), __uint_as_float(cur[2 * z + 1])), nm);
+            const float2 e = make_float2(ex2(a.x), ex2(a.y));
+            sum2 = __fadd2_rn(sum2, e);
+            pk[z] = pack_bf16(e.x, e.y);
           }
           if (k > 0) {
             tc_wait_st();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&p_pair[slot * C::PAIRS + k - 1]);
-            if (lane == 0 && quarter == 0) trace_ev(p, it, 24 + k - 1);
           }
+          // P row u: 12 packed columns at [12u, 12u+12) -- each half zeroes its 6, then the union span
+          // (6 packed columns from zb; this thread's 3 at zb + 3 hf)
           const uint32_t prow = lane_addr + C::P_COL + u * (kHCP / 2);
-          st_zero12(prow);
-          st_zero12(prow + kHCP / 2);
-          st_row<6>(prow + zb, pa);
-          st_row<6>(prow + kHCP / 2 + zb, pb);
+          tmem_st_h4<6>(prow, z4);
+          tmem_st_h2<6>(prow + 4, z2);
+          tmem_st_h4<6>(prow + 12, z4);
+          tmem_st_h2<6>(prow + 16, z2);
+          const uint32_t pa2[2] = {pk[0], pk[1]}, pb2[2] = {pk[3], pk[4]};
+          tmem_st_h2<3>(prow + zb, pa2);
+          tmem_st_h1<3>(prow + zb + 2, pk[2]);
+          tmem_st_h2<3>(prow + 12 + zb, pb2);
+          tmem_st_h1<3>(prow + 12 + zb + 2, pk[5]);
         }
         tc_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_pair[slot * C::PAIRS + C::PAIRS - 1]);
-        if (lane == 0 && quarter == 0) trace_ev(p, it, 24 + C::PAIRS - 1);
       }
-      const float sum = sum2.x + sum2.y;
+      float sum = sum2.x + sum2.y;
+      sum += __shfl_xor_sync(0xffffffffu, sum, 16);
       if (tr) trace_ev(p, it, 7);
-      if (lane == 0) trace_ev(p, it, 10 + quarter);
-      // ---- epilogue: O / sum -> bf16, LSE
+      // ---- epilogue: O / sum -> bf16 (this thread: head dims [16 hf, 16 hf + 16)), LSE
       mbar_wait(&o_full[slot], ph);
       if (tr) trace_ev(p, it, 8);
       tc_fence_after();
-      uint32_t o[32];
+      float o[16];
       {
-        uint32_t oa[kOAcc][32];
+        uint32_t oa[kOAcc][16];
 #pragma unroll
-        for (int a = 0; a < kOAcc; ++a) tmem_ld32(lane_addr + C::O_COL + a * kD, oa[a]);
+        for (int a = 0; a < kOAcc; ++a) tmem_ld_h16<16>(lane_addr + C::O_COL + a * kD, oa[a]);
         tc_wait_ld();
 #pragma unroll
-        for (int z = 0; z < 32; ++z) {
+        for (int z = 0; z < 16; ++z) {
           float acc = __uint_as_float(oa[0][z]);
 #pragma unroll
           for (int a = 1; a < kOAcc; ++a) acc += __uint_as_float(oa[a][z]);
-          o[z] = __float_as_uint(acc);
+          o[z] = acc;
         }
       }
       tc_fence_before();
@@ -522,14 +504,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (i < q_end && j < p.W) {
         const float inv = 1.f / sum;
         const size_t qi = ((size_t)bh * p.q_rows + (i - p.q_row0)) * p.W + j;
-        uint4 *dst = (uint4 *)(p.out + qi * kD);
+        uint4 *dst = (uint4 *)(p.out + qi * kD + 16 * hf);
 #pragma unroll
-        for (int z = 0; z < kD; z += 8)
-          dst[z / 8] = make_uint4(pack_bf16(__uint_as_float(o[z]) * inv, __uint_as_float(o[z + 1]) * inv),
-                                  pack_bf16(__uint_as_float(o[z + 2]) * inv, __uint_as_float(o[z + 3]) * inv),
-                                  pack_bf16(__uint_as_float(o[z + 4]) * inv, __uint_as_float(o[z + 5]) * inv),
-                                  pack_bf16(__uint_as_float(o[z + 6]) * inv, __uint_as_float(o[z + 7]) * inv));
-        if (p.lse) p.lse[qi] = (mx + __log2f(sum)) * 0.69314718055994531f;
+        for (int z = 0; z < 16; z += 8)
+          dst[z / 8] = make_uint4(pack_bf16(o[z] * inv, o[z + 1] * inv), pack_bf16(o[z + 2] * inv, o[z + 3] * inv),
+                                  pack_bf16(o[z + 4] * inv, o[z + 5] * inv), pack_bf16(o[z + 6] * inv, o[z + 7] * inv));
+        if (p.lse && hf == 0) p.lse[qi] = (mx + __log2f(sum)) * 0.69314718055994531f;
       }
       if (tr) trace_ev(p, it, 9);
     }

@@ -196,6 +196,50 @@ __device__ __forceinline__ void tmem_st32_zero(uint32_t addr) {
       : "memory");
 }
 
+
+// ---- 16 lanes x 2 column blocks per warp (tcgen05 .16x32bx2): thread t < 16 accesses lane
+// (base + t) at columns [col, col + N), thread t >= 16 lane (base + t - 16) at columns
+// [col + SPLIT, col + SPLIT + N); base = the lane field of addr (0 or 16 within the warp's quarter).
+template <int SPLIT>
+__device__ __forceinline__ void tmem_ld_h8(uint32_t addr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.16x32bx2.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(addr), "n"(SPLIT));
+}
+template <int SPLIT>
+__device__ __forceinline__ void tmem_ld_h4(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.16x32bx2.x4.b32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr), "n"(SPLIT));
+}
+template <int SPLIT>
+__device__ __forceinline__ void tmem_ld_h2(uint32_t addr, uint32_t (&r)[2]) {
+  asm volatile("tcgen05.ld.sync.aligned.16x32bx2.x2.b32 {%0,%1}, [%2], %3;" : "=r"(r[0]), "=r"(r[1]) : "r"(addr), "n"(SPLIT));
+}
+template <int SPLIT>
+__device__ __forceinline__ void tmem_ld_h16(uint32_t addr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x32bx2.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16], %17;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(addr), "n"(SPLIT));
+}
+template <int SPLIT>
+__device__ __forceinline__ void tmem_st_h4(uint32_t addr, const uint32_t (&r)[4]) {
+  asm volatile("tcgen05.st.sync.aligned.16x32bx2.x4.b32 [%0], %5, {%1,%2,%3,%4};" ::"r"(addr), "r"(r[0]), "r"(r[1]),
+               "r"(r[2]), "r"(r[3]), "n"(SPLIT)
+               : "memory");
+}
+template <int SPLIT>
+__device__ __forceinline__ void tmem_st_h2(uint32_t addr, const uint32_t (&r)[2]) {
+  asm volatile("tcgen05.st.sync.aligned.16x32bx2.x2.b32 [%0], %3, {%1,%2};" ::"r"(addr), "r"(r[0]), "r"(r[1]), "n"(SPLIT)
+               : "memory");
+}
+template <int SPLIT>
+__device__ __forceinline__ void tmem_st_h1(uint32_t addr, uint32_t r) {
+  asm volatile("tcgen05.st.sync.aligned.16x32bx2.x1.b32 [%0], %2, {%1};" ::"r"(addr), "r"(r), "n"(SPLIT) : "memory");
+}
+
 // ---------------------------------------------------------------- UMMA
 // Shared-memory matrix descriptor, 64-byte swizzle (TMA CU_TENSOR_MAP_SWIZZLE_64B), rows of
 // 64 bytes (32 bf16), 8-row core groups 512 bytes apart.  Works both as a K-major operand
