@@ -69,47 +69,85 @@ def measured_peaks() -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled every 200 ms while the timed region runs."""
+    """SM clocks / clock-event (throttle) reasons sampled while the timed region runs: NVML polled
+    every ~0.5 ms by a helper process (a timed region of 20 steps lasts only ~8 ms), nvidia-smi
+    every 200 ms if NVML is unavailable."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event reason bits
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
 
     def __init__(self, index: int):
-        self.index = index
-        self.rows: list[list[str]] = []
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        ids = [x for x in vis.split(",") if x.strip()]
+        self.index = int(ids[index]) if index < len(ids) and ids[index].strip().isdigit() else index
+        self.rows: list[tuple] = []
         self._stop = threading.Event()
         self._t = None
 
+    POLL = ("import sys, time, pynvml as nv\n"
+            "nv.nvmlInit(); h = nv.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))\n"
+            "mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)\n"
+            "rs = getattr(nv, 'nvmlDeviceGetCurrentClocksEventReasons', None) or nv.nvmlDeviceGetCurrentClocksThrottleReasons\n"
+            "while True:\n"
+            "    print(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), mx, rs(h), flush=True)\n"
+            "    time.sleep(0.0005)\n")
+
     def __enter__(self):
-        def run():
-            while not self._stop.is_set():
-                try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                         timeout=5).stdout
-                    for line in out.strip().splitlines():
-                        self.rows.append([x.strip() for x in line.split(",")])
-                except Exception:
-                    pass
-                self._stop.wait(0.2)
-        self._t = threading.Thread(target=run, daemon=True)
-        self._t.start()
+        # a separate process polls NVML (~2 kHz), so the samples do not depend on this process's GIL
+        try:
+            self._p = subprocess.Popen([sys.executable, "-c", self.POLL, str(self.index)], stdout=subprocess.PIPE,
+                                       stderr=subprocess.DEVNULL, text=True)
+            first = self._p.stdout.readline()  # the poller is running before the timed region starts
+            if not first:
+                raise RuntimeError("nvml poller failed")
+            self._first = first
+        except Exception:
+            self._p = None
+            self._t = threading.Thread(target=self._run_smi, daemon=True)
+            self._t.start()
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self._p is not None:
+            self._p.terminate()
+            out, _ = self._p.communicate(timeout=10)
+            for line in (self._first + out).splitlines():
+                f = line.split()
+                if len(f) == 3:
+                    self.rows.append((float(f[0]), float(f[1]), int(f[2])))
+        else:
+            self._stop.set()
+            self._t.join(timeout=10)
+
+    def _run_smi(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout
+                for line in out.strip().splitlines():
+                    r = [x.strip() for x in line.split(",")]
+                    bits = 0
+                    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+                    for i, n in enumerate(names):
+                        if len(r) > 5 + i and r[5 + i] == "Active":
+                            bits |= self.BITS[n]
+                    if r[1].replace(".", "").isdigit():
+                        self.rows.append((float(r[1]), float(r[2]) if r[2].replace(".", "").isdigit() else 0.0, bits))
+            except Exception:
+                pass
+            self._stop.wait(0.2)
 
     def summary(self) -> dict:
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({n for r in self.rows for n, b in self.BITS.items() if r[2] & b})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(r[1] for r in self.rows),
+                "sm_mhz_min": min(sm), "reasons": reasons, "samples": len(self.rows)}
 
 
 def cpu_baseline(shape: Shape, target_s: float = 12.0) -> dict:
