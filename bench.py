@@ -325,6 +325,34 @@ def main():
                     "step_frac_hbm": ((260 + 516) * nq / (ms * 1e-3) / 1e9) / peaks["hbm_gbs"],
                     "step_frac_tensor": (f_fwd + f_bwd) / (ms * 1e-3) / 1e12 / peaks.get("bf16_tflops", 1659.7)}
 
+    # ---- context: the paper's own decomposition (QK+RPB kernel writing the attention
+    # weights, softmax, AV, and their gradients) on the same inputs, same device
+    paper = None
+    if not args.no_extras:
+        s0 = sets[0]
+        _, _, attn = na2d.paper_forward(s0["q"], s0["k"], s0["v"], rpb, L, scale)
+        dsb = torch.empty_like(attn)
+
+        def pstep(i):
+            s = sets[i % 2]
+            na2d.paper_forward(s["q"], s["k"], s["v"], rpb, L, scale)
+            na2d.paper_backward(s["q"], s["k"], s["v"], rpb, attn, s["dout"], L, scale, dS=dsb)
+
+        for i in range(2):
+            pstep(i)
+        barrier()
+        k3 = max(3, min(args.steps, 10))
+        e0.record()
+        for i in range(k3):
+            pstep(i)
+        e1.record()
+        barrier()
+        pms = e0.elapsed_time(e1) / k3
+        paper = {"value": (f_fwd + f_bwd) / (pms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": pms,
+                 "attn_bytes": attn.numel() * 4, "speedup_fused_vs_paper": pms / ms,
+                 "what": "paper's unfused decomposition on this GPU (na2d_paper_forward/backward, CUDA-core kernels)"}
+        del attn, dsb
+
     # ---- end to end through the host-buffer C-ABI entry (pinned host memory)
     e2e = None
     if not args.no_extras:
@@ -378,7 +406,7 @@ def main():
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": config_dict(shape, world),
                 "impl": "na2d", "gpu_launches": launches_per_step * args.steps,
                 "kernel_families": [na2d.na2d_kernel_family(p, 0), na2d.na2d_kernel_family(p, 1)],
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "paper_design": paper,
                 "clocks": sampler.summary() if sampler else None}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -121,6 +121,22 @@ na2d_status na2d_step_host(const na2d_problem *p, const void *q, const void *k, 
                            void *dk, void *dv, float *drpb, void *device_workspace,
                            size_t workspace_bytes, void *stream);
 
+/* The paper's own NA decomposition (App. A), kept as a
+ * comparison path: a QK kernel that adds the RPB while writing the attention weights
+ * [B][heads][rows][W][Lh*Lw] (fp32, Lh = min(L, height), Lw = min(L, width), window positions in
+ * row-major order), a softmax kernel (in place; writes lse) and an AV kernel; the backward runs
+ * the three kernels' gradients from the stored weights (dB by fp32 atomics, so its rounding order
+ * is not fixed).  Same semantics as na2d_forward / na2d_backward (Eq. 2).
+ * attn: device memory of na2d_paper_attn_bytes(p) bytes written by na2d_paper_forward and read by
+ * na2d_paper_backward; dS: another buffer of the same size (backward scratch).  All pointers
+ * 16-byte aligned device memory; lse required (it is written).  Errors as na2d_forward. */
+size_t na2d_paper_attn_bytes(const na2d_problem *p);
+na2d_status na2d_paper_forward(const na2d_problem *p, const void *q, const void *k, const void *v,
+                               const float *rpb, void *out, float *lse, float *attn, void *stream);
+na2d_status na2d_paper_backward(const na2d_problem *p, const void *q, const void *k, const void *v,
+                                const void *dout, const float *attn, float *dS, void *dq, void *dk,
+                                void *dv, float *drpb, void *stream);
+
 /* Number of kernel launches na2d_forward (which = 0) or na2d_backward (which = 1) issues
  * for this problem, or -1 if the problem is invalid.  For launch accounting in benchmarks. */
 int na2d_launch_count(const na2d_problem *p, int which);

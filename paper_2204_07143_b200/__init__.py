@@ -44,7 +44,7 @@ class na2d_problem(ctypes.Structure):
 EXPORTS = ("na2d_status_string", "na2d_version", "na2d_forward", "na2d_backward_workspace_bytes",
            "na2d_backward", "na2d_step_host_workspace_bytes", "na2d_step_host", "na2d_launch_count",
            "na2d_kernel_family", "na2d_profile_enable", "na2d_profile_read", "na2d_last_cuda_error",
-           "na2d_debug_set_trace")
+           "na2d_debug_set_trace", "na2d_paper_attn_bytes", "na2d_paper_forward", "na2d_paper_backward")
 
 _lib = None
 
@@ -78,6 +78,12 @@ def load_library():
     lib.na2d_kernel_family.restype = ctypes.c_char_p
     lib.na2d_last_cuda_error.restype = ctypes.c_char_p
     lib.na2d_debug_set_trace.argtypes = [ctypes.c_void_p]
+    lib.na2d_paper_attn_bytes.argtypes = [P]
+    lib.na2d_paper_attn_bytes.restype = SZ
+    lib.na2d_paper_forward.argtypes = [P] + [VP] * 8
+    lib.na2d_paper_forward.restype = ctypes.c_int
+    lib.na2d_paper_backward.argtypes = [P] + [VP] * 11
+    lib.na2d_paper_backward.restype = ctypes.c_int
     lib.na2d_debug_set_trace.restype = ctypes.c_int
     lib.na2d_profile_enable.argtypes = [ctypes.c_int]
     lib.na2d_profile_enable.restype = ctypes.c_int
@@ -220,4 +226,33 @@ def backward(q, k, v, rpb, out, lse, dout, kernel_size: int, scale: float | None
     na2d_backward(p, _dev(q, "q"), _dev(k, "k"), _dev(v, "v"), _dev(rpb, "rpb"), _dev(out, "out"),
                   _dev(lse, "lse"), _dev(dout, "dout"), _dev(dq, "dq"), _dev(dk, "dk"), _dev(dv, "dv"),
                   _dev(drpb, "drpb"), _dev(workspace, "workspace"), workspace.numel(), _stream(q))
+    return dq, dk, dv, drpb
+
+
+def paper_forward(q, k, v, rpb, kernel_size: int, scale: float | None = None):
+    """The paper's unfused decomposition: QK+RPB -> softmax -> AV, materialising the
+    attention weights.  Returns (out, lse, attn [B,heads,H,W,Lh*Lw] fp32)."""
+    import torch
+    p = problem_for(q, k, kernel_size, scale)
+    nwin = min(kernel_size, q.shape[2]) * min(kernel_size, q.shape[3])
+    out = torch.empty_like(q)
+    lse = torch.empty(q.shape[:4], device=q.device, dtype=torch.float32)
+    attn = torch.empty(q.shape[:4] + (nwin,), device=q.device, dtype=torch.float32)
+    _check(load_library().na2d_paper_forward(ctypes.byref(p), _dev(q, "q"), _dev(k, "k"), _dev(v, "v"),
+                                             _dev(rpb, "rpb"), _dev(out, "out"), _dev(lse, "lse"),
+                                             _dev(attn, "attn"), _stream(q)), "na2d_paper_forward")
+    return out, lse, attn
+
+
+def paper_backward(q, k, v, rpb, attn, dout, kernel_size: int, scale: float | None = None, dS=None):
+    """Gradients of the unfused decomposition from its stored attention weights."""
+    import torch
+    p = problem_for(q, k, kernel_size, scale)
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    drpb = torch.empty_like(rpb) if rpb is not None else None
+    dS = torch.empty_like(attn) if dS is None else dS
+    _check(load_library().na2d_paper_backward(ctypes.byref(p), _dev(q, "q"), _dev(k, "k"), _dev(v, "v"),
+                                              _dev(dout, "dout"), _dev(attn, "attn"), _dev(dS, "dS"),
+                                              _dev(dq, "dq"), _dev(dk, "dk"), _dev(dv, "dv"),
+                                              _dev(drpb, "drpb"), _stream(q)), "na2d_paper_backward")
     return dq, dk, dv, drpb

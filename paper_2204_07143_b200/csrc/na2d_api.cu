@@ -152,6 +152,39 @@ na2d_status na2d_backward(const na2d_problem *p, const void *q, const void *k, c
   return cuda_status(simt_backward(g, q, k, v, rpb, out, lse, dout, dq, dk, dv, drpb, D, st));
 }
 
+size_t na2d_paper_attn_bytes(const na2d_problem *p) {
+  Geo g;
+  if (make_geo(p, &g) != NA2D_OK) return 0;
+  return n_query(g) * (size_t)wlen(g.H, g.L) * wlen(g.W, g.L) * sizeof(float);
+}
+
+na2d_status na2d_paper_forward(const na2d_problem *p, const void *q, const void *k, const void *v, const float *rpb,
+                               void *out, float *lse, float *attn, void *stream) {
+  Geo g;
+  na2d_status s = make_geo(p, &g);
+  if (s != NA2D_OK) return s;
+  if (!q || !k || !v || !out || !lse || !attn) return NA2D_ERR_NULL_POINTER;
+  const void *ptrs[] = {q, k, v, rpb, out, lse, attn};
+  for (const void *ptr : ptrs)
+    if (!aligned16(ptr)) return NA2D_ERR_ALIGNMENT;
+  (void)cudaGetLastError();
+  return cuda_status(unfused_forward(g, q, k, v, rpb, out, lse, attn, (cudaStream_t)stream));
+}
+
+na2d_status na2d_paper_backward(const na2d_problem *p, const void *q, const void *k, const void *v, const void *dout,
+                                const float *attn, float *dS, void *dq, void *dk, void *dv, float *drpb,
+                                void *stream) {
+  Geo g;
+  na2d_status s = make_geo(p, &g);
+  if (s != NA2D_OK) return s;
+  if (!q || !k || !v || !dout || !attn || !dS || !dq || !dk || !dv) return NA2D_ERR_NULL_POINTER;
+  const void *ptrs[] = {q, k, v, dout, attn, dS, dq, dk, dv, drpb};
+  for (const void *ptr : ptrs)
+    if (!aligned16(ptr)) return NA2D_ERR_ALIGNMENT;
+  (void)cudaGetLastError();
+  return cuda_status(unfused_backward(g, q, k, v, dout, attn, dS, dq, dk, dv, drpb, (cudaStream_t)stream));
+}
+
 size_t na2d_step_host_workspace_bytes(const na2d_problem *p) {
   Geo g;
   if (make_geo(p, &g) != NA2D_OK) return 0;

@@ -53,6 +53,12 @@ cudaError_t simt_backward_dkdv(const Geo &g, const void *q, const void *k, const
                                const float *lse, const void *dout, const float *D, void *dk, void *dv,
                                cudaStream_t st);
 
+// The paper's unfused decomposition (QK+RPB -> softmax -> AV and gradients): na2d_unfused.cu
+cudaError_t unfused_forward(const Geo &g, const void *q, const void *k, const void *v, const float *rpb, void *out,
+                            float *lse, float *attn, cudaStream_t st);
+cudaError_t unfused_backward(const Geo &g, const void *q, const void *k, const void *v, const void *dout,
+                             const float *attn, float *dS, void *dq, void *dk, void *dv, float *drpb, cudaStream_t st);
+
 // Debug timeline buffer set through na2d_debug_set_trace (null = tracing off).
 void *debug_trace_buffer();
 
