@@ -33,10 +33,10 @@ using namespace sm100;
 using namespace tc;
 
 constexpr int kStages = 2;
-constexpr int kThreads = 320;  // warps 0-3 / 4-7 elementwise groups, warp 8 producer, warp 9 MMA
+constexpr int kThreads = 352;  // warps 0-3 / 4-7 elementwise, 8 producer, 9 S^T/dP^T issuer, 10 dV/dK issuer
 // (the sub-partition scheduler favours the highest warp id: the producer / MMA warps never wait for
 // the elementwise warps sharing their sub-partitions)
-constexpr int kProducerWarp = 8, kMmaWarp = 9;
+constexpr int kProducerWarp = 8, kMmaWarp = 9, kMmaKvWarp = 10;
 constexpr int kNCH = 96;       // queries per chunk (N of the S^T / dP^T MMAs)
 constexpr int kSlot = 192;     // TMEM columns per chunk slot: S^T [0,96), dP^T [96,192)
 constexpr int kACC_COL = 384;  // dV / dK accumulators: buffer b at 384 + 64b (dV), + 32 (dK)
@@ -234,7 +234,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t *bars = (uint64_t *)(smem + C::BAR_OFF);
   uint64_t *full = bars, *empty = bars + kStages;
   uint64_t *s_full = bars + 2 * kStages, *ds_full = s_full + 2, *acc_full = s_full + 4, *acc_free = s_full + 6;
-  uint32_t *tmem_slot = (uint32_t *)(bars + 2 * kStages + 8);
+  uint64_t *slot_free = s_full + 8;  // chunk slot x: the dV/dK MMAs reading it have completed
+  uint32_t *tmem_slot = (uint32_t *)(bars + 2 * kStages + 10);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int t_begin = (int)((long)p.num_tiles * blockIdx.x / gridDim.x);
@@ -266,6 +267,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&ds_full[s], 4);
       mbar_init(&acc_full[s], 1);
       mbar_init(&acc_free[s], 4);
+      mbar_init(&slot_free[s], 1);
     }
     fence_barrier_init();
     tma_prefetch(&tm_q);
@@ -374,35 +376,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) ktrace(p, it, 15);
     }
   } else if (warp == kMmaWarp) {
-    // ================= MMA issuer: S^T/dP^T of chunk c, then dV/dK of chunk c-1 (in-order tensor
-    // core => a chunk slot is rewritten only after the dV/dK MMAs that read it).  dV/dK accumulate
-    // in TMEM buffer (tile & 1), so a tile's MMAs never wait for the previous tile's epilogue.
+    // ================= S^T / dP^T issuer: chunk c into TMEM chunk slot c & 1, once the dV/dK MMAs
+    // of chunk c - 2 (which read that slot) have completed.  dV/dK have their own issuing warp, so
+    // neither stream waits behind the other's dependencies.
     constexpr uint32_t idesc_s = idesc_bf16(64, kNCH, false);
-    constexpr uint32_t idesc_o = idesc_bf16(64, kD, true);
-    const int ntiles = t_end - t_begin;
-    int it = 0, k = 0, c = 0;
-    int nch = 1, row0[2] = {0, 0};  // current tile: chunks, first halo row of each sub-tile
-    bool prev = false, prev_first = false, prev_last = false;
-    int prev_stage = 0, prev_it = 0, prev_row[2] = {0, 0};
-    for (;;) {
-      const bool have = it < ntiles;
+    int c = 0;
+    for (int it = 0; it < t_end - t_begin; ++it) {
       const int stage = it % kStages;
-      if (have) {
-        if (k == 0) {
-          mbar_wait(&full[stage], (it / kStages) & 1);
-          if (lane == 0) ktrace(p, c, 3);
-          tc_fence_after();
-          const TileInfo &ti = tinfo[stage];
-          nch = ti.nchunks;
-          row0[0] = ti.qs_lo[0] - ti.qr0;
-          row0[1] = ti.qs_lo[1] - ti.qr0;
-        }
+      mbar_wait(&full[stage], (it / kStages) & 1);
+      if (lane == 0) ktrace(p, c, 3);
+      const TileInfo &ti = tinfo[stage];
+      const int nch = ti.nchunks, row0a = ti.qs_lo[0] - ti.qr0, row0b = ti.qs_lo[1] - ti.qr0;
+      const uint64_t dqs = sdesc_sw64(smem_u32(smem + stage * C::STAGE_BYTES));
+      const uint64_t dkt = dqs + ((2 * C::Q_BYTES) >> 4), dvt = dkt + (C::KT_BYTES >> 4);
+      for (int k = 0; k < nch; ++k, ++c) {
         const int x = c & 1;
+        if (c >= 2) mbar_wait(&slot_free[x], ((c >> 1) - 1) & 1);
+        tc_fence_after();
         // descriptors: per-stage bases + immediate offsets (short issue bursts, no per-MMA chains)
-        const uint64_t dqs = sdesc_sw64(smem_u32(smem + stage * C::STAGE_BYTES));
-        const uint64_t dq0 = dqs + (((row0[0] + C::CR * k) * QP * kRowBytes) >> 4);
-        const uint64_t dq1 = dqs + (((row0[1] + C::CR * k) * QP * kRowBytes) >> 4);
-        const uint64_t dkt = dqs + ((2 * C::Q_BYTES) >> 4), dvt = dkt + (C::KT_BYTES >> 4);
+        const uint64_t dq0 = dqs + (((row0a + C::CR * k) * QP * kRowBytes) >> 4);
+        const uint64_t dq1 = dqs + (((row0b + C::CR * k) * QP * kRowBytes) >> 4);
         const uint32_t s0 = tmem + x * kSlot, s1 = s0 + ((uint32_t)16 << 16);
         if (elect_one()) {
 #pragma unroll
@@ -418,19 +411,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) ktrace(p, c, 0);
       }
-      if (prev) {
-        const int x = (c - 1) & 1, b = prev_it & 1;
-        mbar_wait(&ds_full[x], ((c - 1) >> 1) & 1);
-        if (lane == 0) ktrace(p, c - 1, 1);
-        if (prev_first) mbar_wait(&acc_free[b], ((prev_it >> 1) & 1) ^ 1);
-        if (lane == 0) ktrace(p, c - 1, 2);
+    }
+  } else if (warp == kMmaKvWarp) {
+    // ================= dV / dK issuer: chunk c once its P^T / dS^T are in TMEM; accumulates in TMEM
+    // buffer (tile & 1), so a tile's MMAs never wait for the previous tile's epilogue
+    constexpr uint32_t idesc_o = idesc_bf16(64, kD, true);
+    int c = 0;
+    for (int it = 0; it < t_end - t_begin; ++it) {
+      const int stage = it % kStages, b = it & 1;
+      // the stage cannot advance past this tile before this warp commits its empty[] below
+      mbar_wait(&full[stage], (it / kStages) & 1);
+      const TileInfo &ti = tinfo[stage];
+      const int nch = ti.nchunks, row0a = ti.qs_lo[0] - ti.qr0, row0b = ti.qs_lo[1] - ti.qr0;
+      const uint64_t dqs = sdesc_sw64(smem_u32(smem + stage * C::STAGE_BYTES));
+      const uint32_t o0 = tmem + kACC_COL + b * 2 * kD, o1 = o0 + ((uint32_t)16 << 16);
+      for (int k = 0; k < nch; ++k, ++c) {
+        const int x = c & 1;
+        mbar_wait(&ds_full[x], (c >> 1) & 1);
+        if (lane == 0) ktrace(p, c, 1);
+        if (k == 0) mbar_wait(&acc_free[b], ((it >> 1) & 1) ^ 1);
+        if (lane == 0) ktrace(p, c, 2);
         tc_fence_after();
-        const uint64_t dqs = sdesc_sw64(smem_u32(smem + prev_stage * C::STAGE_BYTES));
-        const uint64_t dq0 = dqs + ((prev_row[0] * QP * kRowBytes) >> 4);
-        const uint64_t dq1 = dqs + ((prev_row[1] * QP * kRowBytes) >> 4);
+        const uint64_t dq0 = dqs + (((row0a + C::CR * k) * QP * kRowBytes) >> 4);
+        const uint64_t dq1 = dqs + (((row0b + C::CR * k) * QP * kRowBytes) >> 4);
         const uint32_t a0 = tmem + x * kSlot, a1 = a0 + ((uint32_t)16 << 16);
-        const uint32_t o0 = tmem + kACC_COL + b * 2 * kD, o1 = o0 + ((uint32_t)16 << 16);
-        const uint32_t acc0 = prev_first ? 0u : 1u;
+        const uint32_t acc0 = k == 0 ? 0u : 1u;
         if (elect_one()) {
 #pragma unroll
           for (int ks = 0; ks < kNCH / 16; ++ks) {
@@ -441,25 +446,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_ts(o1, a1 + ks * 8, dq1 + doo, idesc_o, acc);
             mma_ts(o1 + kD, a1 + kNCH + ks * 8, dq1 + bo, idesc_o, acc);
           }
-          if (prev_last) {
+          mma_commit(&slot_free[x]);
+          if (k == nch - 1) {
             mma_commit(&acc_full[b]);
-            mma_commit(&empty[prev_stage]);
+            mma_commit(&empty[stage]);
           }
         }
         __syncwarp();
-      }
-      if (!have) break;
-      prev = true;
-      prev_first = k == 0;
-      prev_last = k == nch - 1;
-      prev_stage = stage;
-      prev_it = it;
-      prev_row[0] = row0[0] + C::CR * k;
-      prev_row[1] = row0[1] + C::CR * k;
-      ++c;
-      if (++k == nch) {
-        k = 0;
-        ++it;
       }
     }
   } else {
