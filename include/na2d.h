@@ -111,8 +111,12 @@ na2d_status na2d_backward(const na2d_problem *p, const void *q, const void *k, c
                           size_t workspace_bytes, void *stream);
 
 /* End-to-end step through HOST buffers: copies q,k,v,dout,rpb host->device, runs forward and
- * backward, copies out,lse,dq,dk,dv,drpb device->host, all enqueued on `stream`.  The host
- * buffers (pinned memory recommended) must stay valid until the stream is synchronised.
+ * backward, copies out,lse,dq,dk,dv,drpb device->host.  The work is pipelined over up to 8 batch
+ * chunks on three non-blocking streams owned by the library (created once per host thread and
+ * device): chunk c+1's host->device copies and chunk c-1's device->host copies overlap chunk c's
+ * kernels.  It starts after the work already enqueued on `stream`, and `stream` waits for its
+ * completion, so callers synchronise on `stream` as before.  The host buffers (pinned memory
+ * required for overlap) must stay valid until the stream is synchronised.
  * device_workspace: >= na2d_step_host_workspace_bytes(p) bytes of device memory.  Whole
  * maps only (no band fields). */
 size_t na2d_step_host_workspace_bytes(const na2d_problem *p);

@@ -185,14 +185,89 @@ na2d_status na2d_paper_backward(const na2d_problem *p, const void *q, const void
   return cuda_status(unfused_backward(g, q, k, v, dout, attn, dS, dq, dk, dv, drpb, (cudaStream_t)stream));
 }
 
+}  // extern "C" (reopened below)
+
+namespace na2d {
+namespace {
+
+constexpr int kHostChunks = 8;  // batch chunks of the pipelined host step
+
+// Per (host thread, device): the three non-blocking streams of the pipelined host step and its
+// events, created on first use and kept (no per-call allocation).
+struct HostPipe {
+  int dev = -1;
+  cudaStream_t in = nullptr, comp = nullptr, out = nullptr;
+  cudaEvent_t start = nullptr, done = nullptr, drpb_ready = nullptr;
+  cudaEvent_t in_ev[kHostChunks] = {}, comp_ev[kHostChunks] = {};
+};
+cudaError_t host_pipe(HostPipe **pp) {
+  static thread_local HostPipe pipes[8];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  HostPipe &hp = pipes[dev & 7];
+  if (hp.dev != dev) {
+    const unsigned fl = cudaStreamNonBlocking, ef = cudaEventDisableTiming;
+    if ((e = cudaStreamCreateWithFlags(&hp.in, fl)) != cudaSuccess) return e;
+    if ((e = cudaStreamCreateWithFlags(&hp.comp, fl)) != cudaSuccess) return e;
+    if ((e = cudaStreamCreateWithFlags(&hp.out, fl)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&hp.start, ef)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&hp.done, ef)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&hp.drpb_ready, ef)) != cudaSuccess) return e;
+    for (int c = 0; c < kHostChunks; ++c) {
+      if ((e = cudaEventCreateWithFlags(&hp.in_ev[c], ef)) != cudaSuccess) return e;
+      if ((e = cudaEventCreateWithFlags(&hp.comp_ev[c], ef)) != cudaSuccess) return e;
+    }
+    hp.dev = dev;
+  }
+  *pp = &hp;
+  return cudaSuccess;
+}
+
+// drpb = sum over chunks of the per-chunk tables, in chunk order (deterministic)
+__global__ void sum_tables_kernel(const float *__restrict__ parts, int nparts, size_t stride, int n,
+                                  float *__restrict__ dst) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int c = 0; c < nparts; ++c) acc += parts[(size_t)c * stride + e];
+    dst[e] = acc;
+  }
+}
+
+// Chunks are whole groups of `gran` images, so every chunk's tensor and LSE offsets stay
+// 16-byte aligned (the kernels' TMA descriptors need it).
+int host_gran(const Geo &g) {
+  const size_t per_img = (size_t)g.heads * g.q_rows * g.W, img_bytes = per_img * g.d * (g.dtype == NA2D_F32 ? 4 : 2);
+  for (int gr = 1; gr < 4; gr *= 2)
+    if ((gr * per_img) % 4 == 0 && (gr * img_bytes) % 16 == 0) return gr;
+  return 4;
+}
+int host_chunks(const Geo &g) {
+  const int units = (g.B + host_gran(g) - 1) / host_gran(g);
+  return units < kHostChunks ? units : kHostChunks;
+}
+int host_chunk_b0(const Geo &g, int c) {  // first image of chunk c (c = host_chunks(g) -> B)
+  const int gr = host_gran(g), units = (g.B + gr - 1) / gr, nc = host_chunks(g);
+  const int b = gr * (int)((long)units * c / nc);
+  return b < g.B ? b : g.B;
+}
+// per-chunk dRPB table stride in floats (16-byte aligned)
+size_t host_tbl_stride(const Geo &g) { return ((size_t)g.heads * (2 * g.L - 1) * (2 * g.L - 1) + 3) & ~(size_t)3; }
+
+}  // namespace
+}  // namespace na2d
+
+extern "C" {
+
 size_t na2d_step_host_workspace_bytes(const na2d_problem *p) {
   Geo g;
   if (make_geo(p, &g) != NA2D_OK) return 0;
   if (g.q_rows != g.H || g.kv_rows != g.H) return 0;
   const size_t t = align_up(n_query(g) * g.d * elem_size(g));
   const size_t TT = 2 * g.L - 1;
-  // q k v dout out dq dk dv | lse | rpb drpb | backward workspace
-  return 8 * t + align_up(n_query(g) * sizeof(float)) + 2 * align_up(g.heads * TT * TT * sizeof(float)) + bwd_ws(g);
+  // q k v dout out dq dk dv | lse | rpb drpb | per-chunk drpb | backward workspace (one chunk at a time)
+  return 8 * t + align_up(n_query(g) * sizeof(float)) + 2 * align_up(g.heads * TT * TT * sizeof(float)) +
+         align_up(host_chunks(g) * host_tbl_stride(g) * sizeof(float)) + bwd_ws(g);
 }
 
 na2d_status na2d_step_host(const na2d_problem *p, const void *q, const void *k, const void *v, const float *rpb,
@@ -212,36 +287,72 @@ na2d_status na2d_step_host(const na2d_problem *p, const void *q, const void *k, 
   const size_t bytes = n_query(g) * g.d * elem_size(g);
   const size_t t = align_up(bytes);
   const size_t TT = 2 * g.L - 1;
-  const size_t tb = g.heads * TT * TT * sizeof(float);
+  const size_t tbl = g.heads * TT * TT;
+  const size_t tb = tbl * sizeof(float);
   char *w = (char *)device_workspace;
   char *dq_ = w, *dk_ = w + t, *dv_ = w + 2 * t, *dout_ = w + 3 * t, *out_ = w + 4 * t;
   char *q_ = w + 5 * t, *k_ = w + 6 * t, *v_ = w + 7 * t;
   float *lse_ = (float *)(w + 8 * t);
   float *rpb_ = (float *)(w + 8 * t + align_up(n_query(g) * sizeof(float)));
   float *drpb_ = (float *)((char *)rpb_ + align_up(tb));
-  char *ws = (char *)drpb_ + align_up(tb);
-  cudaError_t e = cudaSuccess;
-#define NA2D_TRY(x)                  \
-  do {                               \
-    e = (x);                         \
+  const int nc = host_chunks(g);
+  float *drpb_parts = (float *)((char *)drpb_ + align_up(tb));
+  const size_t tstride = host_tbl_stride(g);
+  char *ws = (char *)drpb_parts + align_up(nc * tstride * sizeof(float));
+  HostPipe *hp = nullptr;
+  cudaError_t e = host_pipe(&hp);
+  if (e != cudaSuccess) return cuda_status(e);
+#define NA2D_TRY(x)                              \
+  do {                                           \
+    e = (x);                                     \
     if (e != cudaSuccess) return cuda_status(e); \
   } while (0)
-  NA2D_TRY(cudaMemcpyAsync(q_, q, bytes, cudaMemcpyHostToDevice, st));
-  NA2D_TRY(cudaMemcpyAsync(k_, k, bytes, cudaMemcpyHostToDevice, st));
-  NA2D_TRY(cudaMemcpyAsync(v_, v, bytes, cudaMemcpyHostToDevice, st));
-  NA2D_TRY(cudaMemcpyAsync(dout_, dout, bytes, cudaMemcpyHostToDevice, st));
-  if (rpb) NA2D_TRY(cudaMemcpyAsync(rpb_, rpb, tb, cudaMemcpyHostToDevice, st));
-  s = na2d_forward(p, q_, k_, v_, rpb ? rpb_ : nullptr, out_, lse_, stream);
-  if (s != NA2D_OK) return s;
-  s = na2d_backward(p, q_, k_, v_, rpb ? rpb_ : nullptr, out_, lse_, dout_, dq_, dk_, dv_, rpb ? drpb_ : nullptr, ws,
-                    bwd_ws(g), stream);
-  if (s != NA2D_OK) return s;
-  NA2D_TRY(cudaMemcpyAsync(out, out_, bytes, cudaMemcpyDeviceToHost, st));
-  NA2D_TRY(cudaMemcpyAsync(lse, lse_, n_query(g) * sizeof(float), cudaMemcpyDeviceToHost, st));
-  NA2D_TRY(cudaMemcpyAsync(dq, dq_, bytes, cudaMemcpyDeviceToHost, st));
-  NA2D_TRY(cudaMemcpyAsync(dk, dk_, bytes, cudaMemcpyDeviceToHost, st));
-  NA2D_TRY(cudaMemcpyAsync(dv, dv_, bytes, cudaMemcpyDeviceToHost, st));
-  if (drpb) NA2D_TRY(cudaMemcpyAsync(drpb, drpb_, tb, cudaMemcpyDeviceToHost, st));
+  // Pipelined over batch chunks on three streams: copies in (H2D) for chunk c + 1 and copies out
+  // (D2H) for chunk c - 1 run on the copy engines while chunk c computes; ordered after the
+  // caller's prior work on `stream`, and `stream` waits for the last copy.
+  NA2D_TRY(cudaEventRecord(hp->start, st));
+  NA2D_TRY(cudaStreamWaitEvent(hp->in, hp->start, 0));
+  NA2D_TRY(cudaStreamWaitEvent(hp->comp, hp->start, 0));
+  NA2D_TRY(cudaStreamWaitEvent(hp->out, hp->start, 0));
+  if (rpb) NA2D_TRY(cudaMemcpyAsync(rpb_, rpb, tb, cudaMemcpyHostToDevice, hp->in));
+  const size_t per_img = bytes / g.B, lse_per_img = (size_t)g.heads * g.q_rows * g.W * sizeof(float);
+  for (int c = 0; c < nc; ++c) {
+    const int b0 = host_chunk_b0(g, c), b1 = host_chunk_b0(g, c + 1);
+    if (b1 <= b0) continue;
+    const size_t off = (size_t)b0 * per_img, n = (size_t)(b1 - b0) * per_img;
+    const size_t loff = (size_t)b0 * lse_per_img, ln = (size_t)(b1 - b0) * lse_per_img;
+    NA2D_TRY(cudaMemcpyAsync(q_ + off, (const char *)q + off, n, cudaMemcpyHostToDevice, hp->in));
+    NA2D_TRY(cudaMemcpyAsync(k_ + off, (const char *)k + off, n, cudaMemcpyHostToDevice, hp->in));
+    NA2D_TRY(cudaMemcpyAsync(v_ + off, (const char *)v + off, n, cudaMemcpyHostToDevice, hp->in));
+    NA2D_TRY(cudaMemcpyAsync(dout_ + off, (const char *)dout + off, n, cudaMemcpyHostToDevice, hp->in));
+    NA2D_TRY(cudaEventRecord(hp->in_ev[c], hp->in));
+    NA2D_TRY(cudaStreamWaitEvent(hp->comp, hp->in_ev[c], 0));
+    na2d_problem pc = *p;
+    pc.batch = b1 - b0;
+    s = na2d_forward(&pc, q_ + off, k_ + off, v_ + off, rpb ? rpb_ : nullptr, out_ + off,
+                     (float *)((char *)lse_ + loff), hp->comp);
+    if (s != NA2D_OK) return s;
+    s = na2d_backward(&pc, q_ + off, k_ + off, v_ + off, rpb ? rpb_ : nullptr, out_ + off,
+                      (float *)((char *)lse_ + loff), dout_ + off, dq_ + off, dk_ + off, dv_ + off,
+                      rpb ? drpb_parts + c * tstride : nullptr, ws, bwd_ws(g), hp->comp);
+    if (s != NA2D_OK) return s;
+    NA2D_TRY(cudaEventRecord(hp->comp_ev[c], hp->comp));
+    NA2D_TRY(cudaStreamWaitEvent(hp->out, hp->comp_ev[c], 0));
+    NA2D_TRY(cudaMemcpyAsync((char *)out + off, out_ + off, n, cudaMemcpyDeviceToHost, hp->out));
+    NA2D_TRY(cudaMemcpyAsync((char *)lse + loff, (char *)lse_ + loff, ln, cudaMemcpyDeviceToHost, hp->out));
+    NA2D_TRY(cudaMemcpyAsync((char *)dq + off, dq_ + off, n, cudaMemcpyDeviceToHost, hp->out));
+    NA2D_TRY(cudaMemcpyAsync((char *)dk + off, dk_ + off, n, cudaMemcpyDeviceToHost, hp->out));
+    NA2D_TRY(cudaMemcpyAsync((char *)dv + off, dv_ + off, n, cudaMemcpyDeviceToHost, hp->out));
+  }
+  if (drpb) {
+    sum_tables_kernel<<<(unsigned)((tbl + 255) / 256), 256, 0, hp->comp>>>(drpb_parts, nc, tstride, (int)tbl, drpb_);
+    NA2D_TRY(cudaGetLastError());
+    NA2D_TRY(cudaEventRecord(hp->drpb_ready, hp->comp));
+    NA2D_TRY(cudaStreamWaitEvent(hp->out, hp->drpb_ready, 0));
+    NA2D_TRY(cudaMemcpyAsync(drpb, drpb_, tb, cudaMemcpyDeviceToHost, hp->out));
+  }
+  NA2D_TRY(cudaEventRecord(hp->done, hp->out));
+  NA2D_TRY(cudaStreamWaitEvent(st, hp->done, 0));
 #undef NA2D_TRY
   return NA2D_OK;
 }
