@@ -111,6 +111,15 @@ __device__ __forceinline__ int key_col0(const BwdKParams &p, int tcol, int L) {
   return tcol * kTQW;
 }
 
+// Query rows chunk k of a key tile actually needs, rounded up to even (a row pair is 3 MMA K-steps):
+// the last chunk of an interior tile holds 2 of its 4 rows, so its MMAs use N = 48 and its
+// elementwise pass stops after one row pair.
+template <int CR>
+__device__ __forceinline__ int chunk_rows_even(int qs_n0, int qs_n1, int k) {
+  const int rows = max(qs_n0, qs_n1) - CR * k;
+  return rows >= CR ? CR : max(2, (rows + 1) & ~1);
+}
+
 struct KTile {
   int bh, kr0, kc0;   // key tile origin (global row, column)
   int qr0, qc0;       // query halo origin (global)
@@ -151,12 +160,14 @@ __device__ __forceinline__ KTile ktile(const BwdKParams &p, int t) {
 template <int L, int QP, bool FAST>
 __device__ __forceinline__ void chunk_rows(uint32_t lane_addr, int uc, const float *tbl_row0,
                                            const int (&colterm)[CfgK<L, QP>::UCW], const float *lrow0,
-                                           int pk, int i_base, int H, int rows_here, int Lh, float sl2) {
+                                           int pk, int i_base, int H, int rows_here, int Lh, float sl2,
+                                           int rows_even) {
   using C = CfgK<L, QP>;
   constexpr int UW = FAST ? C::UCWF : C::UCW;
   constexpr float log2e = 1.4426950408889634f;
 #pragma unroll
   for (int u0 = 0; u0 < C::CR; u0 += 2) {
+    if (u0 >= rows_even) break;  // rows past the chunk's (even) row count are never read by the MMAs
     // two chunk rows per step: all four x16 TMEM loads in flight before the wait
     constexpr int NR = 2;
     uint32_t sv[NR][16], dpv[NR][16];
@@ -380,6 +391,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // of chunk c - 2 (which read that slot) have completed.  dV/dK have their own issuing warp, so
     // neither stream waits behind the other's dependencies.
     constexpr uint32_t idesc_s = idesc_bf16(64, kNCH, false);
+    constexpr uint32_t idesc_s2 = idesc_bf16(64, 2 * QP, false);  // a chunk of one row pair
     int c = 0;
     for (int it = 0; it < t_end - t_begin; ++it) {
       const int stage = it % kStages;
@@ -387,10 +399,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) ktrace(p, c, 3);
       const TileInfo &ti = tinfo[stage];
       const int nch = ti.nchunks, row0a = ti.qs_lo[0] - ti.qr0, row0b = ti.qs_lo[1] - ti.qr0;
+      const int qn0 = ti.qs_n[0], qn1 = ti.qs_n[1];
       const uint64_t dqs = sdesc_sw64(smem_u32(smem + stage * C::STAGE_BYTES));
       const uint64_t dkt = dqs + ((2 * C::Q_BYTES) >> 4), dvt = dkt + (C::KT_BYTES >> 4);
       for (int k = 0; k < nch; ++k, ++c) {
         const int x = c & 1;
+        const uint32_t ids = chunk_rows_even<C::CR>(qn0, qn1, k) == C::CR ? idesc_s : idesc_s2;
         if (c >= 2) mbar_wait(&slot_free[x], ((c >> 1) - 1) & 1);
         tc_fence_after();
         // descriptors: per-stage bases + immediate offsets (short issue bursts, no per-MMA chains)
@@ -401,10 +415,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int kk = 0; kk < kD / 16; ++kk) {
             const uint32_t ko = (kk * 32) >> 4;
-            mma_ss(s0, dkt + ko, dq0 + ko, idesc_s, kk);
-            mma_ss(s0 + kNCH, dvt + ko, dq0 + (C::Q_BYTES >> 4) + ko, idesc_s, kk);
-            mma_ss(s1, dkt + (4096 >> 4) + ko, dq1 + ko, idesc_s, kk);
-            mma_ss(s1 + kNCH, dvt + (4096 >> 4) + ko, dq1 + (C::Q_BYTES >> 4) + ko, idesc_s, kk);
+            mma_ss(s0, dkt + ko, dq0 + ko, ids, kk);
+            mma_ss(s0 + kNCH, dvt + ko, dq0 + (C::Q_BYTES >> 4) + ko, ids, kk);
+            mma_ss(s1, dkt + (4096 >> 4) + ko, dq1 + ko, ids, kk);
+            mma_ss(s1 + kNCH, dvt + (4096 >> 4) + ko, dq1 + (C::Q_BYTES >> 4) + ko, ids, kk);
           }
           mma_commit(&s_full[x]);
         }
@@ -423,6 +437,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&full[stage], (it / kStages) & 1);
       const TileInfo &ti = tinfo[stage];
       const int nch = ti.nchunks, row0a = ti.qs_lo[0] - ti.qr0, row0b = ti.qs_lo[1] - ti.qr0;
+      const int qn0 = ti.qs_n[0], qn1 = ti.qs_n[1];
       const uint64_t dqs = sdesc_sw64(smem_u32(smem + stage * C::STAGE_BYTES));
       const uint32_t o0 = tmem + kACC_COL + b * 2 * kD, o1 = o0 + ((uint32_t)16 << 16);
       for (int k = 0; k < nch; ++k, ++c) {
@@ -436,9 +451,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t dq1 = dqs + (((row0b + C::CR * k) * QP * kRowBytes) >> 4);
         const uint32_t a0 = tmem + x * kSlot, a1 = a0 + ((uint32_t)16 << 16);
         const uint32_t acc0 = k == 0 ? 0u : 1u;
+        const int nks = chunk_rows_even<C::CR>(qn0, qn1, k) * QP / 16;  // K-steps actually holding P / dS
         if (elect_one()) {
 #pragma unroll
           for (int ks = 0; ks < kNCH / 16; ++ks) {
+            if (ks >= nks) break;
             const uint32_t acc = ks == 0 ? acc0 : 1u;
             const uint32_t bo = (ks * 16 * kRowBytes) >> 4, doo = (C::Q_BYTES >> 4) + bo;
             mma_ts(o0, a0 + ks * 8, dq0 + doo, idesc_o, acc);              // dV += P^T dO
@@ -520,6 +537,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const TileInfo &ti = tinfo[stage];
       const int h = ti.head, bh = ti.bh, kr0 = ti.kr0, kc0 = ti.kc0, qr0 = ti.qr0, qc0 = ti.qc0;
       const int nch = ti.nchunks, qs_lo = ti.qs_lo[half], qs_n = ti.qs_n[half];
+      const int qn0 = ti.qs_n[0], qn1 = ti.qs_n[1];
       const int uc = ti.uc[quarter];
       const bool fast = ti.fast[quarter];
       int colterm[C::UCW];
@@ -553,9 +571,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         // clips, so its P / dS columns may hold anything
         if (kc0 + 4 * quarter < p.W) {
           if (fast)
-            chunk_rows<L, QP, true>(lane_addr, uc, tbl_row0, colterm, lrow0, pk, i_base, p.H, rows_here, Lh, sl2);
+            chunk_rows<L, QP, true>(lane_addr, uc, tbl_row0, colterm, lrow0, pk, i_base, p.H, rows_here, Lh, sl2,
+                                    chunk_rows_even<C::CR>(qn0, qn1, k));
           else
-            chunk_rows<L, QP, false>(lane_addr, uc, tbl_row0, colterm, lrow0, pk, i_base, p.H, rows_here, Lh, sl2);
+            chunk_rows<L, QP, false>(lane_addr, uc, tbl_row0, colterm, lrow0, pk, i_base, p.H, rows_here, Lh, sl2,
+                                     chunk_rows_even<C::CR>(qn0, qn1, k));
         }
         tc_wait_st();
         tc_fence_before();
