@@ -80,6 +80,9 @@ struct BwdKParams {
   int tma_lsd;  // LSE / D halos by TMA (W * 4 bytes 16-byte aligned) instead of lane loads
   float scale;
   const float *rpb, *lse, *D;
+  const float *drpb_part;  // B1's per-CTA dRPB tables (null: nothing to reduce)
+  int part_ctas;
+  float *drpb;
   __nv_bfloat16 *dk, *dv;
   long long *trace;
 };
@@ -253,6 +256,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int t_end = (int)((long)p.num_tiles * (blockIdx.x + 1) / gridDim.x);
   const int q_end = p.q_row0 + p.q_rows;
 
+  // a10 final: dRPB = sum of B1's per-CTA partial tables, one warp per cell, lane l summing CTAs
+  // l, l + 32, ... in order, then a fixed butterfly (deterministic for a given B1 grid)
+  if (p.drpb_part) {
+    const int n = p.heads * (2 * L - 1) * (2 * L - 1);
+    for (int e = blockIdx.x * (kThreads / 32) + warp; e < n; e += gridDim.x * (kThreads / 32)) {
+      float acc = 0.f;
+      for (int b = lane; b < p.part_ctas; b += 32) acc += __ldg(&p.drpb_part[(size_t)b * n + e]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) p.drpb[e] = acc;
+    }
+  }
   // zero the never-loaded tail rows of the Q / dO halos (read by partial chunks)
   for (int s = 0; s < kStages; ++s)
     for (int q2 = 0; q2 < 2; ++q2) {
@@ -609,7 +624,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int L, int QP>
 cudaError_t launch_dkdv_t(const Geo &g, const void *q, const void *k, const void *v, const float *rpb,
-                          const float *lse, const void *dout, const float *D, void *dk, void *dv, cudaStream_t st) {
+                          const float *lse, const void *dout, const float *D, void *dk, void *dv,
+                          const float *drpb_part, int part_ctas, float *drpb, cudaStream_t st) {
   using C = CfgK<L, QP>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
@@ -650,6 +666,9 @@ cudaError_t launch_dkdv_t(const Geo &g, const void *q, const void *k, const void
   p.rpb = rpb;
   p.lse = lse;
   p.D = D;
+  p.drpb_part = drpb_part;
+  p.part_ctas = part_ctas;
+  p.drpb = drpb;
   p.dk = (__nv_bfloat16 *)dk;
   p.dv = (__nv_bfloat16 *)dv;
   p.trace = (long long *)debug_trace_buffer();
@@ -694,14 +713,14 @@ bool tc_dkdv_supported(const Geo &g) {
 
 cudaError_t tc_backward_dkdv(const Geo &g, const void *q, const void *k, const void *v, const float *rpb,
                              const float *lse, const void *dout, const float *D, void *dk, void *dv,
-                             cudaStream_t st) {
+                             const float *drpb_part, int part_ctas, float *drpb, cudaStream_t st) {
   // the query halo of a 16-column key tile is at most 16 + 2NS + 1 <= 23 columns away from the right
   // clamp zone; tiles reaching it are shifted (key_col0)
   if (!tc_dkdv_supported(g)) return cudaErrorNotSupported;
   switch (g.L) {
-    case 3: return launch_dkdv_t<3, 24>(g, q, k, v, rpb, lse, dout, D, dk, dv, st);
-    case 5: return launch_dkdv_t<5, 24>(g, q, k, v, rpb, lse, dout, D, dk, dv, st);
-    case 7: return launch_dkdv_t<7, 24>(g, q, k, v, rpb, lse, dout, D, dk, dv, st);
+    case 3: return launch_dkdv_t<3, 24>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, st);
+    case 5: return launch_dkdv_t<5, 24>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, st);
+    case 7: return launch_dkdv_t<7, 24>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, st);
   }
   return cudaErrorInvalidValue;
 }

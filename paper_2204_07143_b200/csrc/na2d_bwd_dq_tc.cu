@@ -524,18 +524,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// drpb[h][c] = sum over CTAs of drpb_part[cta][h][c]: one warp per cell, lane l sums CTAs
-// l, l+32, ... in order, then a fixed butterfly -- deterministic for a given CTA count.
-__global__ void drpb_reduce_kernel(const float *__restrict__ part, int ctas, int n, float *__restrict__ drpb) {
-  const int e = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
-  if (e >= n) return;
-  float s = 0.f;
-  for (int b = lane; b < ctas; b += 32) s += part[(size_t)b * n + e];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) drpb[e] = s;
-}
-
 template <int L>
 cudaError_t launch_dq(const Geo &g, const void *q, const void *k, const void *v, const float *rpb, const void *out,
                       const float *lse, const void *dout, void *dq, float *drpb, float *D, float *part,
@@ -584,13 +572,7 @@ cudaError_t launch_dq(const Geo &g, const void *q, const void *k, const void *v,
     ProfScope ps("na2d_bwd_dq_tc", st);
     na2d_bwd_dq_kernel<L><<<grid, kThreads, C::SMEM, st>>>(tq, tdo, tk, tv, tdq, p);
   }
-  e = cudaGetLastError();
-  if (e != cudaSuccess || !rpb) return e;
-  {
-    ProfScope ps("na2d_bwd_drpb_reduce", st);
-    const int n = g.heads * TT * TT;
-    drpb_reduce_kernel<<<(n + 3) / 4, 128, 0, st>>>(part, grid, n, drpb);
-  }
+  // the per-CTA dRPB partial tables are summed by the dK/dV kernel (B2), which runs next
   return cudaGetLastError();
 }
 

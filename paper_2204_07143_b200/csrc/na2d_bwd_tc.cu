@@ -60,12 +60,13 @@ cudaError_t tc_backward(const Geo &g, const void *q, const void *k, const void *
                         float *drpb, float *D, void *scratch, cudaStream_t st) {
   cudaError_t e = tc_backward_dq(g, q, k, v, rpb, out, lse, dout, dq, drpb, D, (float *)scratch, st);
   if (e != cudaSuccess) return e;
-  return tc_backward_dkdv(g, q, k, v, rpb, lse, dout, D, dk, dv, st);
+  return tc_backward_dkdv(g, q, k, v, rpb, lse, dout, D, dk, dv, rpb ? (const float *)scratch : nullptr,
+                          dq_grid(g), drpb, st);
 }
 
 int tc_launches(const Geo &g, int which) {
   if (which == 0) return 1;
-  return 2 + (1 /* dK/dV */);
+  return 2;  // B1 (dQ, D, per-CTA dRPB partials), B2 (dK, dV, and the dRPB partial reduction)
 }
 
 }  // namespace na2d

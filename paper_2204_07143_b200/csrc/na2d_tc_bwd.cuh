@@ -62,9 +62,11 @@ struct BwdQParams {
 int dq_grid(const Geo &g);
 int max_query_halo_width(const Geo &g, bool shift);
 bool tc_dkdv_supported(const Geo &g);
+// drpb_part (may be null): B1's per-CTA dRPB tables [part_ctas][heads][(2L-1)^2]; B2 sums them
+// into drpb (fixed CTA order, one warp per cell) before its own work
 cudaError_t tc_backward_dkdv(const Geo &g, const void *q, const void *k, const void *v, const float *rpb,
                              const float *lse, const void *dout, const float *D, void *dk, void *dv,
-                             cudaStream_t st);
+                             const float *drpb_part, int part_ctas, float *drpb, cudaStream_t st);
 cudaError_t tc_backward_dq(const Geo &g, const void *q, const void *k, const void *v, const float *rpb,
                            const void *out, const float *lse, const void *dout, void *dq, float *drpb, float *D,
                            float *part, cudaStream_t st);
