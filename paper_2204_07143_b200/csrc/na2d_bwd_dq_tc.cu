@@ -153,6 +153,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&tm_dq);
   }
   for (int c = threadIdx.x; c < 8 * kGroups * C::TT * C::TT; c += kThreads) s_db[c] = 0.f;
+  if (p.drpb_part)  // this CTA's partial tables (only this CTA writes them; B2 reads them after B1)
+    for (int c = threadIdx.x; c < p.heads * C::TT * C::TT; c += kThreads)
+      p.drpb_part[(size_t)blockIdx.x * p.heads * C::TT * C::TT + c] = 0.f;
   if (warp == kProducerWarp) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
@@ -562,12 +565,7 @@ cudaError_t launch_dq(const Geo &g, const void *q, const void *k, const void *v,
   p.drpb_part = rpb ? part : nullptr;
   p.trace = (long long *)debug_trace_buffer();
   const int grid = dq_grid(g);
-  const int TT = 2 * L - 1;
-  cudaError_t e;
-  if (rpb) {
-    e = cudaMemsetAsync(part, 0, sizeof(float) * grid * g.heads * TT * TT, st);
-    if (e != cudaSuccess) return e;
-  }
+  (void)drpb;  // summed from the partial tables by B2
   {
     ProfScope ps("na2d_bwd_dq_tc", st);
     na2d_bwd_dq_kernel<L><<<grid, kThreads, C::SMEM, st>>>(tq, tdo, tk, tv, tdq, p);
