@@ -78,6 +78,7 @@ struct BwdKParams {
   int tiles_h, tiles_w, num_tiles;
   int shift_cols;  // last two key tile columns start at W-L-16 and W-16 (key_col0)
   int tma_lsd;  // LSE / D halos by TMA (W * 4 bytes 16-byte aligned) instead of lane loads
+  int *tile_counter;  // dynamic tile scheduler (zero at launch): CTA b takes tile b, then gridDim + atomicAdd
   float scale;
   const float *rpb, *lse, *D;
   const float *drpb_part;  // B1's per-CTA dRPB tables (null: nothing to reduce)
@@ -134,9 +135,12 @@ template <int L, int QP>
 __device__ __forceinline__ KTile ktile(const BwdKParams &p, int t) {
   using C = CfgK<L, QP>;
   KTile g;
+  // head-major order: consecutive tiles share the head, so the bias table is rebuilt only when a
+  // CTA's next (dynamically scheduled) tile belongs to the other head
   const int per = p.tiles_h * p.tiles_w;
-  g.bh = t / per;
-  const int rem = t - g.bh * per;
+  const int u = t / per, rem = t - u * per;
+  const int h = u / p.B;
+  g.bh = (u - h * p.B) * p.heads + h;
   g.kr0 = p.kv_row0 + (rem / p.tiles_w) * kTQH;
   g.kc0 = key_col0(p, rem % p.tiles_w, L);
   const int q_end = p.q_row0 + p.q_rows, kv_end = p.kv_row0 + p.kv_rows;
@@ -252,8 +256,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t *tmem_slot = (uint32_t *)(bars + 2 * kStages + 10);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int t_begin = (int)((long)p.num_tiles * blockIdx.x / gridDim.x);
-  const int t_end = (int)((long)p.num_tiles * (blockIdx.x + 1) / gridDim.x);
   const int q_end = p.q_row0 + p.q_rows;
 
   // a10 final: dRPB = sum of B1's per-CTA partial tables, one warp per cell, lane l summing CTAs
@@ -306,6 +308,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   if (warp == kProducerWarp) tmem_alloc<512>(tmem_slot);
+#ifdef NA2D_TRACE
+  if (threadIdx.x == 0 && p.trace) {  // per-CTA wall-clock span (load balance)
+    uint64_t gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    p.trace[17408 + 2 * blockIdx.x] = (long long)gt;
+  }
+#endif
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -314,13 +323,27 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == kProducerWarp) {
     // ================= producer: tile description, TMA (K, V sub-tile blocks; Q, dO halos) + LSE / D
+    // Tiles are handed out dynamically (the first one per CTA statically): a CTA that runs ahead takes
+    // more tiles, so the kernel does not wait for the slowest static share.  After the last tile a
+    // description with bh = -1 ends every consumer's loop.
     int it = 0;
-    for (int t = t_begin; t < t_end; ++t, ++it) {
+    for (int t = blockIdx.x;; ++it) {
       const int s = it % kStages;
       mbar_wait_sleep(&empty[s], ((it / kStages) & 1) ^ 1, 1024);
+      TileInfo *ti = tinfo + s;
+      if (t >= p.num_tiles) {  // end of work: sentinel, released like a loaded stage
+        if (lane == 0) {
+          ti->bh = -1;
+          mbar_arrive(&full[s]);
+        }
+        if (!p.tma_lsd) {
+          __syncwarp();
+          mbar_arrive(&full[s]);  // the 32 lane arrivals of the LSE / D staging
+        }
+        break;
+      }
       if (lane == 0) ktrace(p, it, 14);
       const KTile g = ktile<L, QP>(p, t);
-      TileInfo *ti = tinfo + s;
       if (lane < 4) {  // union origin of lane quarter q = lane (warp-uniform in the consumers)
         const int ucr = (inv_lo(min(g.kc0 + 4 * lane, p.W - 1), p.W, L, 0, p.W) - g.qc0) & ~1;
         // interior quarters (all union columns of class NS, UCWF wide) take the immediate-offset path
@@ -400,6 +423,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(&full[s]);
       }
       if (lane == 0) ktrace(p, it, 15);
+      int nt = 0;
+      if (lane == 0) nt = (int)gridDim.x + atomicAdd(p.tile_counter, 1);
+      t = __shfl_sync(0xffffffffu, nt, 0);
     }
   } else if (warp == kMmaWarp) {
     // ================= S^T / dP^T issuer: chunk c into TMEM chunk slot c & 1, once the dV/dK MMAs
@@ -408,11 +434,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr uint32_t idesc_s = idesc_bf16(64, kNCH, false);
     constexpr uint32_t idesc_s2 = idesc_bf16(64, 2 * QP, false);  // a chunk of one row pair
     int c = 0;
-    for (int it = 0; it < t_end - t_begin; ++it) {
+    for (int it = 0;; ++it) {
       const int stage = it % kStages;
       mbar_wait(&full[stage], (it / kStages) & 1);
       if (lane == 0) ktrace(p, c, 3);
       const TileInfo &ti = tinfo[stage];
+      if (ti.bh < 0) break;
       const int nch = ti.nchunks, row0a = ti.qs_lo[0] - ti.qr0, row0b = ti.qs_lo[1] - ti.qr0;
       const int qn0 = ti.qs_n[0], qn1 = ti.qs_n[1];
       const uint64_t dqs = sdesc_sw64(smem_u32(smem + stage * C::STAGE_BYTES));
@@ -446,11 +473,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     // buffer (tile & 1), so a tile's MMAs never wait for the previous tile's epilogue
     constexpr uint32_t idesc_o = idesc_bf16(64, kD, true);
     int c = 0;
-    for (int it = 0; it < t_end - t_begin; ++it) {
+    for (int it = 0;; ++it) {
       const int stage = it % kStages, b = it & 1;
       // the stage cannot advance past this tile before this warp commits its empty[] below
       mbar_wait(&full[stage], (it / kStages) & 1);
       const TileInfo &ti = tinfo[stage];
+      if (ti.bh < 0) break;
       const int nch = ti.nchunks, row0a = ti.qs_lo[0] - ti.qr0, row0b = ti.qs_lo[1] - ti.qr0;
       const int qn0 = ti.qs_n[0], qn1 = ti.qs_n[1];
       const uint64_t dqs = sdesc_sw64(smem_u32(smem + stage * C::STAGE_BYTES));
@@ -545,11 +573,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     int cur_head = -1;
     int c = 0;
     int pend_it = -1, pend_bh = 0, pend_kr0 = 0, pend_kc0 = 0;  // deferred epilogue
-    for (int t = t_begin; t < t_end; ++t) {
-      const int it = t - t_begin, stage = it % kStages;
+    for (int it = 0;; ++it) {
+      const int stage = it % kStages;
       mbar_wait(&full[stage], (it / kStages) & 1);  // tile description, LSE / D staged
       if (trq) ktrace(p, c, 16 + 4 * grp);
       const TileInfo &ti = tinfo[stage];
+      if (ti.bh < 0) break;  // end of work
       const int h = ti.head, bh = ti.bh, kr0 = ti.kr0, kc0 = ti.kc0, qr0 = ti.qr0, qc0 = ti.qc0;
       const int nch = ti.nchunks, qs_lo = ti.qs_lo[half], qs_n = ti.qs_n[half];
       const int qn0 = ti.qs_n[0], qn1 = ti.qs_n[1];
@@ -619,13 +648,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == kProducerWarp) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
+#ifdef NA2D_TRACE
+    if (lane == 0 && p.trace) {
+      uint64_t gt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+      p.trace[17408 + 2 * blockIdx.x + 1] = (long long)gt;
+    }
+#endif
   }
 }
 
 template <int L, int QP>
 cudaError_t launch_dkdv_t(const Geo &g, const void *q, const void *k, const void *v, const float *rpb,
                           const float *lse, const void *dout, const float *D, void *dk, void *dv,
-                          const float *drpb_part, int part_ctas, float *drpb, cudaStream_t st) {
+                          const float *drpb_part, int part_ctas, float *drpb, int *tile_counter,
+                          cudaStream_t st) {
   using C = CfgK<L, QP>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
@@ -666,6 +703,7 @@ cudaError_t launch_dkdv_t(const Geo &g, const void *q, const void *k, const void
   p.rpb = rpb;
   p.lse = lse;
   p.D = D;
+  p.tile_counter = tile_counter;
   p.drpb_part = drpb_part;
   p.part_ctas = part_ctas;
   p.drpb = drpb;
@@ -713,14 +751,15 @@ bool tc_dkdv_supported(const Geo &g) {
 
 cudaError_t tc_backward_dkdv(const Geo &g, const void *q, const void *k, const void *v, const float *rpb,
                              const float *lse, const void *dout, const float *D, void *dk, void *dv,
-                             const float *drpb_part, int part_ctas, float *drpb, cudaStream_t st) {
+                             const float *drpb_part, int part_ctas, float *drpb, int *tile_counter,
+                             cudaStream_t st) {
   // the query halo of a 16-column key tile is at most 16 + 2NS + 1 <= 23 columns away from the right
   // clamp zone; tiles reaching it are shifted (key_col0)
   if (!tc_dkdv_supported(g)) return cudaErrorNotSupported;
   switch (g.L) {
-    case 3: return launch_dkdv_t<3, 24>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, st);
-    case 5: return launch_dkdv_t<5, 24>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, st);
-    case 7: return launch_dkdv_t<7, 24>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, st);
+    case 3: return launch_dkdv_t<3, 24>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, tile_counter, st);
+    case 5: return launch_dkdv_t<5, 24>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, tile_counter, st);
+    case 7: return launch_dkdv_t<7, 24>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, tile_counter, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -153,10 +153,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&tm_dq);
   }
   for (int c = threadIdx.x; c < 8 * kGroups * C::TT * C::TT; c += kThreads) s_db[c] = 0.f;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && p.b2_tile_counter) *p.b2_tile_counter = 0;  // for B2 (next)
   if (p.drpb_part)  // this CTA's partial tables (only this CTA writes them; B2 reads them after B1)
     for (int c = threadIdx.x; c < p.heads * C::TT * C::TT; c += kThreads)
       p.drpb_part[(size_t)blockIdx.x * p.heads * C::TT * C::TT + c] = 0.f;
   if (warp == kProducerWarp) tmem_alloc<512>(tmem_slot);
+#ifdef NA2D_TRACE
+  if (threadIdx.x == 0 && p.trace) {  // per-CTA wall-clock span (load balance)
+    uint64_t gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    p.trace[16896 + 2 * blockIdx.x] = (long long)gt;
+  }
+#endif
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -524,13 +532,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == kProducerWarp) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
+#ifdef NA2D_TRACE
+    if (lane == 0 && p.trace) {
+      uint64_t gt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+      p.trace[16896 + 2 * blockIdx.x + 1] = (long long)gt;
+    }
+#endif
   }
 }
 
 template <int L>
 cudaError_t launch_dq(const Geo &g, const void *q, const void *k, const void *v, const float *rpb, const void *out,
                       const float *lse, const void *dout, void *dq, float *drpb, float *D, float *part,
-                      cudaStream_t st) {
+                      int *b2_tile_counter, cudaStream_t st) {
   using C = CfgQ<L>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
@@ -563,6 +578,7 @@ cudaError_t launch_dq(const Geo &g, const void *q, const void *k, const void *v,
   p.dq = (__nv_bfloat16 *)dq;
   p.D = D;
   p.drpb_part = rpb ? part : nullptr;
+  p.b2_tile_counter = b2_tile_counter;
   p.trace = (long long *)debug_trace_buffer();
   const int grid = dq_grid(g);
   (void)drpb;  // summed from the partial tables by B2
@@ -583,11 +599,11 @@ int dq_grid(const Geo &g) {
 
 cudaError_t tc_backward_dq(const Geo &g, const void *q, const void *k, const void *v, const float *rpb,
                            const void *out, const float *lse, const void *dout, void *dq, float *drpb, float *D,
-                           float *part, cudaStream_t st) {
+                           float *part, int *b2_tile_counter, cudaStream_t st) {
   switch (g.L) {
-    case 3: return launch_dq<3>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D, part, st);
-    case 5: return launch_dq<5>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D, part, st);
-    case 7: return launch_dq<7>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D, part, st);
+    case 3: return launch_dq<3>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D, part, b2_tile_counter, st);
+    case 5: return launch_dq<5>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D, part, b2_tile_counter, st);
+    case 7: return launch_dq<7>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D, part, b2_tile_counter, st);
   }
   return cudaErrorInvalidValue;
 }

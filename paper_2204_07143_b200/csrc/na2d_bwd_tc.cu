@@ -52,16 +52,18 @@ bool tc_backward_supported(const Geo &g) {
 
 size_t tc_backward_scratch_bytes(const Geo &g) {
   const int TT = 2 * g.L - 1;
-  return sizeof(float) * (size_t)dq_grid(g) * g.heads * TT * TT;
+  return sizeof(float) * (size_t)dq_grid(g) * g.heads * TT * TT + 16;  // + B2 tile counter
 }
 
 cudaError_t tc_backward(const Geo &g, const void *q, const void *k, const void *v, const float *rpb,
                         const void *out, const float *lse, const void *dout, void *dq, void *dk, void *dv,
                         float *drpb, float *D, void *scratch, cudaStream_t st) {
-  cudaError_t e = tc_backward_dq(g, q, k, v, rpb, out, lse, dout, dq, drpb, D, (float *)scratch, st);
+  const int TT = 2 * g.L - 1;
+  int *counter = (int *)((char *)scratch + sizeof(float) * (size_t)dq_grid(g) * g.heads * TT * TT);
+  cudaError_t e = tc_backward_dq(g, q, k, v, rpb, out, lse, dout, dq, drpb, D, (float *)scratch, counter, st);
   if (e != cudaSuccess) return e;
   return tc_backward_dkdv(g, q, k, v, rpb, lse, dout, D, dk, dv, rpb ? (const float *)scratch : nullptr,
-                          dq_grid(g), drpb, st);
+                          dq_grid(g), drpb, counter, st);
 }
 
 int tc_launches(const Geo &g, int which) {

@@ -158,6 +158,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&tm_v);
   }
   if (warp == kProducerWarp) tmem_alloc<512>(tmem_slot);
+#ifdef NA2D_TRACE
+  if (threadIdx.x == 0 && p.trace) {  // per-CTA wall-clock span (load balance)
+    uint64_t gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    p.trace[16384 + 2 * blockIdx.x] = (long long)gt;
+  }
+#endif
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -518,6 +525,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == kProducerWarp) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
+#ifdef NA2D_TRACE
+    if (lane == 0 && p.trace) {
+      uint64_t gt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+      p.trace[16384 + 2 * blockIdx.x + 1] = (long long)gt;
+    }
+#endif
   }
 }
 

@@ -56,6 +56,7 @@ struct BwdQParams {
   __nv_bfloat16 *dq;
   float *D;          // [B*heads*q_rows*W] written
   float *drpb_part;  // [grid][heads][TT*TT] partial tables (null if no rpb)
+  int *b2_tile_counter;  // zeroed by this kernel for B2's dynamic tile scheduler
   long long *trace;  // debug timeline (na2d_debug_set_trace) or null
 };
 
@@ -66,9 +67,10 @@ bool tc_dkdv_supported(const Geo &g);
 // into drpb (fixed CTA order, one warp per cell) before its own work
 cudaError_t tc_backward_dkdv(const Geo &g, const void *q, const void *k, const void *v, const float *rpb,
                              const float *lse, const void *dout, const float *D, void *dk, void *dv,
-                             const float *drpb_part, int part_ctas, float *drpb, cudaStream_t st);
+                             const float *drpb_part, int part_ctas, float *drpb, int *tile_counter,
+                             cudaStream_t st);
 cudaError_t tc_backward_dq(const Geo &g, const void *q, const void *k, const void *v, const float *rpb,
                            const void *out, const float *lse, const void *dout, void *dq, float *drpb, float *D,
-                           float *part, cudaStream_t st);
+                           float *part, int *b2_tile_counter, cudaStream_t st);
 
 }  // namespace na2d
