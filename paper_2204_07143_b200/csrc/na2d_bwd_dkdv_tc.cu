@@ -258,18 +258,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int q_end = p.q_row0 + p.q_rows;
 
-  // a10 final: dRPB = sum of B1's per-CTA partial tables, one warp per cell, lane l summing CTAs
-  // l, l + 32, ... in order, then a fixed butterfly (deterministic for a given B1 grid)
-  if (p.drpb_part) {
-    const int n = p.heads * (2 * L - 1) * (2 * L - 1);
-    for (int e = blockIdx.x * (kThreads / 32) + warp; e < n; e += gridDim.x * (kThreads / 32)) {
-      float acc = 0.f;
-      for (int b = lane; b < p.part_ctas; b += 32) acc += __ldg(&p.drpb_part[(size_t)b * n + e]);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) p.drpb[e] = acc;
-    }
-  }
   // zero the never-loaded tail rows of the Q / dO halos (read by partial chunks)
   for (int s = 0; s < kStages; ++s)
     for (int q2 = 0; q2 < 2; ++q2) {
@@ -319,6 +307,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();  // B1 is complete (D, partial tables, zeroed tile counter): global memory from here on
+  // a10 final: dRPB = sum of B1's per-CTA partial tables, one warp per cell, lane l summing CTAs
+  // l, l + 32, ... in order, then a fixed butterfly (deterministic for a given B1 grid)
+  if (p.drpb_part) {
+    const int n = p.heads * (2 * L - 1) * (2 * L - 1);
+    for (int e = blockIdx.x * (kThreads / 32) + warp; e < n; e += gridDim.x * (kThreads / 32)) {
+      float acc = 0.f;
+      for (int b = lane; b < p.part_ctas; b += 32) acc += __ldg(&p.drpb_part[(size_t)b * n + e]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) p.drpb[e] = acc;
+    }
+  }
   const float log2e = 1.4426950408889634f;
 
   if (warp == kProducerWarp) {
@@ -712,8 +714,8 @@ cudaError_t launch_dkdv_t(const Geo &g, const void *q, const void *k, const void
   p.trace = (long long *)debug_trace_buffer();
   const int grid = p.num_tiles < tc::num_sms() ? p.num_tiles : tc::num_sms();
   ProfScope ps("na2d_bwd_dkdv_tc", st);
-  na2d_bwd_dkdv_kernel<L, QP><<<grid, kThreads, C::SMEM, st>>>(tq, tdo, tk, tv, tl, td, tdk, tdv, p);
-  return cudaGetLastError();
+  const cudaError_t e = launch_pdl(na2d_bwd_dkdv_kernel<L, QP>, grid, kThreads, C::SMEM, st, tq, tdo, tk, tv, tl, td, tdk, tdv, p);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace

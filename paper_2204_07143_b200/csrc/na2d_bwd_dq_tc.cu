@@ -153,10 +153,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&tm_dq);
   }
   for (int c = threadIdx.x; c < 8 * kGroups * C::TT * C::TT; c += kThreads) s_db[c] = 0.f;
-  if (blockIdx.x == 0 && threadIdx.x == 0 && p.b2_tile_counter) *p.b2_tile_counter = 0;  // for B2 (next)
-  if (p.drpb_part)  // this CTA's partial tables (only this CTA writes them; B2 reads them after B1)
-    for (int c = threadIdx.x; c < p.heads * C::TT * C::TT; c += kThreads)
-      p.drpb_part[(size_t)blockIdx.x * p.heads * C::TT * C::TT + c] = 0.f;
   if (warp == kProducerWarp) tmem_alloc<512>(tmem_slot);
 #ifdef NA2D_TRACE
   if (threadIdx.x == 0 && p.trace) {  // per-CTA wall-clock span (load balance)
@@ -169,6 +165,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();  // the previous kernel (forward / last step's B2) is complete: global memory from here on
+  if (blockIdx.x == 0 && threadIdx.x == 0 && p.b2_tile_counter) *p.b2_tile_counter = 0;  // for B2 (next)
+  if (p.drpb_part) {  // this CTA's partial tables (only this CTA writes them; B2 reads them after B1)
+    for (int c = threadIdx.x; c < p.heads * C::TT * C::TT; c += kThreads)
+      p.drpb_part[(size_t)blockIdx.x * p.heads * C::TT * C::TT + c] = 0.f;
+    __syncthreads();
+  }
 
   if (warp == kProducerWarp) {
     // ================= producer: TMA (Q, dO 4x4 blocks; K, V halo) + the tile's LSE (log2 units)
@@ -584,7 +588,8 @@ cudaError_t launch_dq(const Geo &g, const void *q, const void *k, const void *v,
   (void)drpb;  // summed from the partial tables by B2
   {
     ProfScope ps("na2d_bwd_dq_tc", st);
-    na2d_bwd_dq_kernel<L><<<grid, kThreads, C::SMEM, st>>>(tq, tdo, tk, tv, tdq, p);
+    const cudaError_t e = launch_pdl(na2d_bwd_dq_kernel<L>, grid, kThreads, C::SMEM, st, tq, tdo, tk, tv, tdq, p);
+    if (e != cudaSuccess) return e;
   }
   // the per-CTA dRPB partial tables are summed by the dK/dV kernel (B2), which runs next
   return cudaGetLastError();

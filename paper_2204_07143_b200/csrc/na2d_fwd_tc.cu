@@ -169,6 +169,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();  // the previous kernel on the stream is complete: global memory from here on
 
   if (warp == kProducerWarp) {
     // ================= producer (whole warp converged; one elected thread writes the tile
@@ -569,8 +571,8 @@ cudaError_t launch_fwd(const Geo &g, const void *q, const void *k, const void *v
   p.trace = (long long *)debug_trace_buffer();
   const int grid = p.num_tiles < num_sms() ? p.num_tiles : num_sms();
   ProfScope ps("na2d_fwd_tc", st);
-  na2d_fwd_tc_kernel<L><<<grid, kThreads, C::SMEM, st>>>(tq, tk, tv, p);
-  return cudaGetLastError();
+  const cudaError_t e = launch_pdl(na2d_fwd_tc_kernel<L>, grid, kThreads, C::SMEM, st, tq, tk, tv, p);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace

@@ -54,6 +54,15 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity, 
   }
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// The kernels are launched with programmatic stream serialization: a kernel triggers its dependents
+// as soon as it starts (all its CTAs are resident: grids <= one CTA per SM), so the next kernel's
+// CTAs take SMs as they free up and run their prologue (barriers, TMEM, descriptor prefetch) during
+// this kernel's tail; pdl_wait() then blocks until the previous grid has completed and its memory
+// is visible.  No global memory may be touched before pdl_wait().
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ---------------------------------------------------------------- fences / barriers
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
