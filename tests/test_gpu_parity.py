@@ -157,3 +157,36 @@ def test_step_host_matches_device_path():
         np.testing.assert_array_equal(outs[n].float().numpy(), ref[n])
     np.testing.assert_allclose(lse.numpy(), ref["lse"], atol=1e-6)
     np.testing.assert_allclose(drpb.numpy(), ref["drpb"], atol=1e-3, rtol=1e-4)
+
+
+@pytest.mark.parametrize("shape,dtype", [
+    (Shape("nan7", 2, 2, 19, 37, 32, 7), "bf16"),   # ragged tiles, B2 shifted key columns (W = 5 mod 16)
+    (Shape("nan5", 1, 2, 13, 21, 32, 5), "bf16"),
+    (Shape("nan3", 1, 1, 9, 18, 32, 3), "bf16"),
+    (Shape("nanf", 1, 2, 11, 14, 32, 7), "f32"),
+], ids=lambda x: x.name if isinstance(x, Shape) else x)
+def test_every_output_element_written(shape, dtype):
+    """Outputs pre-filled with NaN come back fully overwritten (out, lse, dq, dk, dv, drpb) and
+    equal to the oracle.  compute-sanitizer's initcheck does not see the TMA (bulk async) stores
+    of the tensor-core kernels, so this is the direct check that every element is written."""
+    import torch
+    import oracle
+    import paper_2204_07143_b200 as na2d
+    from tests.parity import compare
+    inp = make_inputs(shape, seed=9, dtype=dtype)
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    t = {n: torch.from_numpy(inp[n]).cuda().to(tdt) for n in ("q", "k", "v", "dout")}
+    rpb = torch.from_numpy(inp["rpb"]).cuda()
+    nan = lambda like, dt=None: torch.full_like(like, float("nan"), dtype=dt or like.dtype)  # noqa: E731
+    out, lse = nan(t["q"]), torch.full(t["q"].shape[:4], float("nan"), device="cuda")
+    na2d.forward(t["q"], t["k"], t["v"], rpb, shape.kernel_size, out=out, lse=lse)
+    grads = (nan(t["q"]), nan(t["k"]), nan(t["v"]), nan(rpb))
+    na2d.backward(t["q"], t["k"], t["v"], rpb, out, lse, t["dout"], shape.kernel_size, grads=grads)
+    torch.cuda.synchronize()
+    got = dict(out=out, lse=lse, dq=grads[0], dk=grads[1], dv=grads[2], drpb=grads[3])
+    for n, x in got.items():
+        assert not torch.isnan(x).any(), f"{n}: {int(torch.isnan(x).sum())} elements never written"
+    ref = oracle.na2d_backward(inp["q"], inp["k"], inp["v"], inp["rpb"], inp["dout"], shape.kernel_size,
+                               shape.d ** -0.5)
+    compare({n: x.float().cpu().numpy() for n, x in got.items()}, ref, dtype,
+            names=["out", "lse", "dq", "dk", "dv", "drpb"])
