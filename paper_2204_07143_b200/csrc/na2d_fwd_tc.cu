@@ -53,7 +53,12 @@ constexpr int kThreads = 640;     // 20 warps
 // MMA-issue warps take the two highest ids so the busy elementwise warps sharing their
 // sub-partitions (warp % 4) never delay a TMA or MMA issue.
 constexpr int kProducerWarp = 16, kMmaWarp = 17, kProducerVWarp = 18, kPvWarp = 19;
-constexpr int kOAcc = 3;           // independent PV accumulators (summed in the epilogue)
+// O accumulators outside both S slots, shared by the two slots' tiles: the next QK of a slot waits
+// only for that slot's PV MMAs (not for its epilogue), and PV of tile t waits for the epilogue
+// of tile t - 1 (which precedes it by half a slot cycle)
+#ifndef NA2D_FWD_SHARED_O
+#define NA2D_FWD_SHARED_O 1
+#endif
 
 template <int L>
 struct Cfg {
@@ -62,8 +67,17 @@ struct Cfg {
   static constexpr int PAIRS = UR / 2;         // union row pairs (3 PV K-steps each)
   static constexpr int NSUB = UR * kHCP;       // S columns per sub-tile (keys)
   static constexpr int P_COL = 0;              // P (bf16 pairs) aliased over consumed S
-  static constexpr int O_COL = NSUB / 2;       // O partial accumulators past the compacted x / P
-  static_assert(O_COL + kOAcc * kD <= 256, "slot budget");
+#if NA2D_FWD_SHARED_O
+  static constexpr int SLOT = NSUB;            // TMEM columns per slot: S (then x / P)
+  static constexpr int O_COL = 2 * NSUB;       // O partial accumulators (absolute column)
+  static constexpr int OACC = (512 - O_COL) / kD < 3 ? (512 - O_COL) / kD : 3;  // independent PV chains
+  static_assert(OACC >= 1, "TMEM budget");
+#else
+  static constexpr int SLOT = 256;
+  static constexpr int O_COL = NSUB / 2;       // O partial accumulators past the compacted x / P (in the slot)
+  static constexpr int OACC = 3;
+  static_assert(O_COL + OACC * kD <= 256, "slot budget");
+#endif
   static_assert(2 * kHCP == 3 * 16, "a union row pair is 3 PV K-steps");
   static constexpr int KV_ROWS = HR * kHCP;
   static constexpr int Q_BYTES = 128 * kRowBytes;
@@ -129,7 +143,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   // tile description it % kTInfo written (the elementwise warps must not wait on full[]: by the time
   // a slow group gets there, full[] may already have completed the next phase of its stage)
   uint64_t *ti_full = p_pair + 2 * C::PAIRS;
-  uint32_t *tmem_slot = (uint32_t *)(ti_full + kTInfo);
+  uint64_t *o_free = ti_full + kTInfo;  // shared O read out by the epilogue of the previous tile
+  uint32_t *tmem_slot = (uint32_t *)(o_free + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int t_begin = (int)((long)p.num_tiles * blockIdx.x / gridDim.x);
@@ -149,9 +164,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&s_full[s], 1);
       mbar_init(&o_full[s], 1);
-      mbar_init(&tmem_free[s], 8);  // both lane-half groups of the slot
+      mbar_init(&tmem_free[s], NA2D_FWD_SHARED_O ? 1 : 8);  // PV commit / both lane-half groups' epilogue
       for (int k = 0; k < C::PAIRS; ++k) mbar_init(&p_pair[s * C::PAIRS + k], 8);
     }
+    mbar_init(o_free, 8);
     fence_barrier_init();
     tma_prefetch(&tm_q);
     tma_prefetch(&tm_k);
@@ -272,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t dq = sdesc_sw64(smem_u32(smem + s * C::QK_BYTES));
       const uint64_t dk = dq + (C::Q_BYTES >> 4);
       const uint64_t dk0 = dk + ((rb0 * kHCP * kRowBytes) >> 4), dk1 = dk + ((rb1 * kHCP * kRowBytes) >> 4);
-      const uint32_t d0 = tmem + slot * 256, d1 = d0 + ((uint32_t)16 << 16);
+      const uint32_t d0 = tmem + slot * C::SLOT, d1 = d0 + ((uint32_t)16 << 16);
       if (elect_one()) {  // two independent accumulation chains (sub-tiles) interleaved
         mma_ss(d0, dq, dk0, idesc_qk, 0);
         mma_ss(d1, dq + (4096 >> 4), dk1, idesc_qk, 0);
@@ -293,11 +309,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int rb0 = vinfo[2 * s], rb1 = vinfo[2 * s + 1];
       const uint64_t dv = sdesc_sw64(smem_u32(smem + C::V_OFF + s * C::KV_BYTES));
       const uint64_t dv0 = dv + ((rb0 * kHCP * kRowBytes) >> 4), dv1 = dv + ((rb1 * kHCP * kRowBytes) >> 4);
-      const uint32_t b0 = tmem + slot * 256, b1 = b0 + ((uint32_t)16 << 16);
+      const uint32_t b0 = tmem + slot * C::SLOT, b1 = b0 + ((uint32_t)16 << 16);
+#if NA2D_FWD_SHARED_O
+      const uint32_t o0 = tmem + C::O_COL, o1 = o0 + ((uint32_t)16 << 16);
+#else
+      const uint32_t o0 = b0 + C::O_COL, o1 = b1 + C::O_COL;
+#endif
       // fully unrolled: every descriptor / TMEM address below is the tile's base + an immediate, so
       // each pair's issue is a short independent burst (no dependent address chain per pair)
 #pragma unroll
       for (int k = 0; k < C::PAIRS; ++k) {
+#if NA2D_FWD_SHARED_O
+        if (k == 0 && it > 0) mbar_wait(o_free, (it - 1) & 1);  // epilogue of tile it - 1 read O
+#endif
         mbar_wait(&p_pair[slot * C::PAIRS + k], (it >> 1) & 1);
         if (lane == 0) trace_ev(p, it, 19 + k);
         tc_fence_after();
@@ -307,13 +331,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int k3 = 0; k3 < 3; ++k3) {
             const int ks = 3 * k + k3;
-            const uint32_t voff = (ks * 16 * kRowBytes) >> 4;
-            mma_ts(b0 + C::O_COL + k3 * kD, b0 + C::P_COL + ks * 8, dv0 + voff, idesc_pv, k > 0 ? acc : 0u);
-            mma_ts(b1 + C::O_COL + k3 * kD, b1 + C::P_COL + ks * 8, dv1 + voff, idesc_pv, k > 0 ? acc : 0u);
+            const uint32_t voff = (ks * 16 * kRowBytes) >> 4, oc = (ks % C::OACC) * kD;
+            const uint32_t a = ks >= C::OACC ? acc : 0u;
+            mma_ts(o0 + oc, b0 + C::P_COL + ks * 8, dv0 + voff, idesc_pv, a);
+            mma_ts(o1 + oc, b1 + C::P_COL + ks * 8, dv1 + voff, idesc_pv, a);
           }
           if (k == C::PAIRS - 1) {
             mma_commit(&o_full[slot]);
             mma_commit(&empty_v[s]);
+#if NA2D_FWD_SHARED_O
+            mma_commit(&tmem_free[slot]);  // P read: the slot may take the next QK
+#endif
           }
         }
         __syncwarp();
@@ -332,7 +360,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int stid = threadIdx.x - slot * 256;       // 0..255 within the slot's two groups
     const int Lh = wlen(p.H, L), Lw = wlen(p.W, L);
     const float2 sl2x2 = make_float2(p.scale_log2, p.scale_log2);
-    const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32 + 16 * hh) << 16) + slot * 256;
+    const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32 + 16 * hh) << 16) + slot * C::SLOT;
+#if NA2D_FWD_SHARED_O
+    const uint32_t o_addr = tmem + ((uint32_t)(quarter * 32 + 16 * hh) << 16) + C::O_COL;
+#else
+    const uint32_t o_addr = lane_addr + C::O_COL;
+#endif
     int cur_head = -1;
     for (int it = slot; it < t_end - t_begin; it += 2) {
       const uint32_t ph = (it >> 1) & 1;
@@ -495,21 +528,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       float o[16];
       {
-        uint32_t oa[kOAcc][16];
+        uint32_t oa[C::OACC][16];
 #pragma unroll
-        for (int a = 0; a < kOAcc; ++a) tmem_ld_h16<16>(lane_addr + C::O_COL + a * kD, oa[a]);
+        for (int a = 0; a < C::OACC; ++a) tmem_ld_h16<16>(o_addr + a * kD, oa[a]);
         tc_wait_ld();
 #pragma unroll
         for (int z = 0; z < 16; ++z) {
           float acc = __uint_as_float(oa[0][z]);
 #pragma unroll
-          for (int a = 1; a < kOAcc; ++a) acc += __uint_as_float(oa[a][z]);
+          for (int a = 1; a < C::OACC; ++a) acc += __uint_as_float(oa[a][z]);
           o[z] = acc;
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tmem_free[slot]);
+      if (lane == 0) mbar_arrive(NA2D_FWD_SHARED_O ? o_free : &tmem_free[slot]);
       if (i < q_end && j < p.W) {
         const float inv = 1.f / sum;
         const size_t qi = ((size_t)bh * p.q_rows + (i - p.q_row0)) * p.W + j;
