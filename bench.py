@@ -394,7 +394,7 @@ def main():
         TT = (2 * L - 1) ** 2 * shape.heads * 4
         e2e = {"value": (f_fwd + f_bwd) * world / (ems * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ems,
                "h2d_bytes_per_step": 4 * tb + TT, "d2h_bytes_per_step": 4 * tb + hlse.numel() * 4 + TT,
-               "path": "na2d_step_host (pinned host buffers; H2D + fwd + bwd + D2H pipelined over 8 batch chunks on three library streams)"}
+               "path": "na2d_step_host (pinned host buffers; H2D + fwd + bwd + D2H pipelined over up to 16 batch chunks on three library streams)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_extras:

@@ -111,7 +111,7 @@ na2d_status na2d_backward(const na2d_problem *p, const void *q, const void *k, c
                           size_t workspace_bytes, void *stream);
 
 /* End-to-end step through HOST buffers: copies q,k,v,dout,rpb host->device, runs forward and
- * backward, copies out,lse,dq,dk,dv,drpb device->host.  The work is pipelined over up to 8 batch
+ * backward, copies out,lse,dq,dk,dv,drpb device->host.  The work is pipelined over up to 16 batch
  * chunks on three non-blocking streams owned by the library (created once per host thread and
  * device): chunk c+1's host->device copies and chunk c-1's device->host copies overlap chunk c's
  * kernels.  It starts after the work already enqueued on `stream`, and `stream` waits for its

@@ -190,7 +190,10 @@ na2d_status na2d_paper_backward(const na2d_problem *p, const void *q, const void
 namespace na2d {
 namespace {
 
-constexpr int kHostChunks = 8;  // batch chunks of the pipelined host step
+#ifndef NA2D_HOST_CHUNKS
+#define NA2D_HOST_CHUNKS 16
+#endif
+constexpr int kHostChunks = NA2D_HOST_CHUNKS;  // batch chunks of the pipelined host step
 
 // Per (host thread, device): the three non-blocking streams of the pipelined host step and its
 // events, created on first use and kept (no per-call allocation).
