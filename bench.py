@@ -235,10 +235,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test knob: run N ranks on fewer GPUs (ranks share a device, gloo instead of NCCL) to exercise
+    # the N > 1 code path on a one-GPU box; never used for reported numbers
+    share = os.environ.get("NA2D_BENCH_SHARE_GPU") == "1"
+    if share:
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     na2d.load_library()
 
     # ---- inputs: this rank's batch shard of the global synthetic batch, resident in HBM
@@ -268,7 +276,7 @@ def main():
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            dist.barrier() if share else dist.barrier(device_ids=[local])
         torch.cuda.synchronize()
 
     for i in range(args.warmup):
