@@ -222,6 +222,8 @@ def main():
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="na2d", choices=["na2d", "reference"])
     ap.add_argument("--no-extras", action="store_true", help="skip cpu baseline / e2e / clocks (profiling runs)")
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "f16"],
+                    help="16-bit I/O type of the tensor-core path (BASELINE's metric is bf16)")
     args = ap.parse_args()
     shape = CONFIGS[args.config]
     if args.impl == "reference":
@@ -251,9 +253,10 @@ def main():
 
     # ---- inputs: this rank's batch shard of the global synthetic batch, resident in HBM
     g = shape.replace(B=shape.B * world)
-    inp = make_inputs(g, dtype="bf16", rpb="swin", batch_offset=rank * shape.B, batch_count=shape.B)
+    inp = make_inputs(g, dtype=args.dtype, rpb="swin", batch_offset=rank * shape.B, batch_count=shape.B)
+    el = torch.float16 if args.dtype == "f16" else torch.bfloat16
     sets = []
-    t = {n: torch.from_numpy(inp[n]).to(dev).to(torch.bfloat16) for n in ("q", "k", "v", "dout")}
+    t = {n: torch.from_numpy(inp[n]).to(dev).to(el) for n in ("q", "k", "v", "dout")}
     sets.append(t)
     sets.append({n: x.flip(0).contiguous() for n, x in t.items()})
     rpb = torch.from_numpy(inp["rpb"]).to(dev)
@@ -336,7 +339,7 @@ def main():
     # ---- context: the paper's own decomposition (QK+RPB kernel writing the attention
     # weights, softmax, AV, and their gradients) on the same inputs, same device
     paper = None
-    if not args.no_extras:
+    if not args.no_extras and args.dtype == "bf16":  # the comparison path has no fp16 I/O
         s0 = sets[0]
         _, _, attn = na2d.paper_forward(s0["q"], s0["k"], s0["v"], rpb, L, scale)
         dsb = torch.empty_like(attn)
@@ -411,7 +414,7 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": config_dict(shape, world),
+                "vs_baseline": None, "dtype": args.dtype, "data": "synthetic", "config": config_dict(shape, world),
                 "impl": "na2d", "gpu_launches": launches_per_step * args.steps,
                 "kernel_families": [na2d.na2d_kernel_family(p, 0), na2d.na2d_kernel_family(p, 1)],
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "paper_design": paper,

@@ -44,6 +44,9 @@
  *
  * Precision: NA2D_BF16 = bf16 in/out, fp32 accumulation (tcgen05 tensor cores), fp32 LSE and
  * dRPB.  NA2D_F32 = fp32 in/out, fp32 SIMT FMA (no TF32), for 1e-4 relative parity.
+ * NA2D_F16 = fp16 in/out (mixed-precision training I/O), same kernels as bf16 with fp16 MMA
+ * operands (P and dS rounded to fp16); tensor-core shapes only (dim = 32, kernel_size 3/5/7),
+ * other shapes and the paper-decomposition calls return NA2D_ERR_UNSUPPORTED.
  */
 #ifndef NA2D_H_
 #define NA2D_H_
@@ -70,7 +73,7 @@ typedef enum {
   NA2D_ERR_CUDA = 9           /* a CUDA runtime call or kernel launch failed */
 } na2d_status;
 
-typedef enum { NA2D_BF16 = 0, NA2D_F32 = 1 } na2d_dtype;
+typedef enum { NA2D_BF16 = 0, NA2D_F32 = 1, NA2D_F16 = 2 } na2d_dtype;
 
 typedef struct {
   int32_t batch;        /* B */

@@ -110,6 +110,9 @@ def make_inputs(shape: Shape, seed: int | None = None, dtype: str = "bf16", rpb:
     if dtype == "bf16":
         for n in ("q", "k", "v", "dout"):
             out[n] = bf16_round(out[n])
+    elif dtype == "f16":  # fp16-representable (IEEE round to nearest even)
+        for n in ("q", "k", "v", "dout"):
+            out[n] = out[n].astype(np.float16).astype(np.float32)
     elif dtype != "f32":
         raise ValueError(dtype)
     return out

@@ -20,7 +20,7 @@ import os
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libna2d.so")
 
-NA2D_BF16, NA2D_F32 = 0, 1
+NA2D_BF16, NA2D_F32, NA2D_F16 = 0, 1, 2
 _STATUS = ["ok", "null pointer", "kernel size", "shape", "dtype", "unsupported", "alignment", "workspace",
            "invalid argument", "cuda"]
 
@@ -173,7 +173,9 @@ def _dtype_code(t):
         return NA2D_BF16
     if t.dtype == torch.float32:
         return NA2D_F32
-    raise TypeError(f"unsupported dtype {t.dtype} (bf16 or fp32)")
+    if t.dtype == torch.float16:
+        return NA2D_F16
+    raise TypeError(f"unsupported dtype {t.dtype} (bf16, fp16 or fp32)")
 
 
 def _dev(t, name):

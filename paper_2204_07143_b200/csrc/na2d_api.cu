@@ -17,7 +17,7 @@ bool aligned16(const void *p) { return p == nullptr || ((uintptr_t)p & 15u) == 0
 // Synchronous validation; fills g on success.
 na2d_status make_geo(const na2d_problem *p, Geo *g) {
   if (!p) return NA2D_ERR_NULL_POINTER;
-  if (p->dtype != NA2D_BF16 && p->dtype != NA2D_F32) return NA2D_ERR_DTYPE;
+  if (p->dtype != NA2D_BF16 && p->dtype != NA2D_F32 && p->dtype != NA2D_F16) return NA2D_ERR_DTYPE;
   if (p->kernel_size < 3 || (p->kernel_size % 2) == 0) return NA2D_ERR_KERNEL_SIZE;
   if (p->batch <= 0 || p->heads <= 0 || p->height <= 0 || p->width <= 0 || p->dim <= 0) return NA2D_ERR_SHAPE;
   if (!(isfinite(p->scale) && p->scale > 0.f)) return NA2D_ERR_INVALID_ARG;
@@ -94,7 +94,7 @@ const char *na2d_status_string(na2d_status s) {
     case NA2D_ERR_NULL_POINTER: return "a required pointer is NULL";
     case NA2D_ERR_KERNEL_SIZE: return "kernel_size must be odd and >= 3 (PAPER App. A: odd number greater than 1)";
     case NA2D_ERR_SHAPE: return "invalid shape (dimension <= 0, overflow, or band misses needed K/V rows)";
-    case NA2D_ERR_DTYPE: return "dtype must be NA2D_BF16 or NA2D_F32";
+    case NA2D_ERR_DTYPE: return "dtype must be NA2D_BF16, NA2D_F32 or NA2D_F16";
     case NA2D_ERR_UNSUPPORTED: return "unsupported problem (dim must be even and <= 128, kernel_size <= 31)";
     case NA2D_ERR_ALIGNMENT: return "tensor base pointers must be 16-byte aligned";
     case NA2D_ERR_WORKSPACE: return "workspace smaller than na2d_backward_workspace_bytes()";
@@ -116,6 +116,7 @@ na2d_status na2d_forward(const na2d_problem *p, const void *q, const void *k, co
   if (!q || !k || !v || !out) return NA2D_ERR_NULL_POINTER;
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(out) || !aligned16(lse) || !aligned16(rpb))
     return NA2D_ERR_ALIGNMENT;
+  if (g.dtype == NA2D_F16 && !use_tc(g, 0)) return NA2D_ERR_UNSUPPORTED;  // fp16: tensor-core shapes only
   cudaStream_t st = (cudaStream_t)stream;
   (void)cudaGetLastError();  // a non-sticky error left by an unrelated earlier runtime call is not ours
   if (use_tc(g, 0)) return cuda_status(tc_forward(g, q, k, v, rpb, out, lse, st));
@@ -136,6 +137,7 @@ na2d_status na2d_backward(const na2d_problem *p, const void *q, const void *k, c
   if (s != NA2D_OK) return s;
   if (!q || !k || !v || !out || !lse || !dout || !dq || !dk || !dv) return NA2D_ERR_NULL_POINTER;
   if ((rpb == nullptr) != (drpb == nullptr)) return NA2D_ERR_INVALID_ARG;
+  if (g.dtype == NA2D_F16 && !use_tc(g, 1)) return NA2D_ERR_UNSUPPORTED;  // fp16: tensor-core shapes only
   const size_t need = bwd_ws(g);
   if (workspace_bytes < need) return NA2D_ERR_WORKSPACE;
   if (!workspace) return NA2D_ERR_NULL_POINTER;
@@ -164,6 +166,7 @@ na2d_status na2d_paper_forward(const na2d_problem *p, const void *q, const void 
   na2d_status s = make_geo(p, &g);
   if (s != NA2D_OK) return s;
   if (!q || !k || !v || !out || !lse || !attn) return NA2D_ERR_NULL_POINTER;
+  if (g.dtype == NA2D_F16) return NA2D_ERR_UNSUPPORTED;  // comparison path: bf16 / fp32 only
   const void *ptrs[] = {q, k, v, rpb, out, lse, attn};
   for (const void *ptr : ptrs)
     if (!aligned16(ptr)) return NA2D_ERR_ALIGNMENT;
@@ -178,6 +181,7 @@ na2d_status na2d_paper_backward(const na2d_problem *p, const void *q, const void
   na2d_status s = make_geo(p, &g);
   if (s != NA2D_OK) return s;
   if (!q || !k || !v || !dout || !attn || !dS || !dq || !dk || !dv) return NA2D_ERR_NULL_POINTER;
+  if (g.dtype == NA2D_F16) return NA2D_ERR_UNSUPPORTED;  // comparison path: bf16 / fp32 only
   const void *ptrs[] = {q, k, v, dout, attn, dS, dq, dk, dv, drpb};
   for (const void *ptr : ptrs)
     if (!aligned16(ptr)) return NA2D_ERR_ALIGNMENT;

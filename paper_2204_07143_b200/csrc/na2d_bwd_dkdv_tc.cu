@@ -164,7 +164,7 @@ __device__ __forceinline__ KTile ktile(const BwdKParams &p, int t) {
 //   P = exp2(s*scale*log2e + B'[row][col] - LSE*log2e),  dS = P (dP - D)  -> bf16 pairs over S / dP.
 // FAST: every union column of the quarter is an interior column (column-clamp class NS), so the
 // bias address is trow - z (immediate offsets); otherwise per-column class offsets (colterm).
-template <int L, int QP, bool FAST>
+template <int L, int QP, bool FAST, bool F16>
 __device__ __forceinline__ void chunk_rows(uint32_t lane_addr, int uc, const float *tbl_row0,
                                            const int (&colterm)[CfgK<L, QP>::UCW], const float *lrow0,
                                            int pk, int i_base, int H, int rows_here, int Lh, float sl2,
@@ -213,8 +213,8 @@ __device__ __forceinline__ void chunk_rows(uint32_t lane_addr, int uc, const flo
         const float2 P = make_float2(ex2(ar.x), ex2(ar.y));
         const float2 dp = make_float2(__uint_as_float(dpv[y][z]), __uint_as_float(dpv[y][z + 1]));
         const float2 dS = __fmul2_rn(P, __fadd2_rn(dp, make_float2(-dz.x, -dz.y)));
-        pp[z / 2] = pack_bf16(P.x, P.y);
-        dd[z / 2] = pack_bf16(dS.x, dS.y);
+        pp[z / 2] = pack_el<F16>(P.x, P.y);
+        dd[z / 2] = pack_el<F16>(dS.x, dS.y);
       }
       const uint32_t prow = lane_addr + u * (QP / 2);
       const uint32_t drow = prow + kNCH;
@@ -237,7 +237,7 @@ struct TileInfo {
 };
 static_assert(sizeof(TileInfo) <= kTileInfoBytes, "TileInfo size");
 
-template <int L, int QP>
+template <int L, int QP, bool F16>
 __global__ void __launch_bounds__(kThreads, 1)
     na2d_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                          const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
@@ -433,8 +433,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ================= S^T / dP^T issuer: chunk c into TMEM chunk slot c & 1, once the dV/dK MMAs
     // of chunk c - 2 (which read that slot) have completed.  dV/dK have their own issuing warp, so
     // neither stream waits behind the other's dependencies.
-    constexpr uint32_t idesc_s = idesc_bf16(64, kNCH, false);
-    constexpr uint32_t idesc_s2 = idesc_bf16(64, 2 * QP, false);  // a chunk of one row pair
+    constexpr uint32_t idesc_s = idesc_el<F16>(64, kNCH, false);
+    constexpr uint32_t idesc_s2 = idesc_el<F16>(64, 2 * QP, false);  // a chunk of one row pair
     int c = 0;
     for (int it = 0;; ++it) {
       const int stage = it % kStages;
@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == kMmaKvWarp) {
     // ================= dV / dK issuer: chunk c once its P^T / dS^T are in TMEM; accumulates in TMEM
     // buffer (tile & 1), so a tile's MMAs never wait for the previous tile's epilogue
-    constexpr uint32_t idesc_o = idesc_bf16(64, kD, true);
+    constexpr uint32_t idesc_o = idesc_el<F16>(64, kD, true);
     int c = 0;
     for (int it = 0;; ++it) {
       const int stage = it % kStages, b = it & 1;
@@ -551,15 +551,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int z = 0; z < 4; ++z) {
           const int zz = (z ^ (R >> 1)) & 3;
           *(uint4 *)(rv + 16 * zz) = make_uint4(
-              pack_bf16(__uint_as_float(a0[8 * z]), __uint_as_float(a0[8 * z + 1])),
-              pack_bf16(__uint_as_float(a0[8 * z + 2]), __uint_as_float(a0[8 * z + 3])),
-              pack_bf16(__uint_as_float(a0[8 * z + 4]), __uint_as_float(a0[8 * z + 5])),
-              pack_bf16(__uint_as_float(a0[8 * z + 6]), __uint_as_float(a0[8 * z + 7])));
+              pack_el<F16>(__uint_as_float(a0[8 * z]), __uint_as_float(a0[8 * z + 1])),
+              pack_el<F16>(__uint_as_float(a0[8 * z + 2]), __uint_as_float(a0[8 * z + 3])),
+              pack_el<F16>(__uint_as_float(a0[8 * z + 4]), __uint_as_float(a0[8 * z + 5])),
+              pack_el<F16>(__uint_as_float(a0[8 * z + 6]), __uint_as_float(a0[8 * z + 7])));
           *(uint4 *)(rk + 16 * zz) = make_uint4(
-              pack_bf16(__uint_as_float(a1[8 * z]) * p.scale, __uint_as_float(a1[8 * z + 1]) * p.scale),
-              pack_bf16(__uint_as_float(a1[8 * z + 2]) * p.scale, __uint_as_float(a1[8 * z + 3]) * p.scale),
-              pack_bf16(__uint_as_float(a1[8 * z + 4]) * p.scale, __uint_as_float(a1[8 * z + 5]) * p.scale),
-              pack_bf16(__uint_as_float(a1[8 * z + 6]) * p.scale, __uint_as_float(a1[8 * z + 7]) * p.scale));
+              pack_el<F16>(__uint_as_float(a1[8 * z]) * p.scale, __uint_as_float(a1[8 * z + 1]) * p.scale),
+              pack_el<F16>(__uint_as_float(a1[8 * z + 2]) * p.scale, __uint_as_float(a1[8 * z + 3]) * p.scale),
+              pack_el<F16>(__uint_as_float(a1[8 * z + 4]) * p.scale, __uint_as_float(a1[8 * z + 5]) * p.scale),
+              pack_el<F16>(__uint_as_float(a1[8 * z + 6]) * p.scale, __uint_as_float(a1[8 * z + 7]) * p.scale));
         }
         fence_proxy_async_smem();
         __syncwarp();
@@ -617,10 +617,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         // clips, so its P / dS columns may hold anything
         if (kc0 + 4 * quarter < p.W) {
           if (fast)
-            chunk_rows<L, QP, true>(lane_addr, uc, tbl_row0, colterm, lrow0, pk, i_base, p.H, rows_here, Lh, sl2,
+            chunk_rows<L, QP, true, F16>(lane_addr, uc, tbl_row0, colterm, lrow0, pk, i_base, p.H, rows_here, Lh, sl2,
                                     chunk_rows_even<C::CR>(qn0, qn1, k));
           else
-            chunk_rows<L, QP, false>(lane_addr, uc, tbl_row0, colterm, lrow0, pk, i_base, p.H, rows_here, Lh, sl2,
+            chunk_rows<L, QP, false, F16>(lane_addr, uc, tbl_row0, colterm, lrow0, pk, i_base, p.H, rows_here, Lh, sl2,
                                      chunk_rows_even<C::CR>(qn0, qn1, k));
         }
         tc_wait_st();
@@ -660,7 +660,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int L, int QP>
+template <int L, int QP, bool F16>
 cudaError_t launch_dkdv_t(const Geo &g, const void *q, const void *k, const void *v, const float *rpb,
                           const float *lse, const void *dout, const float *D, void *dk, void *dv,
                           const float *drpb_part, int part_ctas, float *drpb, int *tile_counter,
@@ -670,17 +670,17 @@ cudaError_t launch_dkdv_t(const Geo &g, const void *q, const void *k, const void
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
     attr_err =
-        cudaFuncSetAttribute(na2d_bwd_dkdv_kernel<L, QP>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        cudaFuncSetAttribute(na2d_bwd_dkdv_kernel<L, QP, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   });
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap tq, tdo, tk, tv, tdk, tdv;
   const int BH = g.B * g.heads;
-  if (!make_tmap_bf16_4d(&tq, q, kD, g.W, g.q_rows, BH, QP, C::QRH) ||
-      !make_tmap_bf16_4d(&tdo, dout, kD, g.W, g.q_rows, BH, QP, C::QRH) ||
-      !make_tmap_bf16_4d(&tk, k, kD, g.W, g.kv_rows, BH, 4, 4) ||
-      !make_tmap_bf16_4d(&tv, v, kD, g.W, g.kv_rows, BH, 4, 4) ||
-      !make_tmap_bf16_4d(&tdk, dk, kD, g.W, g.kv_rows, BH, 4, 4) ||
-      !make_tmap_bf16_4d(&tdv, dv, kD, g.W, g.kv_rows, BH, 4, 4))
+  if (!make_tmap_e16_4d(F16, &tq, q, kD, g.W, g.q_rows, BH, QP, C::QRH) ||
+      !make_tmap_e16_4d(F16, &tdo, dout, kD, g.W, g.q_rows, BH, QP, C::QRH) ||
+      !make_tmap_e16_4d(F16, &tk, k, kD, g.W, g.kv_rows, BH, 4, 4) ||
+      !make_tmap_e16_4d(F16, &tv, v, kD, g.W, g.kv_rows, BH, 4, 4) ||
+      !make_tmap_e16_4d(F16, &tdk, dk, kD, g.W, g.kv_rows, BH, 4, 4) ||
+      !make_tmap_e16_4d(F16, &tdv, dv, kD, g.W, g.kv_rows, BH, 4, 4))
     return cudaErrorInvalidValue;
   CUtensorMap tl, td;
   const bool tma_lsd = (g.W * 4) % 16 == 0 && make_tmap_f32_3d(&tl, lse, g.W, g.q_rows, BH, C::LP, C::QRH) &&
@@ -714,7 +714,7 @@ cudaError_t launch_dkdv_t(const Geo &g, const void *q, const void *k, const void
   p.trace = (long long *)debug_trace_buffer();
   const int grid = p.num_tiles < tc::num_sms() ? p.num_tiles : tc::num_sms();
   ProfScope ps("na2d_bwd_dkdv_tc", st);
-  const cudaError_t e = launch_pdl(na2d_bwd_dkdv_kernel<L, QP>, grid, kThreads, C::SMEM, st, tq, tdo, tk, tv, tl, td, tdk, tdv, p);
+  const cudaError_t e = launch_pdl(na2d_bwd_dkdv_kernel<L, QP, F16>, grid, kThreads, C::SMEM, st, tq, tdo, tk, tv, tl, td, tdk, tdv, p);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
@@ -758,10 +758,14 @@ cudaError_t tc_backward_dkdv(const Geo &g, const void *q, const void *k, const v
   // the query halo of a 16-column key tile is at most 16 + 2NS + 1 <= 23 columns away from the right
   // clamp zone; tiles reaching it are shifted (key_col0)
   if (!tc_dkdv_supported(g)) return cudaErrorNotSupported;
+  const bool f16 = g.dtype == NA2D_F16;
   switch (g.L) {
-    case 3: return launch_dkdv_t<3, 24>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, tile_counter, st);
-    case 5: return launch_dkdv_t<5, 24>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, tile_counter, st);
-    case 7: return launch_dkdv_t<7, 24>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, tile_counter, st);
+    case 3: return f16 ? launch_dkdv_t<3, 24, true>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, tile_counter, st)
+                 : launch_dkdv_t<3, 24, false>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, tile_counter, st);
+    case 5: return f16 ? launch_dkdv_t<5, 24, true>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, tile_counter, st)
+                 : launch_dkdv_t<5, 24, false>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, tile_counter, st);
+    case 7: return f16 ? launch_dkdv_t<7, 24, true>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, tile_counter, st)
+                 : launch_dkdv_t<7, 24, false>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, tile_counter, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -117,7 +117,7 @@ __device__ __forceinline__ void qtrace(const BwdQParams &p, int it, int ev) {
   if (p.trace && blockIdx.x % 37 == 0 && it < 32) p.trace[4096 + ((size_t)(blockIdx.x / 37) * 32 + it) * 32 + ev] = clock64();
 }
 
-template <int L>
+template <int L, bool F16>
 __global__ void __launch_bounds__(kThreads, 1)
     na2d_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                        const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
@@ -232,8 +232,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // S / dP of tile it + 1 straight behind it (the in-order tensor pipe finishes reading dS and the
     // K tile before S / dP overwrite their columns), so the elementwise warps start the next tile
     // while the epilogue reads dQ.
-    constexpr uint32_t idesc_s = idesc_bf16(64, C::NSUB, false);
-    constexpr uint32_t idesc_q = idesc_bf16(64, kD, true);
+    constexpr uint32_t idesc_s = idesc_el<F16>(64, C::NSUB, false);
+    constexpr uint32_t idesc_q = idesc_el<F16>(64, kD, true);
     const int n = t_end - t_begin;
     const uint32_t t0 = tmem, t1 = tmem + ((uint32_t)16 << 16);
     auto issue_sdp = [&](int it) {
@@ -462,8 +462,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                                         __fadd2_rn(make_float2(__uint_as_float(pb_[z]), __uint_as_float(pb_[z + 1])), nD));
           acc[ul][z / 2] = __fadd2_rn(acc[ul][z / 2], dsa);
           acc[ul + 1][z / 2] = __fadd2_rn(acc[ul + 1][z / 2], dsb);
-          da[z / 2] = pack_bf16(dsa.x, dsa.y);
-          db[z / 2] = pack_bf16(dsb.x, dsb.y);
+          da[z / 2] = pack_el<F16>(dsa.x, dsa.y);
+          db[z / 2] = pack_el<F16>(dsb.x, dsb.y);
         }
         const uint32_t prow = ds_base + u * (kHCP / 2);
         st_zero12(prow);
@@ -513,10 +513,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int z = 2 * hh + z2;
           const uint32_t *v = o[hh] + 8 * z2;
           *(uint4 *)(orow + 16 * ((z ^ (R >> 1)) & 3)) = make_uint4(
-              pack_bf16(__uint_as_float(v[0]) * p.scale, __uint_as_float(v[1]) * p.scale),
-              pack_bf16(__uint_as_float(v[2]) * p.scale, __uint_as_float(v[3]) * p.scale),
-              pack_bf16(__uint_as_float(v[4]) * p.scale, __uint_as_float(v[5]) * p.scale),
-              pack_bf16(__uint_as_float(v[6]) * p.scale, __uint_as_float(v[7]) * p.scale));
+              pack_el<F16>(__uint_as_float(v[0]) * p.scale, __uint_as_float(v[1]) * p.scale),
+              pack_el<F16>(__uint_as_float(v[2]) * p.scale, __uint_as_float(v[3]) * p.scale),
+              pack_el<F16>(__uint_as_float(v[4]) * p.scale, __uint_as_float(v[5]) * p.scale),
+              pack_el<F16>(__uint_as_float(v[6]) * p.scale, __uint_as_float(v[7]) * p.scale));
         }
       fence_proxy_async_smem();
       __syncwarp();
@@ -549,7 +549,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int L>
+template <int L, bool F16>
 cudaError_t launch_dq(const Geo &g, const void *q, const void *k, const void *v, const float *rpb, const void *out,
                       const float *lse, const void *dout, void *dq, float *drpb, float *D, float *part,
                       int *b2_tile_counter, cudaStream_t st) {
@@ -557,16 +557,16 @@ cudaError_t launch_dq(const Geo &g, const void *q, const void *k, const void *v,
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(na2d_bwd_dq_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    attr_err = cudaFuncSetAttribute(na2d_bwd_dq_kernel<L, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   });
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap tq, tdo, tk, tv, tdq;
   const int BH = g.B * g.heads;
-  if (!make_tmap_bf16_4d(&tq, q, kD, g.W, g.q_rows, BH, 4, 4) ||
-      !make_tmap_bf16_4d(&tdo, dout, kD, g.W, g.q_rows, BH, 4, 4) ||
-      !make_tmap_bf16_4d(&tk, k, kD, g.W, g.kv_rows, BH, kHCP, C::HR) ||
-      !make_tmap_bf16_4d(&tv, v, kD, g.W, g.kv_rows, BH, kHCP, C::HR) ||
-      !make_tmap_bf16_4d(&tdq, dq, kD, g.W, g.q_rows, BH, 4, 4))
+  if (!make_tmap_e16_4d(F16, &tq, q, kD, g.W, g.q_rows, BH, 4, 4) ||
+      !make_tmap_e16_4d(F16, &tdo, dout, kD, g.W, g.q_rows, BH, 4, 4) ||
+      !make_tmap_e16_4d(F16, &tk, k, kD, g.W, g.kv_rows, BH, kHCP, C::HR) ||
+      !make_tmap_e16_4d(F16, &tv, v, kD, g.W, g.kv_rows, BH, kHCP, C::HR) ||
+      !make_tmap_e16_4d(F16, &tdq, dq, kD, g.W, g.q_rows, BH, 4, 4))
     return cudaErrorInvalidValue;
   BwdQParams p;
   p.heads = g.heads;
@@ -591,7 +591,7 @@ cudaError_t launch_dq(const Geo &g, const void *q, const void *k, const void *v,
   (void)drpb;  // summed from the partial tables by B2
   {
     ProfScope ps("na2d_bwd_dq_tc", st);
-    const cudaError_t e = launch_pdl(na2d_bwd_dq_kernel<L>, grid, kThreads, C::SMEM, st, tq, tdo, tk, tv, tdq, p);
+    const cudaError_t e = launch_pdl(na2d_bwd_dq_kernel<L, F16>, grid, kThreads, C::SMEM, st, tq, tdo, tk, tv, tdq, p);
     if (e != cudaSuccess) return e;
   }
   // the per-CTA dRPB partial tables are summed by the dK/dV kernel (B2), which runs next
@@ -608,10 +608,14 @@ int dq_grid(const Geo &g) {
 cudaError_t tc_backward_dq(const Geo &g, const void *q, const void *k, const void *v, const float *rpb,
                            const void *out, const float *lse, const void *dout, void *dq, float *drpb, float *D,
                            float *part, int *b2_tile_counter, cudaStream_t st) {
+  const bool f16 = g.dtype == NA2D_F16;
   switch (g.L) {
-    case 3: return launch_dq<3>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D, part, b2_tile_counter, st);
-    case 5: return launch_dq<5>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D, part, b2_tile_counter, st);
-    case 7: return launch_dq<7>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D, part, b2_tile_counter, st);
+    case 3: return f16 ? launch_dq<3, true>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D, part, b2_tile_counter, st)
+                 : launch_dq<3, false>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D, part, b2_tile_counter, st);
+    case 5: return f16 ? launch_dq<5, true>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D, part, b2_tile_counter, st)
+                 : launch_dq<5, false>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D, part, b2_tile_counter, st);
+    case 7: return f16 ? launch_dq<7, true>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D, part, b2_tile_counter, st)
+                 : launch_dq<7, false>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D, part, b2_tile_counter, st);
   }
   return cudaErrorInvalidValue;
 }

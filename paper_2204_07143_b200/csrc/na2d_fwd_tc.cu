@@ -125,7 +125,7 @@ __device__ __forceinline__ void trace_ev(const FwdParams &p, int it, int ev) {
 __device__ __forceinline__ void trace_ev(const FwdParams &, int, int) {}
 #endif
 
-template <int L>
+template <int L, bool F16>
 __global__ void __launch_bounds__(kThreads, 1)
     na2d_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                        const __grid_constant__ CUtensorMap tm_v, const FwdParams p) {
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // The PV MMAs have their own issuing warp, so neither stream waits behind the other's
     // dependencies.  Shared-memory descriptors are built once per stage and advanced by
     // (byte offset >> 4).
-    constexpr uint32_t idesc_qk = idesc_bf16(64, C::NSUB, false);
+    constexpr uint32_t idesc_qk = idesc_el<F16>(64, C::NSUB, false);
     for (int it = 0; it < t_end - t_begin; ++it) {
       const int s = it % kStagesQK, slot = it & 1;
       mbar_wait(&full[s], (it / kStagesQK) & 1);
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == kPvWarp) {
     // ================= PV issuer: O of tile it (slot it & 1) one union row pair at a time as the
     // elementwise warps release it (the PV overlaps pass 2)
-    constexpr uint32_t idesc_pv = idesc_bf16(64, kD, true);
+    constexpr uint32_t idesc_pv = idesc_el<F16>(64, kD, true);
     for (int it = 0; it < t_end - t_begin; ++it) {
       const int s = it % kStagesV, slot = it & 1;
       mbar_wait(&full_v[s], (it / kStagesV) & 1);
@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float2 a = __fadd2_rn(make_float2(__uint_as_float(cur[2 * z]), __uint_as_float(cur[2 * z + 1])), nm);
             const float2 e = make_float2(ex2(a.x), ex2(a.y));
             sum2 = __fadd2_rn(sum2, e);
-            pk[z] = pack_bf16(e.x, e.y);
+            pk[z] = pack_el<F16>(e.x, e.y);
           }
           if (k > 0) {
             tc_wait_st();
@@ -549,8 +549,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint4 *dst = (uint4 *)(p.out + qi * kD + 16 * hf);
 #pragma unroll
         for (int z = 0; z < 16; z += 8)
-          dst[z / 8] = make_uint4(pack_bf16(o[z] * inv, o[z + 1] * inv), pack_bf16(o[z + 2] * inv, o[z + 3] * inv),
-                                  pack_bf16(o[z + 4] * inv, o[z + 5] * inv), pack_bf16(o[z + 6] * inv, o[z + 7] * inv));
+          dst[z / 8] = make_uint4(pack_el<F16>(o[z] * inv, o[z + 1] * inv), pack_el<F16>(o[z + 2] * inv, o[z + 3] * inv),
+                                  pack_el<F16>(o[z + 4] * inv, o[z + 5] * inv), pack_el<F16>(o[z + 6] * inv, o[z + 7] * inv));
         if (p.lse && hf == 0) p.lse[qi] = (mx + __log2f(sum)) * 0.69314718055994531f;
       }
       if (tr) trace_ev(p, it, 9);
@@ -570,21 +570,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int L>
+template <int L, bool F16>
 cudaError_t launch_fwd(const Geo &g, const void *q, const void *k, const void *v, const float *rpb, void *out,
                        float *lse, cudaStream_t st) {
   using C = Cfg<L>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(na2d_fwd_tc_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    attr_err = cudaFuncSetAttribute(na2d_fwd_tc_kernel<L, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   });
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap tq, tk, tv;
   const int BH = g.B * g.heads;
-  if (!make_tmap_bf16_4d(&tq, q, kD, g.W, g.q_rows, BH, 4, 4) ||
-      !make_tmap_bf16_4d(&tk, k, kD, g.W, g.kv_rows, BH, kHCP, C::HR) ||
-      !make_tmap_bf16_4d(&tv, v, kD, g.W, g.kv_rows, BH, kHCP, C::HR))
+  if (!make_tmap_e16_4d(F16, &tq, q, kD, g.W, g.q_rows, BH, 4, 4) ||
+      !make_tmap_e16_4d(F16, &tk, k, kD, g.W, g.kv_rows, BH, kHCP, C::HR) ||
+      !make_tmap_e16_4d(F16, &tv, v, kD, g.W, g.kv_rows, BH, kHCP, C::HR))
     return cudaErrorInvalidValue;
   FwdParams p;
   p.B = g.B;
@@ -604,22 +604,26 @@ cudaError_t launch_fwd(const Geo &g, const void *q, const void *k, const void *v
   p.trace = (long long *)debug_trace_buffer();
   const int grid = p.num_tiles < num_sms() ? p.num_tiles : num_sms();
   ProfScope ps("na2d_fwd_tc", st);
-  const cudaError_t e = launch_pdl(na2d_fwd_tc_kernel<L>, grid, kThreads, C::SMEM, st, tq, tk, tv, p);
+  const cudaError_t e = launch_pdl(na2d_fwd_tc_kernel<L, F16>, grid, kThreads, C::SMEM, st, tq, tk, tv, p);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace
 
 bool tc_forward_supported(const Geo &g) {
-  return g.dtype == NA2D_BF16 && g.d == kD && (g.L == 3 || g.L == 5 || g.L == 7) && tmap_available();
+  return (g.dtype == NA2D_BF16 || g.dtype == NA2D_F16) && g.d == kD && (g.L == 3 || g.L == 5 || g.L == 7) && tmap_available();
 }
 
 cudaError_t tc_forward(const Geo &g, const void *q, const void *k, const void *v, const float *rpb, void *out,
                        float *lse, cudaStream_t st) {
+  const bool f16 = g.dtype == NA2D_F16;
   switch (g.L) {
-    case 3: return launch_fwd<3>(g, q, k, v, rpb, out, lse, st);
-    case 5: return launch_fwd<5>(g, q, k, v, rpb, out, lse, st);
-    case 7: return launch_fwd<7>(g, q, k, v, rpb, out, lse, st);
+    case 3: return f16 ? launch_fwd<3, true>(g, q, k, v, rpb, out, lse, st)
+                 : launch_fwd<3, false>(g, q, k, v, rpb, out, lse, st);
+    case 5: return f16 ? launch_fwd<5, true>(g, q, k, v, rpb, out, lse, st)
+                 : launch_fwd<5, false>(g, q, k, v, rpb, out, lse, st);
+    case 7: return f16 ? launch_fwd<7, true>(g, q, k, v, rpb, out, lse, st)
+                 : launch_fwd<7, false>(g, q, k, v, rpb, out, lse, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -272,6 +272,11 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool b_mn_major)
          | ((uint32_t)(N >> 3) << 17)       // N / 8
          | ((uint32_t)(M >> 4) << 24);      // M / 16
 }
+// the same with fp16 A/B (format code 0) when F16
+template <bool F16>
+__host__ __device__ constexpr uint32_t idesc_el(int M, int N, bool b_mn_major) {
+  return F16 ? idesc_bf16(M, N, b_mn_major) & ~((7u << 7) | (7u << 10)) : idesc_bf16(M, N, b_mn_major);
+}
 
 // D[tmem] (+)= A[smem] * B[smem]
 __device__ __forceinline__ void mma_ss(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
@@ -322,6 +327,16 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
+}
+__device__ __forceinline__ uint32_t pack_f16(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+// the kernels' 16-bit element type: bf16 (F16 = false) or fp16 (F16 = true), RNE
+template <bool F16>
+__device__ __forceinline__ uint32_t pack_el(float lo, float hi) {
+  return F16 ? pack_f16(lo, hi) : pack_bf16(lo, hi);
 }
 
 }  // namespace sm100

@@ -36,6 +36,11 @@ bool bind_context() { return cudaFree(nullptr) == cudaSuccess; }
 bool tmap_available() { return encode_fn() != nullptr; }
 
 bool make_tmap_bf16_4d(CUtensorMap *m, const void *base, int dim, int W, int rows, int outer, int box_w, int box_h) {
+  return make_tmap_e16_4d(false, m, base, dim, W, rows, outer, box_w, box_h);
+}
+
+bool make_tmap_e16_4d(bool f16, CUtensorMap *m, const void *base, int dim, int W, int rows, int outer, int box_w,
+                      int box_h) {
   EncodeFn fn = encode_fn();
   if (!fn || dim * 2 != 64) return false;
   const cuuint64_t gdim[4] = {(cuuint64_t)dim, (cuuint64_t)W, (cuuint64_t)rows, (cuuint64_t)outer};
@@ -43,7 +48,8 @@ bool make_tmap_bf16_4d(CUtensorMap *m, const void *base, int dim, int W, int row
   const cuuint32_t box[4] = {(cuuint32_t)dim, (cuuint32_t)box_w, (cuuint32_t)box_h, 1};
   const cuuint32_t estride[4] = {1, 1, 1, 1};
   auto encode = [&] {
-    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(base), gdim, gstride, box, estride,
+    return fn(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(base),
+              gdim, gstride, box, estride,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   };

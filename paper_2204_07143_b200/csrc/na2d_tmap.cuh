@@ -13,6 +13,9 @@ bool tmap_available();
 // {dim, box_w, box_h, 1} elements and 64-byte swizzle (dim * 2 must be 64).  Out-of-bounds box
 // elements are zero-filled by the hardware.  Returns false on failure.
 bool make_tmap_bf16_4d(CUtensorMap *m, const void *base, int dim, int W, int rows, int outer, int box_w, int box_h);
+// the same for a 16-bit element type: fp16 if f16, else bf16
+bool make_tmap_e16_4d(bool f16, CUtensorMap *m, const void *base, int dim, int W, int rows, int outer, int box_w,
+                      int box_h);
 
 }  // namespace na2d
 

@@ -51,7 +51,7 @@ def run_oracle(inp: dict, L: int, scale: float, backward: bool = True, **band):
 def run_cuda(inp: dict, L: int, scale: float, dtype: str, backward: bool = True, device="cuda", **band):
     import torch
     import paper_2204_07143_b200 as na2d
-    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    tdt = {"bf16": torch.bfloat16, "f16": torch.float16, "f32": torch.float32}[dtype]
     t = {n: torch.from_numpy(np.ascontiguousarray(inp[n])).to(device=device, dtype=tdt) for n in ("q", "k", "v", "dout")}
     rpb = None if inp["rpb"] is None else torch.from_numpy(np.ascontiguousarray(inp["rpb"])).to(device)
     kw = {}

@@ -46,12 +46,12 @@ SMALL = [
 
 
 @pytest.mark.parametrize("shape", SMALL, ids=lambda s: s.name)
-@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("dtype", ["bf16", "f32", "f16"])
 def test_small_shapes(shape, dtype):
     check(shape, dtype)
 
 
-@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("dtype", ["bf16", "f32", "f16"])
 def test_no_rpb(dtype):
     check(Shape("norpb", 2, 2, 19, 23, 32, 7), dtype, rpb=None)
 
@@ -95,7 +95,7 @@ def test_rpb_one_hot_probe(L):
         assert hits >= 1
 
 
-@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("dtype", ["bf16", "f32", "f16"])
 def test_row_band(dtype):
     """Band call (global coordinates) == oracle band call, incl. dk/dv partials."""
     shape = Shape("band", 2, 2, 40, 27, 32, 7)
@@ -121,6 +121,12 @@ def test_baseline_configs_full_size(name):
 
 def test_config1_fp32():
     check(CONFIGS["cfg1_8x8_k3"], "f32")
+
+
+def test_config2_fp16_full_size():
+    """fp16 I/O (NA2D_F16) on the same tcgen05 kernels at the stage-1 configuration."""
+    rep = check(CONFIGS["cfg2_nat_tiny_s1"], "f16")
+    print("cfg2 f16", {k: f"{e:.2e}/{t:.1e}" for k, (e, t) in rep.items()})
 
 
 def test_kernel_family_and_launches():
