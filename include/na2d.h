@@ -44,9 +44,9 @@
  *
  * Precision: NA2D_BF16 = bf16 in/out, fp32 accumulation (tcgen05 tensor cores), fp32 LSE and
  * dRPB.  NA2D_F32 = fp32 in/out, fp32 SIMT FMA (no TF32), for 1e-4 relative parity.
- * NA2D_F16 = fp16 in/out (mixed-precision training I/O), same kernels as bf16 with fp16 MMA
- * operands (P and dS rounded to fp16); tensor-core shapes only (dim = 32, kernel_size 3/5/7),
- * other shapes and the paper-decomposition calls return NA2D_ERR_UNSUPPORTED.
+ * NA2D_F16 = fp16 in/out (mixed-precision training I/O): the bf16 tensor-core kernels with fp16
+ * MMA operands (P and dS rounded to fp16) for dim = 32, kernel_size 3/5/7; the SIMT and
+ * paper-decomposition kernels (fp32 arithmetic, fp16 loads/stores) otherwise.
  */
 #ifndef NA2D_H_
 #define NA2D_H_

@@ -116,7 +116,6 @@ na2d_status na2d_forward(const na2d_problem *p, const void *q, const void *k, co
   if (!q || !k || !v || !out) return NA2D_ERR_NULL_POINTER;
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(out) || !aligned16(lse) || !aligned16(rpb))
     return NA2D_ERR_ALIGNMENT;
-  if (g.dtype == NA2D_F16 && !use_tc(g, 0)) return NA2D_ERR_UNSUPPORTED;  // fp16: tensor-core shapes only
   cudaStream_t st = (cudaStream_t)stream;
   (void)cudaGetLastError();  // a non-sticky error left by an unrelated earlier runtime call is not ours
   if (use_tc(g, 0)) return cuda_status(tc_forward(g, q, k, v, rpb, out, lse, st));
@@ -137,7 +136,6 @@ na2d_status na2d_backward(const na2d_problem *p, const void *q, const void *k, c
   if (s != NA2D_OK) return s;
   if (!q || !k || !v || !out || !lse || !dout || !dq || !dk || !dv) return NA2D_ERR_NULL_POINTER;
   if ((rpb == nullptr) != (drpb == nullptr)) return NA2D_ERR_INVALID_ARG;
-  if (g.dtype == NA2D_F16 && !use_tc(g, 1)) return NA2D_ERR_UNSUPPORTED;  // fp16: tensor-core shapes only
   const size_t need = bwd_ws(g);
   if (workspace_bytes < need) return NA2D_ERR_WORKSPACE;
   if (!workspace) return NA2D_ERR_NULL_POINTER;
@@ -166,7 +164,6 @@ na2d_status na2d_paper_forward(const na2d_problem *p, const void *q, const void 
   na2d_status s = make_geo(p, &g);
   if (s != NA2D_OK) return s;
   if (!q || !k || !v || !out || !lse || !attn) return NA2D_ERR_NULL_POINTER;
-  if (g.dtype == NA2D_F16) return NA2D_ERR_UNSUPPORTED;  // comparison path: bf16 / fp32 only
   const void *ptrs[] = {q, k, v, rpb, out, lse, attn};
   for (const void *ptr : ptrs)
     if (!aligned16(ptr)) return NA2D_ERR_ALIGNMENT;
@@ -181,7 +178,6 @@ na2d_status na2d_paper_backward(const na2d_problem *p, const void *q, const void
   na2d_status s = make_geo(p, &g);
   if (s != NA2D_OK) return s;
   if (!q || !k || !v || !dout || !attn || !dS || !dq || !dk || !dv) return NA2D_ERR_NULL_POINTER;
-  if (g.dtype == NA2D_F16) return NA2D_ERR_UNSUPPORTED;  // comparison path: bf16 / fp32 only
   const void *ptrs[] = {q, k, v, dout, attn, dS, dq, dk, dv, drpb};
   for (const void *ptr : ptrs)
     if (!aligned16(ptr)) return NA2D_ERR_ALIGNMENT;

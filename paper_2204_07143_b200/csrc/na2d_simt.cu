@@ -273,6 +273,7 @@ cudaError_t dkdv_t(const Geo &g, const void *q, const void *k, const void *v, co
 cudaError_t simt_forward(const Geo &g, const void *q, const void *k, const void *v, const float *rpb, void *out,
                          float *lse, cudaStream_t st) {
   if (g.dtype == NA2D_F32) return NA2D_DISPATCH_D(fwd_t, float, g, q, k, v, rpb, out, lse, st);
+  if (g.dtype == NA2D_F16) return NA2D_DISPATCH_D(fwd_t, __half, g, q, k, v, rpb, out, lse, st);
   return NA2D_DISPATCH_D(fwd_t, __nv_bfloat16, g, q, k, v, rpb, out, lse, st);
 }
 
@@ -281,6 +282,8 @@ cudaError_t simt_backward(const Geo &g, const void *q, const void *k, const void
                           float *drpb, float *D, cudaStream_t st) {
   if (g.dtype == NA2D_F32)
     return NA2D_DISPATCH_D(bwd_t, float, g, q, k, v, rpb, out, lse, dout, dq, dk, dv, drpb, D, st);
+  if (g.dtype == NA2D_F16)
+    return NA2D_DISPATCH_D(bwd_t, __half, g, q, k, v, rpb, out, lse, dout, dq, dk, dv, drpb, D, st);
   return NA2D_DISPATCH_D(bwd_t, __nv_bfloat16, g, q, k, v, rpb, out, lse, dout, dq, dk, dv, drpb, D, st);
 }
 
@@ -290,6 +293,7 @@ cudaError_t simt_backward_dkdv(const Geo &g, const void *q, const void *k, const
                                const float *lse, const void *dout, const float *D, void *dk, void *dv,
                                cudaStream_t st) {
   if (g.dtype == NA2D_F32) return NA2D_DISPATCH_D(dkdv_t, float, g, q, k, v, rpb, lse, dout, D, dk, dv, st);
+  if (g.dtype == NA2D_F16) return NA2D_DISPATCH_D(dkdv_t, __half, g, q, k, v, rpb, lse, dout, D, dk, dv, st);
   return NA2D_DISPATCH_D(dkdv_t, __nv_bfloat16, g, q, k, v, rpb, lse, dout, D, dk, dv, st);
 }
 

@@ -241,12 +241,14 @@ cudaError_t unfused_backward_t(const Geo &g, const void *q, const void *k, const
 
 cudaError_t unfused_forward(const Geo &g, const void *q, const void *k, const void *v, const float *rpb, void *out,
                             float *lse, float *attn, cudaStream_t st) {
+  if (g.dtype == NA2D_F16) return unfused_forward_t<__half>(g, q, k, v, rpb, out, lse, attn, st);
   return g.dtype == NA2D_F32 ? unfused_forward_t<float>(g, q, k, v, rpb, out, lse, attn, st)
                              : unfused_forward_t<__nv_bfloat16>(g, q, k, v, rpb, out, lse, attn, st);
 }
 
 cudaError_t unfused_backward(const Geo &g, const void *q, const void *k, const void *v, const void *dout,
                              const float *attn, float *dS, void *dq, void *dk, void *dv, float *drpb, cudaStream_t st) {
+  if (g.dtype == NA2D_F16) return unfused_backward_t<__half>(g, q, k, v, dout, attn, dS, dq, dk, dv, drpb, st);
   return g.dtype == NA2D_F32 ? unfused_backward_t<float>(g, q, k, v, dout, attn, dS, dq, dk, dv, drpb, st)
                              : unfused_backward_t<__nv_bfloat16>(g, q, k, v, dout, attn, dS, dq, dk, dv, drpb, st);
 }

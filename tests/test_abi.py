@@ -124,12 +124,10 @@ def test_no_cpu_path(na2d):
         na2d.forward(q, q, q, None, 3)
 
 
-def test_f16_tensor_core_shapes_only(na2d):
-    """fp16 I/O runs on the tcgen05 kernels only: other shapes and the paper decomposition return
-    NA2D_ERR_UNSUPPORTED before any launch (na2d.h, NA2D_F16)."""
-    lib = na2d.load_library()
+def test_f16_accepted(na2d):
+    """NA2D_F16 is a valid dtype on every path: validation passes and dispatch picks tcgen05 for
+    the tensor-core shapes, SIMT otherwise (no device needed for these host-side queries)."""
     p = P(na2d, dtype=na2d.NA2D_F16, dim=64)
-    assert lib.na2d_forward(ctypes.byref(p), FAKE, FAKE, FAKE, None, FAKE, None, None) == 5
-    p32 = P(na2d, dtype=na2d.NA2D_F16)
-    assert lib.na2d_paper_forward(ctypes.byref(p32), FAKE, FAKE, FAKE, None, FAKE, FAKE, FAKE, None) == 5
+    assert na2d.na2d_launch_count(p, 0) >= 1
+    assert na2d.na2d_kernel_family(p, 0) == "simt"
     assert na2d.na2d_status_string(4).startswith("dtype must be NA2D_BF16, NA2D_F32 or NA2D_F16")

@@ -57,7 +57,7 @@ def test_no_rpb(dtype):
 
 
 @pytest.mark.parametrize("d,L", [(16, 3), (64, 5), (128, 3), (32, 9), (32, 11), (8, 13)])
-@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("dtype", ["bf16", "f32", "f16"])
 def test_other_dims_and_kernel_sizes(d, L, dtype):
     check(Shape(f"d{d}k{L}", 2, 2, 17, 21, d, L), dtype)
 

@@ -113,15 +113,16 @@ def test_mhna_layer_vs_dense_reference():
 
 
 @pytest.mark.gpu
-def test_nat_block_stage1_step():
-    """One NAT-Tiny stage-1 block (C=64, 2 heads, k=7, 56x56) forward + backward in bf16 on the
-    tcgen05 kernels: finite outputs and gradients reaching every parameter."""
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float16], ids=["bf16", "f16"])
+def test_nat_block_stage1_step(dt):
+    """One NAT-Tiny stage-1 block (C=64, 2 heads, k=7, 56x56) forward + backward in bf16 / fp16 on
+    the tcgen05 kernels: finite outputs and gradients reaching every parameter."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_2204_07143_b200.mhna import NATBlock
     torch.manual_seed(1)
-    blk = NATBlock(64, 2, 7, device="cuda")
-    x = torch.randn(4, 56, 56, 64, device="cuda", dtype=torch.bfloat16, requires_grad=True)
+    blk = NATBlock(64, 2, 7, device="cuda", dtype=dt)
+    x = torch.randn(4, 56, 56, 64, device="cuda", dtype=dt, requires_grad=True)
     y = blk(x)
     y.float().square().mean().backward()
     assert torch.isfinite(y).all()

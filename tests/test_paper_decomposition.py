@@ -21,13 +21,13 @@ def cuda_lib():
 
 
 @pytest.mark.parametrize("shape", SHAPES, ids=lambda s: s.name)
-@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("dtype", ["bf16", "f32", "f16"])
 def test_paper_path_vs_oracle(shape, dtype):
     import torch
     import paper_2204_07143_b200 as na2d
     inp = make_inputs(shape, seed=21, dtype=dtype)
     scale = shape.d ** -0.5
-    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    tdt = {"bf16": torch.bfloat16, "f16": torch.float16, "f32": torch.float32}[dtype]
     t = {n: torch.from_numpy(inp[n]).cuda().to(tdt) for n in ("q", "k", "v", "dout")}
     rpb = torch.from_numpy(inp["rpb"]).cuda()
     out, lse, attn = na2d.paper_forward(t["q"], t["k"], t["v"], rpb, shape.kernel_size, scale)
