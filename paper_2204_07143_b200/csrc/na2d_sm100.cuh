@@ -104,18 +104,6 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *m, uin
       : "memory");
 }
 
-// TMA prefetch of a box into L2 (no shared memory, no completion): warms L2 for a later load
-__device__ __forceinline__ void tma_prefetch_l2_4d(const CUtensorMap *m, int c0, int c1, int c2, int c3) {
-  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];"
-               ::"l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-               : "memory");
-}
-__device__ __forceinline__ void tma_prefetch_l2_3d(const CUtensorMap *m, int c0, int c1, int c2) {
-  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];"
-               ::"l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2)
-               : "memory");
-}
-
 // TMA store smem -> global (bulk group of the issuing thread); out-of-bounds box elements are not
 // written.  The smem source must be made visible to the async proxy first (fence_proxy_async_smem).
 __device__ __forceinline__ void tma_store_4d(const CUtensorMap *m, const void *src, int c0, int c1, int c2, int c3) {
@@ -307,15 +295,6 @@ __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
-}
-// bf16 pair without the XU pipe (F2FP): round half away from zero on the magnitude via the
-// integer ALU, then byte-permute the two high halves.  For finite inputs this differs from RNE
-// only on exact ties.  Used for P (non-negative) and outputs; keeps MUFU.EX2 the only XU op.
-__device__ __forceinline__ uint32_t pack_bf16_alu(float lo, float hi) {
-  const uint32_t a = __float_as_uint(lo) + 0x8000u, b = __float_as_uint(hi) + 0x8000u;
-  uint32_t r;
-  asm("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(r) : "r"(a), "r"(b));
-  return r;
 }
 // three-input max (FMNMX3, sm_100)
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
