@@ -29,3 +29,9 @@ for name, off in (("fwd", 16384), ("B1", 16384 + 512), ("B2", 16384 + 1024)):
           f"CTA duration min/median/max {dur.min():.1f}/{np.median(dur):.1f}/{dur.max():.1f} us  end spread {(en.max() - en.min()) / 1e3:.1f} us")
     order = np.argsort(en)
     print("   slowest CTAs:", order[-5:], "fastest:", order[:5])
+# B1 per-CTA durations in CTA order (contiguous tile ranges of the class-grouped order)
+off = 16384 + 512
+st, en = b[off:off + 296:2], b[off + 1:off + 297:2]
+dur = (en - st) / 1e3
+print("B1 per-CTA duration (us), CTA 0..147:")
+print(" ".join(f"{x:.0f}" for x in dur))
