@@ -666,12 +666,7 @@ cudaError_t launch_dkdv_t(const Geo &g, const void *q, const void *k, const void
                           const float *drpb_part, int part_ctas, float *drpb, int *tile_counter,
                           cudaStream_t st) {
   using C = CfgK<L, QP>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err =
-        cudaFuncSetAttribute(na2d_bwd_dkdv_kernel<L, QP, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-  });
+  const cudaError_t attr_err = tc::ensure_smem_attr((const void *)na2d_bwd_dkdv_kernel<L, QP, F16>, C::SMEM);
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap tq, tdo, tk, tv, tdk, tdv;
   const int BH = g.B * g.heads;

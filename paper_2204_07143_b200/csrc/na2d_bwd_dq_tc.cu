@@ -554,11 +554,7 @@ cudaError_t launch_dq(const Geo &g, const void *q, const void *k, const void *v,
                       const float *lse, const void *dout, void *dq, float *drpb, float *D, float *part,
                       int *b2_tile_counter, cudaStream_t st) {
   using C = CfgQ<L>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(na2d_bwd_dq_kernel<L, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-  });
+  const cudaError_t attr_err = tc::ensure_smem_attr((const void *)na2d_bwd_dq_kernel<L, F16>, C::SMEM);
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap tq, tdo, tk, tv, tdq;
   const int BH = g.B * g.heads;

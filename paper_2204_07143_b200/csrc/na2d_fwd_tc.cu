@@ -574,11 +574,7 @@ template <int L, bool F16>
 cudaError_t launch_fwd(const Geo &g, const void *q, const void *k, const void *v, const float *rpb, void *out,
                        float *lse, cudaStream_t st) {
   using C = Cfg<L>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(na2d_fwd_tc_kernel<L, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-  });
+  const cudaError_t attr_err = tc::ensure_smem_attr((const void *)na2d_fwd_tc_kernel<L, F16>, C::SMEM);
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap tq, tk, tv;
   const int BH = g.B * g.heads;

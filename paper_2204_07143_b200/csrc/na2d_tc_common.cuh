@@ -135,7 +135,9 @@ __device__ __forceinline__ float tree_sum(const float (&x)[N]) {
 }
 
 
-int num_sms();
+int num_sms();  // of the current device
+// raise kernel `func`'s dynamic shared-memory limit on the current device (once per device)
+cudaError_t ensure_smem_attr(const void *func, int smem_bytes);
 
 // Launch with programmatic stream serialization (see pdl_trigger / pdl_wait in na2d_sm100.cuh).
 template <typename... KArgs, typename... Args>
