@@ -1,3 +1,4 @@
+#include <string>
 // tcgen05.mma throughput for the shapes the NA2D kernels use (one CTA per SM, 148 CTAs).
 #include <stdint.h>
 #include <stdio.h>
@@ -554,7 +555,15 @@ int main_old5() {
   return 0;
 }
 
-int main() {
+int main(int argc, char **argv) {
+  // `microbench_mma all`: every section (MMA shapes / chains, TMEM contention, issue mechanics,
+  // B2 chunk, forward sequence); default: the forward sequence only
+  if (argc > 1 && std::string(argv[1]) == "all") {
+    main_old();
+    main_old2();
+    main_old4();
+    main_old5();
+  }
   run_seq<8, true, true>("fwd seq: QK + PV, 8 ld/st warps");
   run_seq<108, true, true>("fwd seq: ... + fence::after_thread_sync per PV block");
   run_seq<100, true, true>("fwd seq: fence, no ld/st warps");
