@@ -38,6 +38,12 @@ constexpr int kStages = 2;
 #define NA2D_B1_GROUPS 3
 #endif
 constexpr int kGroups = NA2D_B1_GROUPS;  // elementwise warp groups (each covers the 4 TMEM lane quarters)
+// S / dP issued per elementwise group's union row pairs, last group first, each part with its own
+// commit: a group starts pass 1 as soon as its own columns have landed
+#ifndef NA2D_B1_SPLIT
+#define NA2D_B1_SPLIT 1
+#endif
+static_assert(!NA2D_B1_SPLIT || kGroups == 3, "S / dP parts of 1 or 2 row pairs (N = 48 / 96) assume 3 groups");
 constexpr int kThreads = 64 + kGroups * 128;  // warps 0.. elementwise, then the TMA and MMA warps
 // (the sub-partition scheduler favours the highest warp id: the producer / MMA warps never wait for
 // the elementwise warps sharing their sub-partitions)
@@ -131,7 +137,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t *bars = (uint64_t *)(smem + C::BAR_OFF);
   uint64_t *full = bars, *empty = bars + kStages;
   uint64_t *sp_full = bars + 2 * kStages, *ds_full = sp_full + 1, *dq_full = sp_full + 2, *dq_free = sp_full + 3;
-  uint32_t *tmem_slot = (uint32_t *)(bars + 2 * kStages + 4);
+  uint64_t *sp_part = sp_full + 4;  // [kGroups]: S / dP columns of group g's row pairs (NA2D_B1_SPLIT)
+  uint32_t *tmem_slot = (uint32_t *)(bars + 2 * kStages + 4 + kGroups);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int t_begin = (int)((long)p.num_tiles * blockIdx.x / gridDim.x);
@@ -145,6 +152,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(sp_full, 1);
+    for (int g = 0; g < kGroups; ++g) mbar_init(&sp_part[g], 1);
     mbar_init(ds_full, 4 * kGroups);
     mbar_init(dq_full, 1);
     mbar_init(dq_free, 4);
@@ -233,6 +241,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // K tile before S / dP overwrite their columns), so the elementwise warps start the next tile
     // while the epilogue reads dQ.
     constexpr uint32_t idesc_s = idesc_el<F16>(64, C::NSUB, false);
+    constexpr uint32_t idesc_p1 = idesc_el<F16>(64, 2 * kHCP, false), idesc_p2 = idesc_el<F16>(64, 4 * kHCP, false);
     constexpr uint32_t idesc_q = idesc_el<F16>(64, kD, true);
     const int n = t_end - t_begin;
     const uint32_t t0 = tmem, t1 = tmem + ((uint32_t)16 << 16);
@@ -247,6 +256,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t dk0 = dqs + ((2 * C::Q_BYTES + rb0 * kHCP * kRowBytes) >> 4);
       const uint64_t dk1 = dqs + ((2 * C::Q_BYTES + rb1 * kHCP * kRowBytes) >> 4);
       if (elect_one()) {
+#if NA2D_B1_SPLIT
+        // group g's row pairs = S / dP columns [48 pr0(g), 48 pr0(g+1)) = keys of the same range
+#pragma unroll
+        for (int g = kGroups - 1; g >= 0; --g) {
+          const int c0 = 2 * kHCP * C::pr0(g), nc = 2 * kHCP * (C::pr0(g + 1) - C::pr0(g));
+          const uint32_t id = nc == 2 * kHCP ? idesc_p1 : idesc_p2;
+          const uint32_t bo = (c0 * kRowBytes) >> 4;  // key offset of the part in the K / V halos
+#pragma unroll
+          for (int k = 0; k < kD / 16; ++k) {
+            const uint32_t ko = (k * 32) >> 4;
+            mma_ss(t0 + c0, dqs + ko, dk0 + bo + ko, id, k);
+            mma_ss(t0 + C::DP_COL + c0, dqs + (C::Q_BYTES >> 4) + ko, dk0 + (C::KV_BYTES >> 4) + bo + ko, id, k);
+            mma_ss(t1 + c0, dqs + (4096 >> 4) + ko, dk1 + bo + ko, id, k);
+            mma_ss(t1 + C::DP_COL + c0, dqs + ((C::Q_BYTES + 4096) >> 4) + ko, dk1 + (C::KV_BYTES >> 4) + bo + ko, id, k);
+          }
+          mma_commit(&sp_part[g]);
+        }
+#else
 #pragma unroll
         for (int k = 0; k < kD / 16; ++k) {
           const uint32_t ko = (k * 32) >> 4;
@@ -256,6 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mma_ss(t1 + C::DP_COL, dqs + ((C::Q_BYTES + 4096) >> 4) + ko, dk1 + (C::KV_BYTES >> 4) + ko, idesc_s, k);
         }
         mma_commit(sp_full);
+#endif
       }
       __syncwarp();
       if (lane == 0) qtrace(p, it, 2);
@@ -388,7 +416,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (tq) qtrace(p, it, 8);
       const float nlse2 = -((const float *)(smem + stage * C::STAGE_BYTES + C::LSE_OFF))[half * 64 + quarter * 16 + r * 4 + c];
       const float2 nlse2x2 = make_float2(nlse2, nlse2);
-      mbar_wait(sp_full, ph);
+      mbar_wait(NA2D_B1_SPLIT ? &sp_part[grp] : sp_full, ph);
       if (tq) qtrace(p, it, 9);
       tc_fence_after();
       // ---- pass 1: P = exp2(s*scale*log2e + B' - LSE*log2e) (fp32, written over S in place) and
