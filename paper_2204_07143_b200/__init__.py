@@ -193,6 +193,44 @@ def _stream(t):
     return torch.cuda.current_stream(t.device).cuda_stream
 
 
+def _expect(t, name, shape, dtype, device):
+    """The C ABI cannot see buffer sizes: every tensor's shape, dtype and device is checked here,
+    before the library is called, so a mismatch raises instead of reading or writing out of bounds."""
+    if t is None:
+        return
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: shape {tuple(t.shape)}, expected {tuple(shape)}")
+    if t.dtype != dtype:
+        raise ValueError(f"{name}: dtype {t.dtype}, expected {dtype}")
+    if t.device != device:
+        raise ValueError(f"{name}: on {t.device}, expected {device} (the device of q)")
+
+
+def _validate(q, k, v, rpb, kernel_size, **named):
+    """q [B,heads,H,W,d]; k, v [B,heads,kv_rows,W,d] (kv_rows = H unless a row band); rpb fp32
+    [heads,2L-1,2L-1]; named: dout/out like q, lse fp32 [B,heads,H,W], dq like q, dk/dv like k,
+    drpb like rpb."""
+    import torch
+    if q.dim() != 5:
+        raise ValueError(f"q: expected [B,heads,H,W,d], got shape {tuple(q.shape)}")
+    B, heads, H, W, d = q.shape
+    dev, dt = q.device, q.dtype
+    kshape = (B, heads, k.shape[2] if k.dim() == 5 else -1, W, d)
+    _expect(k, "k", kshape, dt, dev)
+    _expect(v, "v", kshape, dt, dev)
+    T = 2 * int(kernel_size) - 1
+    _expect(rpb, "rpb", (heads, T, T), torch.float32, dev)
+    like = {"dout": (q.shape, dt), "out": (q.shape, dt), "dq": (q.shape, dt), "lse": (q.shape[:4], torch.float32),
+            "dk": (kshape, dt), "dv": (kshape, dt), "drpb": ((heads, T, T), torch.float32)}
+    for n, t in named.items():
+        shape, tdt = like[n]
+        _expect(t, n, shape, tdt, dev)
+    if (rpb is None) != (named.get("drpb", rpb) is None):
+        raise ValueError("drpb must be given exactly when rpb is given")
+    if not q.is_cuda:
+        raise ValueError("q must be a CUDA tensor (no CPU path exists)")
+
+
 def problem_for(q, k, kernel_size, scale=None, *, map_height=0, q_row0=0, kv_row0=0) -> na2d_problem:
     B, heads, H, W, d = q.shape
     return make_problem(B, heads, H, W, d, kernel_size, _dtype_code(q), scale, map_height=map_height,
@@ -204,11 +242,13 @@ def forward(q, k, v, rpb, kernel_size: int, scale: float | None = None, *, map_h
     """Eq. 2 forward.  q: [B,heads,H,W,d] (bf16 or fp32, CUDA); k, v: [B,heads,kv_rows,W,d];
     rpb: [heads,2L-1,2L-1] fp32 or None.  Returns (out, lse fp32 [B,heads,H,W])."""
     import torch
+    _validate(q, k, v, rpb, kernel_size, out=out, lse=lse)
     p = problem_for(q, k, kernel_size, scale, map_height=map_height, q_row0=q_row0, kv_row0=kv_row0)
-    out = torch.empty_like(q) if out is None else out
-    lse = torch.empty(q.shape[:4], device=q.device, dtype=torch.float32) if lse is None else lse
-    na2d_forward(p, _dev(q, "q"), _dev(k, "k"), _dev(v, "v"), _dev(rpb, "rpb"), _dev(out, "out"), _dev(lse, "lse"),
-                 _stream(q))
+    with torch.cuda.device(q.device):  # the library launches on the current device
+        out = torch.empty_like(q) if out is None else out
+        lse = torch.empty(q.shape[:4], device=q.device, dtype=torch.float32) if lse is None else lse
+        na2d_forward(p, _dev(q, "q"), _dev(k, "k"), _dev(v, "v"), _dev(rpb, "rpb"), _dev(out, "out"),
+                     _dev(lse, "lse"), _stream(q))
     return out, lse
 
 
@@ -216,18 +256,24 @@ def backward(q, k, v, rpb, out, lse, dout, kernel_size: int, scale: float | None
              q_row0=0, kv_row0=0, workspace=None, grads=None):
     """Analytic backward of Eq. 2.  Returns (dq, dk, dv, drpb or None)."""
     import torch
-    p = problem_for(q, k, kernel_size, scale, map_height=map_height, q_row0=q_row0, kv_row0=kv_row0)
-    nbytes = na2d_backward_workspace_bytes(p)
-    if workspace is None or workspace.numel() < nbytes:
-        workspace = torch.empty(max(nbytes, 16), device=q.device, dtype=torch.uint8)
     if grads is None:
-        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
-        drpb = torch.empty_like(rpb) if rpb is not None else None
+        _validate(q, k, v, rpb, kernel_size, out=out, lse=lse, dout=dout)
     else:
         dq, dk, dv, drpb = grads
-    na2d_backward(p, _dev(q, "q"), _dev(k, "k"), _dev(v, "v"), _dev(rpb, "rpb"), _dev(out, "out"),
-                  _dev(lse, "lse"), _dev(dout, "dout"), _dev(dq, "dq"), _dev(dk, "dk"), _dev(dv, "dv"),
-                  _dev(drpb, "drpb"), _dev(workspace, "workspace"), workspace.numel(), _stream(q))
+        _validate(q, k, v, rpb, kernel_size, out=out, lse=lse, dout=dout, dq=dq, dk=dk, dv=dv, drpb=drpb)
+    if workspace is not None and (workspace.device != q.device or workspace.dtype != torch.uint8):
+        raise ValueError("workspace must be a uint8 tensor on the device of q")
+    p = problem_for(q, k, kernel_size, scale, map_height=map_height, q_row0=q_row0, kv_row0=kv_row0)
+    with torch.cuda.device(q.device):  # the library launches on the current device
+        nbytes = na2d_backward_workspace_bytes(p)
+        if workspace is None or workspace.numel() < nbytes:
+            workspace = torch.empty(max(nbytes, 16), device=q.device, dtype=torch.uint8)
+        if grads is None:
+            dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+            drpb = torch.empty_like(rpb) if rpb is not None else None
+        na2d_backward(p, _dev(q, "q"), _dev(k, "k"), _dev(v, "v"), _dev(rpb, "rpb"), _dev(out, "out"),
+                      _dev(lse, "lse"), _dev(dout, "dout"), _dev(dq, "dq"), _dev(dk, "dk"), _dev(dv, "dv"),
+                      _dev(drpb, "drpb"), _dev(workspace, "workspace"), workspace.numel(), _stream(q))
     return dq, dk, dv, drpb
 
 
@@ -235,26 +281,37 @@ def paper_forward(q, k, v, rpb, kernel_size: int, scale: float | None = None):
     """The paper's unfused decomposition: QK+RPB -> softmax -> AV, materialising the
     attention weights.  Returns (out, lse, attn [B,heads,H,W,Lh*Lw] fp32)."""
     import torch
+    _validate(q, k, v, rpb, kernel_size)
+    if k.shape[2] != q.shape[2]:
+        raise ValueError("the paper decomposition takes whole maps (k, v rows == q rows)")
     p = problem_for(q, k, kernel_size, scale)
     nwin = min(kernel_size, q.shape[2]) * min(kernel_size, q.shape[3])
     out = torch.empty_like(q)
     lse = torch.empty(q.shape[:4], device=q.device, dtype=torch.float32)
     attn = torch.empty(q.shape[:4] + (nwin,), device=q.device, dtype=torch.float32)
-    _check(load_library().na2d_paper_forward(ctypes.byref(p), _dev(q, "q"), _dev(k, "k"), _dev(v, "v"),
-                                             _dev(rpb, "rpb"), _dev(out, "out"), _dev(lse, "lse"),
-                                             _dev(attn, "attn"), _stream(q)), "na2d_paper_forward")
+    with torch.cuda.device(q.device):
+        _check(load_library().na2d_paper_forward(ctypes.byref(p), _dev(q, "q"), _dev(k, "k"), _dev(v, "v"),
+                                                 _dev(rpb, "rpb"), _dev(out, "out"), _dev(lse, "lse"),
+                                                 _dev(attn, "attn"), _stream(q)), "na2d_paper_forward")
     return out, lse, attn
 
 
 def paper_backward(q, k, v, rpb, attn, dout, kernel_size: int, scale: float | None = None, dS=None):
     """Gradients of the unfused decomposition from its stored attention weights."""
     import torch
+    _validate(q, k, v, rpb, kernel_size, dout=dout)
+    if k.shape[2] != q.shape[2]:
+        raise ValueError("the paper decomposition takes whole maps (k, v rows == q rows)")
+    nwin = min(kernel_size, q.shape[2]) * min(kernel_size, q.shape[3])
+    _expect(attn, "attn", q.shape[:4] + (nwin,), torch.float32, q.device)
+    _expect(dS, "dS", q.shape[:4] + (nwin,), torch.float32, q.device)
     p = problem_for(q, k, kernel_size, scale)
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     drpb = torch.empty_like(rpb) if rpb is not None else None
     dS = torch.empty_like(attn) if dS is None else dS
-    _check(load_library().na2d_paper_backward(ctypes.byref(p), _dev(q, "q"), _dev(k, "k"), _dev(v, "v"),
-                                              _dev(dout, "dout"), _dev(attn, "attn"), _dev(dS, "dS"),
-                                              _dev(dq, "dq"), _dev(dk, "dk"), _dev(dv, "dv"),
-                                              _dev(drpb, "drpb"), _stream(q)), "na2d_paper_backward")
+    with torch.cuda.device(q.device):
+        _check(load_library().na2d_paper_backward(ctypes.byref(p), _dev(q, "q"), _dev(k, "k"), _dev(v, "v"),
+                                                  _dev(dout, "dout"), _dev(attn, "attn"), _dev(dS, "dS"),
+                                                  _dev(dq, "dq"), _dev(dk, "dk"), _dev(dv, "dv"),
+                                                  _dev(drpb, "drpb"), _stream(q)), "na2d_paper_backward")
     return dq, dk, dv, drpb

@@ -3,12 +3,12 @@
 
 Architecture as PAPER.md states it (§3.3 "Neighborhood Attention Transformer", P:204-224,
 Table 2):
-  * tokenizer: two consecutive 3x3 convolutions with 2x2 strides -> H/4 x W/4 (P:220);
+  * tokenizer: two consecutive 3x3 convolutions with 2x2 strides -> H/4 x W/4 (P:222);
   * 4 levels of NAT blocks (x + MHNA(LN(x)), x + MLP(LN(x))), 7x7 neighbourhoods
     (Table 2 caption), every level but the last followed by a downsampler, a 3x3 stride-2
-    convolution that halves the spatial size and doubles the channels (P:222);
+    convolution that halves the spatial size and doubles the channels (P:224);
   * dims and heads double after every level (Table 2 caption): level-1 dim = 32 x heads;
-  * LayerScale for the larger models (P:224).
+  * LayerScale for the larger models (P:227).
 Readings where the paper is silent (R-NAT): the tokenizer's first convolution has
 C/2 output channels; a LayerNorm follows the tokenizer and each downsampler; the classifier is
 LN -> global average pool -> Linear(1000) (the usual hierarchical-transformer head); LayerScale
@@ -39,7 +39,7 @@ HEAD_DIM = 32  # "32 x heads" (Table 2)
 
 
 class ConvTokenizer(nn.Module):
-    """Two 3x3 stride-2 convolutions (P:220), then LayerNorm; NCHW in, channels-last out."""
+    """Two 3x3 stride-2 convolutions (P:222), then LayerNorm; NCHW in, channels-last out."""
 
     def __init__(self, in_ch: int, dim: int, dtype, device):
         super().__init__()
@@ -53,7 +53,7 @@ class ConvTokenizer(nn.Module):
 
 
 class ConvDownsampler(nn.Module):
-    """3x3 stride-2 convolution doubling the channels (P:222), then LayerNorm; channels-last."""
+    """3x3 stride-2 convolution doubling the channels (P:224), then LayerNorm; channels-last."""
 
     def __init__(self, dim: int, dtype, device):
         super().__init__()
@@ -65,7 +65,7 @@ class ConvDownsampler(nn.Module):
 
 
 class LayerScaleBlock(NATBlock):
-    """NAT block with LayerScale (P:224): x + g1 * MHNA(LN(x)), x + g2 * MLP(LN(x))."""
+    """NAT block with LayerScale (P:227): x + g1 * MHNA(LN(x)), x + g2 * MLP(LN(x))."""
 
     def __init__(self, dim, heads, kernel_size, mlp_ratio, layer_scale: float, dtype, device):
         super().__init__(dim, heads, kernel_size, mlp_ratio, dtype=dtype, device=device)

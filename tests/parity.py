@@ -2,28 +2,56 @@
 on the same seeded inputs and compare element by element with the tolerances of
 BASELINE.json's north_star:
 
-* bf16 I/O, fp32 accumulate: max |gpu - oracle| <= 2e-2 on out, lse, dq, dk, dv;
-  drpb <= 2e-2 * max(1, ||drpb_oracle||_inf) (a sum over up to B*H*W terms, reading R7);
+* bf16 / fp16 I/O, fp32 accumulate: max |gpu - oracle| <= 2e-2 on out, lse, dq, dk, dv;
+  drpb (reading R7): the literal max-abs 2e-2 when the per-head reduction is short
+  (B*H*W <= DRPB_SHORT terms: config 1 and every small shape), else
+  1e-3 * max(1, ||drpb_oracle||_inf) (a sum over up to B*H*W fp32 terms; dS is fp32 on every
+  path, so the observed error is ~1e-6 relative);
 * fp32 path: ||gpu - oracle||_inf <= 1e-4 * max(1, ||oracle||_inf) per tensor.
+Peripheral dRPB cells (one term per map) are pinned separately by the GPU cell probe
+(tests/test_gpu_parity.py::test_drpb_cell_probe).
 """
 from __future__ import annotations
+
+import json
+import os
 
 import numpy as np
 
 BF16_ATOL = 2e-2
 F32_RTOL = 1e-4
+DRPB_LONG_RTOL = 1e-3
+DRPB_SHORT = 4096
 
 
-def tolerance(name: str, ref: np.ndarray, dtype: str) -> float:
+def tolerance(name: str, ref: np.ndarray, dtype: str, terms: int | None = None) -> float:
+    """terms: queries per head summed into each dRPB cell (B*H*W); None = short."""
     scale = max(1.0, float(np.abs(ref).max())) if ref.size else 1.0
     if dtype == "f32":
         return F32_RTOL * scale
-    return BF16_ATOL * (scale if name == "drpb" else 1.0)
+    if name == "drpb" and terms is not None and terms > DRPB_SHORT:
+        return DRPB_LONG_RTOL * scale
+    return BF16_ATOL
 
 
-def compare(got: dict, ref: dict, dtype: str, names=None) -> dict:
-    """Return {name: (max_abs_err, tol)}; raises AssertionError on the first violation."""
+def log_errors(label: str, dtype: str, report: dict) -> None:
+    """Append {label, dtype, errors} to $NA2D_PARITY_LOG (jsonl) when set: the parity margins."""
+    path = os.environ.get("NA2D_PARITY_LOG")
+    if not path:
+        return
+    with open(path, "a") as f:
+        f.write(json.dumps({"case": label, "dtype": dtype,
+                            "errors": {k: {"max_abs_err": e, "tol": t, "margin": (t / e if e > 0 else None)}
+                                       for k, (e, t) in report.items()}}) + "\n")
+
+
+def compare(got: dict, ref: dict, dtype: str, names=None, terms: int | None = None) -> dict:
+    """Return {name: (max_abs_err, tol)}; raises AssertionError on the first violation.
+    terms = B*H*W of the problem (selects the dRPB bound, see the module docstring)."""
     report = {}
+    if terms is None and ref.get("out") is not None and np.ndim(ref["out"]) == 5:
+        B, _, H, W, _ = np.shape(ref["out"])
+        terms = B * H * W
     for n in names or got.keys():
         g, r = got[n], ref[n]
         if g is None or r is None:
@@ -34,7 +62,7 @@ def compare(got: dict, ref: dict, dtype: str, names=None) -> dict:
         assert g.shape == r.shape, (n, g.shape, r.shape)
         assert np.all(np.isfinite(g)), f"{n}: non-finite values"
         err = float(np.abs(g - r).max()) if g.size else 0.0
-        tol = tolerance(n, r, dtype)
+        tol = tolerance(n, r, dtype, terms)
         report[n] = (err, tol)
         assert err <= tol, f"{n}: max abs err {err:.3e} > tol {tol:.3e}"
     return report

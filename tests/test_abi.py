@@ -131,3 +131,38 @@ def test_f16_accepted(na2d):
     assert na2d.na2d_launch_count(p, 0) >= 1
     assert na2d.na2d_kernel_family(p, 0) == "simt"
     assert na2d.na2d_status_string(4).startswith("dtype must be NA2D_BF16, NA2D_F32 or NA2D_F16")
+
+
+@pytest.mark.parametrize("bad", ["k_width", "v_dtype", "rpb_bf16", "rpb_shape", "lse_shape", "dout_shape",
+                                 "drpb_bf16", "drpb_missing"])
+def test_torch_wrapper_validates_buffers(na2d, bad):
+    """The C ABI cannot see buffer sizes: the torch wrappers reject any tensor whose shape or dtype
+    does not match q's geometry (else an out-of-bounds device access), before the library is called."""
+    import torch
+    bf = torch.bfloat16
+    q = torch.zeros(1, 2, 8, 8, 32, dtype=bf)
+    k, v, dout = q.clone(), q.clone(), q.clone()
+    rpb = torch.zeros(2, 5, 5)
+    lse = torch.zeros(1, 2, 8, 8)
+    grads = [q.clone(), q.clone(), q.clone(), rpb.clone()]
+    if bad == "k_width":
+        k = torch.zeros(1, 2, 8, 9, 32, dtype=bf)
+    elif bad == "v_dtype":
+        v = v.float()
+    elif bad == "rpb_bf16":
+        rpb = rpb.to(bf)
+    elif bad == "rpb_shape":
+        rpb = torch.zeros(2, 7, 7)
+    elif bad == "lse_shape":
+        lse = torch.zeros(1, 2, 8, 9)
+    elif bad == "dout_shape":
+        dout = torch.zeros(1, 2, 8, 8, 16, dtype=bf)
+    elif bad == "drpb_bf16":
+        grads[3] = grads[3].to(bf)
+    elif bad == "drpb_missing":
+        grads[3] = None
+    with pytest.raises(ValueError, match="shape|dtype|drpb"):
+        if bad in ("lse_shape", "dout_shape", "drpb_bf16", "drpb_missing"):
+            na2d.backward(q, k, v, rpb, q, lse, dout, 3, grads=grads)
+        else:
+            na2d.forward(q, k, v, rpb, 3)

@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 from na2d_inputs import CONFIGS, Shape, make_inputs
-from tests.parity import compare, run_cuda, run_oracle
+from tests.parity import compare, log_errors, run_cuda, run_oracle
 
 pytestmark = pytest.mark.gpu
 
@@ -27,7 +27,16 @@ def check(shape: Shape, dtype="bf16", rpb="parity", seed=None, backward=True, **
     scale = shape.d ** -0.5
     ref = run_oracle(inp, shape.kernel_size, scale, backward=backward)
     got = run_cuda(inp, shape.kernel_size, scale, dtype, backward=backward)
-    return compare(got, ref, dtype)
+    rep = compare(got, ref, dtype)
+    log_errors(shape.name, dtype, rep)
+    return rep
+
+
+def family(shape: Shape, dtype="bf16"):
+    import paper_2204_07143_b200 as na2d
+    code = {"bf16": na2d.NA2D_BF16, "f16": na2d.NA2D_F16, "f32": na2d.NA2D_F32}[dtype]
+    p = na2d.make_problem(shape.B, shape.heads, shape.H, shape.W, shape.d, shape.kernel_size, code)
+    return na2d.na2d_kernel_family(p, 0), na2d.na2d_kernel_family(p, 1)
 
 
 SMALL = [
@@ -95,6 +104,45 @@ def test_rpb_one_hot_probe(L):
         assert hits >= 1
 
 
+@pytest.mark.parametrize("L", [3, 5, 7])
+def test_drpb_cell_probe(L):
+    """dRPB cell by cell (SURVEY c-11 peripheral cells): head h has dO = 0 except at one probe
+    query, so dRPB[h] is nonzero only on that query's L x L window cells and a zeroed, moved or
+    sign-flipped cell (the corner cells get a single term) fails.  The four corner queries hit
+    the four corner cells of the table."""
+    import torch
+    import oracle
+    import paper_2204_07143_b200 as na2d
+    from na2d_inputs import bf16_round
+    H, W, d = 20, 37, 32
+    T = 2 * L - 1
+    probes = [(0, 0), (0, W - 1), (H - 1, 0), (H - 1, W - 1), (H // 2, W // 2), (1, W - 2), (L // 2 + 1, 2)]
+    heads = len(probes)
+    g = np.random.default_rng(100 + L)
+    q, k, v = (bf16_round(g.standard_normal((1, heads, H, W, d)).astype(np.float32)) for _ in range(3))
+    dout = np.zeros_like(q)
+    for h, (i, j) in enumerate(probes):
+        dout[0, h, i, j] = bf16_round(g.standard_normal(d).astype(np.float32))
+    rpb = (g.standard_normal((heads, T, T)) * np.sqrt(d)).astype(np.float32)
+    scale = d ** -0.5
+    ref = oracle.na2d_backward(q, k, v, rpb, dout, L, scale)
+    tq, tk, tv, tdo = (torch.from_numpy(x).cuda().bfloat16() for x in (q, k, v, dout))
+    trpb = torch.from_numpy(rpb).cuda()
+    out, lse = na2d.forward(tq, tk, tv, trpb, L, scale)
+    drpb = na2d.backward(tq, tk, tv, trpb, out, lse, tdo, L, scale)[3].cpu().numpy()
+    for h, (i, j) in enumerate(probes):
+        si, sj = oracle.window_start(i, H, L), oracle.window_start(j, W, L)
+        mask = np.zeros((T, T), bool)
+        mask[si - i + L - 1:si - i + 2 * L - 1, sj - j + L - 1:sj - j + 2 * L - 1] = True
+        assert np.all(drpb[h][~mask] == 0.0), f"probe {h}: cells outside the window written"
+        assert np.all(ref["drpb"][h][~mask] == 0.0)
+        np.testing.assert_allclose(drpb[h], ref["drpb"][h], rtol=1e-3, atol=1e-5, err_msg=f"probe {h} at {(i, j)}")
+    corners = {(0, 0): (T - 1, T - 1), (0, W - 1): (T - 1, 0), (H - 1, 0): (0, T - 1), (H - 1, W - 1): (0, 0)}
+    for h, (i, j) in enumerate(probes[:4]):
+        a, c = corners[(i, j)]
+        assert abs(ref["drpb"][h, a, c]) > 1e-4 and np.sign(drpb[h, a, c]) == np.sign(ref["drpb"][h, a, c])
+
+
 @pytest.mark.parametrize("dtype", ["bf16", "f32", "f16"])
 def test_row_band(dtype):
     """Band call (global coordinates) == oracle band call, incl. dk/dv partials."""
@@ -115,6 +163,8 @@ def test_row_band(dtype):
 def test_baseline_configs_full_size(name):
     """Every BASELINE.json config at full size, fwd + bwd, all outputs element by element
     (the oracle runs on all host cores)."""
+    # north_star "no other paths": every BASELINE config must run on the tcgen05 kernels
+    assert family(CONFIGS[name]) == ("tcgen05", "tcgen05"), family(CONFIGS[name])
     rep = check(CONFIGS[name], "bf16")
     print(name, {k: f"{e:.2e}/{t:.1e}" for k, (e, t) in rep.items()})
 
@@ -125,6 +175,7 @@ def test_config1_fp32():
 
 def test_config2_fp16_full_size():
     """fp16 I/O (NA2D_F16) on the same tcgen05 kernels at the stage-1 configuration."""
+    assert family(CONFIGS["cfg2_nat_tiny_s1"], "f16") == ("tcgen05", "tcgen05")
     rep = check(CONFIGS["cfg2_nat_tiny_s1"], "f16")
     print("cfg2 f16", {k: f"{e:.2e}/{t:.1e}" for k, (e, t) in rep.items()})
 

@@ -9,8 +9,11 @@ from tests.parity import compare, tolerance
 def test_tolerances():
     r = np.array([0.5, -3.0])
     assert tolerance("out", r, "bf16") == 2e-2
-    assert tolerance("drpb", np.array([50.0]), "bf16") == pytest.approx(1.0)
-    assert tolerance("drpb", np.array([0.1]), "bf16") == 2e-2
+    # dRPB: literal 2e-2 on short reductions (small maps, config 1), 1e-3 relative on long ones
+    assert tolerance("drpb", np.array([50.0]), "bf16") == 2e-2
+    assert tolerance("drpb", np.array([50.0]), "bf16", terms=64) == 2e-2
+    assert tolerance("drpb", np.array([50.0]), "bf16", terms=401408) == pytest.approx(5e-2)
+    assert tolerance("drpb", np.array([0.1]), "bf16", terms=401408) == pytest.approx(1e-3)
     assert tolerance("dq", np.array([7.0]), "f32") == pytest.approx(7e-4)
     assert tolerance("dq", np.array([0.5]), "f32") == pytest.approx(1e-4)
 
@@ -30,3 +33,17 @@ def test_fault_injection_is_caught():
         compare(nan, ref, "bf16")
     with pytest.raises(AssertionError):
         compare({"out": ref["out"][:1]}, {"out": ref["out"]}, "bf16")
+
+
+def test_drpb_bound_follows_problem_size():
+    """compare() reads B*H*W from the 5-D reference output: a dRPB error of 2.5e-2 fails on a
+    small map (literal 2e-2) and passes on a long reduction with ||dRPB|| = 50 (5e-2)."""
+    g = np.random.default_rng(1)
+    for (B, H, W), ok in [((1, 8, 8), False), ((128, 56, 56), True)]:
+        ref = {"out": np.zeros((B, 1, H, W, 1)), "drpb": np.full((1, 3, 3), 50.0)}
+        got = {"out": ref["out"], "drpb": ref["drpb"] + 2.5e-2}
+        if ok:
+            compare(got, ref, "bf16")
+        else:
+            with pytest.raises(AssertionError, match="drpb"):
+                compare(got, ref, "bf16")
