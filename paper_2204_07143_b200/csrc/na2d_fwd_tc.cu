@@ -12,24 +12,25 @@
 //     S_s = Q_s K[rb_s..]^T   (M=64, N=NSUB, K=32)   tcgen05.mma SS -> TMEM [0, NSUB)
 //     O_s = P_s V[rb_s..]     (M=64, N=32, K=NSUB)   tcgen05.mma TS (P from TMEM)
 // Softmax.  TMEM lane quarter q holds the 4 x 4 query block at tile columns [4q, 4q+4) of both
-// sub-tiles; the union of its windows is (4+L-1) rows x (4+L-1) columns of S (loaded as L+5
-// even-aligned columns; the exponentials skip the two outside the union).  Per element pair, in
-// packed fp32x2 arithmetic: x = s*scale*log2e + T[cell], T a shared-memory table of the head's
-// relative positional bias B[h][p-i+L-1][q-j+L-1] pre-multiplied by scale*log2e, with
-// -inf outside the query's own window (one table per column-clamp class, plus an all -inf row for
-// rows outside the window; two copies shifted by one column so every lane reads 8-byte aligned
-// pairs).  Exact two-pass softmax (the whole window sits in one tile): pass 1 computes x and the
-// row max (FMNMX3) and stores x compacted to 12 columns per union row over consumed S columns;
-// pass 2 writes P = exp2(x - max) as bf16 pairs in place, one union row pair at a time, each pair
-// released at once to the PV MMAs (which accumulate O in the columns the compaction freed), so
-// PV overlaps pass 2.
-// Pipeline.  Persistent CTAs (one per SM), contiguous head-major tile ranges.  Warp 8: tile
-// descriptions + TMA (3-stage ring); warp 9: MMA issue (QK of tile t, then PV of tile t-1 pair by
-// pair); warps 0-3 and 4-7: two softmax + epilogue groups that ping-pong between two TMEM slots
-// of 256 columns.
+// sub-tiles (lanes 0-15: sub-tile 0, lanes 16-31: sub-tile 1); relative to each sub-tile's own halo
+// base the union of the block's windows is the same (4+L-1) x (4+L-1) keys, so one warp serves
+// both lane halves with the plain 32x32b TMEM shapes, one thread per query.  The union rows are
+// split between two warps per quarter; each thread loads its rows' S (L+5 even-aligned columns,
+// one wait), keeps x = s*scale*log2e + T in registers (packed fp32x2 FFMA2), T a shared-memory
+// table of the head's relative positional bias B[h][p-i+L-1][q-j+L-1] pre-multiplied by
+// scale*log2e, with -inf outside the query's own window (one table per column-clamp class, an
+// all -inf row, two copies shifted by one column so every row read is 8-byte aligned).  Exact
+// softmax (the whole window is in one tile): row max and sum are combined across the two warps
+// through shared memory; P = exp2(x - max) goes to TMEM as bf16 pairs over consumed S columns
+// (each P row zeroed, then its union span written), and the PV MMAs accumulate O.
+// Pipeline.  Persistent CTAs (one per SM), contiguous head-major tile ranges.  Warp 16: tile
+// descriptions + Q/K TMA (3-stage ring); warp 18: V TMA (3-stage ring); warp 17: QK issue;
+// warp 19: PV issue; warps 0-7 and 8-15: softmax + epilogue of the two TMEM slots (alternating
+// tiles).  Waits use mbarrier try_wait with a suspend-time hint (no spin loops).
 #include <math.h>
 
 #include <mutex>
+#include <type_traits>
 
 #include "na2d_internal.cuh"
 #include "na2d_profile.cuh"
@@ -45,53 +46,56 @@ namespace {
 using namespace sm100;
 using namespace tc;
 
-constexpr int kStagesQK = 3;      // Q + K halo ring (released when the QK MMAs complete)
-constexpr int kStagesV = 3;       // V halo ring (released when the PV MMAs complete)
-constexpr int kTInfo = 8;         // tile-description ring (>= 5: see the producer)
-constexpr int kThreads = 640;     // 20 warps
-// The SM sub-partition scheduler favours the highest warp id among eligible warps: the producer and
-// MMA-issue warps take the two highest ids so the busy elementwise warps sharing their
-// sub-partitions (warp % 4) never delay a TMA or MMA issue.
-constexpr int kProducerWarp = 16, kMmaWarp = 17, kProducerVWarp = 18, kPvWarp = 19;
-// O accumulators outside both S slots, shared by the two slots' tiles: the next QK of a slot waits
-// only for that slot's PV MMAs (not for its epilogue), and PV of tile t waits for the epilogue
-// of tile t - 1 (which precedes it by half a slot cycle)
-#ifndef NA2D_FWD_SHARED_O
-#define NA2D_FWD_SHARED_O 1
+// waits of the issuing and elementwise warps (NA2D_FWD_WAIT=2: try_wait with a suspend-time hint)
+#if defined(NA2D_FWD_WAIT) && NA2D_FWD_WAIT == 2
+__device__ __forceinline__ void wait_bar(uint64_t *bar, uint32_t parity) { mbar_wait_hint(bar, parity); }
+#else
+__device__ __forceinline__ void wait_bar(uint64_t *bar, uint32_t parity) { mbar_wait(bar, parity); }
 #endif
+
+constexpr int kStagesQK = 2;      // Q + K halo ring (released when the QK MMAs complete)
+constexpr int kStagesV = 2;       // V halo ring (released when the PV MMAs complete)
+constexpr int kTInfo = 8;         // tile-description ring (>= 5: see the producer)
+constexpr int kThreads = 640;     // 20 warps: 16 elementwise (two groups of 8), 4 producer / MMA-issue
+// The SM sub-partition scheduler favours the highest warp id among eligible warps: the producer and
+// MMA-issue warps take the highest ids so the busy elementwise warps sharing their sub-partitions
+// (warp % 4) never delay a TMA or MMA issue.
+constexpr int kProducerWarp = 16, kMmaWarp = 17, kProducerVWarp = 18, kPvWarp = 19;
 
 template <int L>
 struct Cfg {
-  static constexpr int HR = kTQH + L - 1;      // halo rows
-  static constexpr int UR = 4 + L - 1;         // union rows per sub-tile
-  static constexpr int PAIRS = UR / 2;         // union row pairs (3 PV K-steps each)
-  static constexpr int NSUB = UR * kHCP;       // S columns per sub-tile (keys)
-  static constexpr int P_COL = 0;              // P (bf16 pairs) aliased over consumed S
-#if NA2D_FWD_SHARED_O
-  static constexpr int SLOT = NSUB;            // TMEM columns per slot: S (then x / P)
-  static constexpr int O_COL = 2 * NSUB;       // O partial accumulators (absolute column)
-  static constexpr int OACC = (512 - O_COL) / kD < 3 ? (512 - O_COL) / kD : 3;  // independent PV chains
-  static_assert(OACC >= 1, "TMEM budget");
-#else
-  static constexpr int SLOT = 256;
-  static constexpr int O_COL = NSUB / 2;       // O partial accumulators past the compacted x / P (in the slot)
-  static constexpr int OACC = 3;
-  static_assert(O_COL + OACC * kD <= 256, "slot budget");
-#endif
-  static_assert(2 * kHCP == 3 * 16, "a union row pair is 3 PV K-steps");
-  static constexpr int KV_ROWS = HR * kHCP;
+  static constexpr int HP = kTQW + L - 1;       // halo width = row pitch of the K / V sub-tile buffers
+  static constexpr int UR = 4 + L - 1;          // halo rows of a sub-tile (4 query rows)
+  static constexpr int UH = UR / 2;             // union rows per elementwise warp (two warps per lane quarter)
+  static_assert(UR % 2 == 0, "union rows split evenly between the two warps of a quarter");
+  static constexpr int UW = L + 3;              // union width (keys) of a lane quarter's 4 x 4 query block
+  static constexpr int PROW = HP / 2;           // packed P columns per halo row
+  // keys per sub-tile: UR x HP halo keys (+2: an odd union origin loads one column past the union),
+  // padded to whole PV K-steps of 16 keys; the tail keys are zero rows of K / V
+  static constexpr int NSUB = (UR * HP + 2 + 15) / 16 * 16;
+  static constexpr int KSTEPS = NSUB / 16;
+  static constexpr int BOX_BYTES = UR * HP * kRowBytes;  // one sub-tile's TMA box
+  static constexpr int SUB_BYTES = NSUB * kRowBytes;     // one sub-tile's K or V buffer
+  static_assert(SUB_BYTES % 1024 == 0, "sub-tile buffers stay 1 KB aligned (swizzled TMA / UMMA)");
+  // TMEM: two slots (one per elementwise group) of NSUB columns: S, then P (NSUB/2 packed columns)
+  // over the consumed S; O accumulators past both, shared by the groups' alternating tiles
+  static constexpr int O_COL = 2 * NSUB;
+  static constexpr int OACC = (512 - O_COL) / kD < 4 ? (512 - O_COL) / kD : 4;  // PV chains per sub-tile
+  static_assert(OACC >= 2, "TMEM budget");
   static constexpr int Q_BYTES = 128 * kRowBytes;
-  static constexpr int KV_BYTES = KV_ROWS * kRowBytes;
-  static constexpr int QK_BYTES = Q_BYTES + KV_BYTES;
-  static_assert(QK_BYTES % 1024 == 0 && KV_BYTES % 1024 == 0, "stages must stay 1 KB aligned (swizzled TMA / UMMA)");
+  static constexpr int QK_BYTES = Q_BYTES + 2 * SUB_BYTES;
+  static constexpr int V_BYTES = 2 * SUB_BYTES;
   static constexpr int V_OFF = kStagesQK * QK_BYTES;
   static constexpr int TT = 2 * L - 1;
   static constexpr int TROWS = TT + 1;                             // + all -inf row
   static constexpr int TBL_FLOATS = L * TROWS * kTblStride;        // one table copy
-  static constexpr int TBL_OFF = V_OFF + kStagesV * KV_BYTES;      // 2 groups x 2 parity copies
-  static constexpr int TI_OFF = TBL_OFF + 4 * TBL_FLOATS * 4;
-  static constexpr int VI_OFF = TI_OFF + kTInfo * 64;                // V ring: halo row offsets
-  static constexpr int BAR_OFF = VI_OFF + kStagesV * 16;
+  static constexpr int TBL_OFF = V_OFF + kStagesV * V_BYTES;       // 2 groups x 2 parity copies
+  static constexpr int EX_OFF = TBL_OFF + 4 * TBL_FLOATS * 4;      // row max / sum exchange [2][2][4][2][32]
+  static constexpr int RB_OFF = EX_OFF + 2 * 2 * 4 * 2 * 32 * 4;   // per group: scaled RPB + window max
+  static constexpr int RB_FLOATS = 256;
+  static_assert(TT * TT + L * L <= RB_FLOATS, "RPB staging");
+  static constexpr int TI_OFF = RB_OFF + 2 * RB_FLOATS * 4;
+  static constexpr int BAR_OFF = TI_OFF + kTInfo * 64;
   static constexpr int SMEM = BAR_OFF + 320 + 1024;
   static_assert(SMEM <= 232448, "shared memory");
 };
@@ -106,14 +110,6 @@ struct FwdParams {
   long long *trace;  // debug timeline (na2d_debug_set_trace, builds with -DNA2D_TRACE) or null
 };
 
-// Tile description (ring of kTInfo), written by the Q/K producer before it arms full_qk.
-struct FTile {
-  int bh, head, i0, j0, hr0, hc0;
-  int rb[2];  // first halo row of sub-tile s (relative to hr0)
-  int uc[4];  // union origin of lane quarter q: bit 0 = first needed column odd, rest = even column
-};
-static_assert(sizeof(FTile) <= 64, "FTile");
-
 #ifdef NA2D_TRACE
 // Debug timeline: trace[(cta * kTraceTiles + it) * kTraceEv + ev] = clock64() for CTAs < 4.
 constexpr int kTraceTiles = 32, kTraceEv = 32;
@@ -125,6 +121,14 @@ __device__ __forceinline__ void trace_ev(const FwdParams &p, int it, int ev) {
 __device__ __forceinline__ void trace_ev(const FwdParams &, int, int) {}
 #endif
 
+// Tile description (ring of kTInfo), written by the Q/K producer before it arms full_qk.
+struct FTile {
+  int bh, head, i0, j0, hr0, hc0;
+  int rb[2];  // first halo row of sub-tile s (relative to hr0)
+  int uc[4];  // union origin (first needed halo column) of lane quarter q
+};
+static_assert(sizeof(FTile) <= 64, "FTile");
+
 template <int L, bool F16>
 __global__ void __launch_bounds__(kThreads, 1)
     na2d_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -132,23 +136,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   using C = Cfg<L>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-  float *tables = (float *)(smem + C::TBL_OFF);
   FTile *tinfo = (FTile *)(smem + C::TI_OFF);
-  int *vinfo = (int *)(smem + C::VI_OFF);  // [V slot][2]: rb of the two sub-tiles
   uint64_t *bars = (uint64_t *)(smem + C::BAR_OFF);
   uint64_t *full = bars, *empty = bars + kStagesQK;                     // Q/K ring
   uint64_t *full_v = bars + 2 * kStagesQK, *empty_v = full_v + kStagesV;  // V ring
-  uint64_t *s_full = full_v + 2 * kStagesV, *o_full = s_full + 2, *tmem_free = s_full + 4;
-  uint64_t *p_pair = s_full + 6;  // [slot][pair]: union row pair of P written by the 4 warps
+  uint64_t *s_full = full_v + 2 * kStagesV;  // [group]: S of the group's tile in its slot
+  uint64_t *slot_free = s_full + 2;          // [group]: PV of the slot's tile complete (P read)
+  uint64_t *p_ready = s_full + 4;            // [group]: P written by the group's 8 warps
+  uint64_t *o_full = s_full + 6;             // [group]: PV of the group's tile complete
+  uint64_t *o_free = s_full + 8;             // shared O read out by the epilogue of the previous tile
   // tile description it % kTInfo written (the elementwise warps must not wait on full[]: by the time
   // a slow group gets there, full[] may already have completed the next phase of its stage)
-  uint64_t *ti_full = p_pair + 2 * C::PAIRS;
-  uint64_t *o_free = ti_full + kTInfo;  // shared O read out by the epilogue of the previous tile
-  uint32_t *tmem_slot = (uint32_t *)(o_free + 1);
+  uint64_t *ti_full = s_full + 9;
+  uint32_t *tmem_slot = (uint32_t *)(ti_full + kTInfo);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int t_begin = (int)((long)p.num_tiles * blockIdx.x / gridDim.x);
   const int t_end = (int)((long)p.num_tiles * (blockIdx.x + 1) / gridDim.x);
+  const int ntile = t_end - t_begin;
   const int q_end = p.q_row0 + p.q_rows;
 
   if (warp == kProducerWarp && lane == 0) {
@@ -161,11 +166,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&full_v[s], 1);
       mbar_init(&empty_v[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&s_full[s], 1);
-      mbar_init(&o_full[s], 1);
-      mbar_init(&tmem_free[s], NA2D_FWD_SHARED_O ? 1 : 8);  // PV commit / both lane-half groups' epilogue
-      for (int k = 0; k < C::PAIRS; ++k) mbar_init(&p_pair[s * C::PAIRS + k], 8);
+    for (int g = 0; g < 2; ++g) {
+      mbar_init(&s_full[g], 1);
+      mbar_init(&slot_free[g], 1);
+      mbar_init(&p_ready[g], 8);
+      mbar_init(&o_full[g], 1);
     }
     mbar_init(o_free, 8);
     fence_barrier_init();
@@ -174,13 +179,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&tm_v);
   }
   if (warp == kProducerWarp) tmem_alloc<512>(tmem_slot);
-#ifdef NA2D_TRACE
-  if (threadIdx.x == 0 && p.trace) {  // per-CTA wall-clock span (load balance)
-    uint64_t gt;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-    p.trace[16384 + 2 * blockIdx.x] = (long long)gt;
+  // the K / V sub-tile buffer rows past the TMA box (keys [UR*HP, NSUB)) are read by the MMAs but
+  // never loaded: zero them once (S / O stay finite there; P is zero for those keys)
+  for (int e = threadIdx.x; e < (kStagesQK + kStagesV) * 2 * (C::SUB_BYTES - C::BOX_BYTES) / 16; e += kThreads) {
+    constexpr int per = (C::SUB_BYTES - C::BOX_BYTES) / 16;
+    const int buf = e / per, o = e % per;
+    uint8_t *base = buf < 2 * kStagesQK ? smem + (buf >> 1) * C::QK_BYTES + C::Q_BYTES + (buf & 1) * C::SUB_BYTES
+                                        : smem + C::V_OFF + (buf - 2 * kStagesQK) * C::SUB_BYTES;
+    *(uint4 *)(base + C::BOX_BYTES + o * 16) = make_uint4(0, 0, 0, 0);
   }
-#endif
+  fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -190,15 +198,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == kProducerWarp) {
     // ================= producer (whole warp converged; one elected thread writes the tile
-    // description and issues the TMA loads: Q 4x4 blocks, K / V halo).  Head-major tile order
-    // (consecutive tiles share the head: bias table rebuilds are rare), stepped incrementally.
+    // description and issues the TMA loads: Q 4x4 blocks, the K halo rows of each sub-tile).
+    // Head-major tile order (consecutive tiles share the head: bias table rebuilds are rare).
     const int per = p.tiles_h * p.tiles_w;
     const int u0 = t_begin / per, rem0 = t_begin - u0 * per;
     int h = u0 / p.B, b = u0 - h * p.B, tr = rem0 / p.tiles_w, tcol = rem0 - tr * p.tiles_w;
-    for (int it = 0; it < t_end - t_begin; ++it) {
+    for (int it = 0; it < ntile; ++it) {
       const int s = it % kStagesQK;
-      // full[s] re-arms once QK(it - 3) has completed; the description slot it % kTInfo was last read
-      // (tile it - kTInfo) before that tile's epilogue, which precedes QK(it - kTInfo + 2) <= QK(it - 3)
+      // full[s] re-arms once QK(it - kStagesQK) has completed; the description slot it % kTInfo was
+      // last read (tile it - kTInfo) before that tile's S was loaded, long before
       mbar_wait_sleep(&empty[s], ((it / kStagesQK) & 1) ^ 1, 1024);
       if (lane == 0) trace_ev(p, it, 0);
       const int bh = b * p.heads + h;
@@ -218,14 +226,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int q = 0; q < 4; ++q) ti->uc[q] = wstart(min(j0 + 4 * q, p.W - 1), p.W, L) - hc0;
         mbar_arrive(&ti_full[it % kTInfo]);  // release: the description above is visible to its waiters
         uint8_t *st = smem + s * C::QK_BYTES;
-        mbar_expect_tx(&full[s], C::QK_BYTES);
+        mbar_expect_tx(&full[s], C::Q_BYTES + 2 * C::BOX_BYTES);
         // Q: sub-tile sb, quarter qb -> 16 rows = 4x4 block (rows i0+4sb.., cols j0+4qb..)
 #pragma unroll
         for (int sb = 0; sb < 2; ++sb)
 #pragma unroll
           for (int qb = 0; qb < 4; ++qb)
             tma_load_4d(st + (64 * sb + 16 * qb) * kRowBytes, &tm_q, &full[s], 0, j0 + 4 * qb, i0 - p.q_row0 + 4 * sb, bh);
-        tma_load_4d(st + C::Q_BYTES, &tm_k, &full[s], 0, hc0, hr0 - p.kv_row0, bh);
+#pragma unroll
+        for (int sb = 0; sb < 2; ++sb)
+          tma_load_4d(st + C::Q_BYTES + sb * C::SUB_BYTES, &tm_k, &full[s], 0, hc0, hr0 + ti->rb[sb] - p.kv_row0, bh);
       }
       __syncwarp();
       if (++tcol == p.tiles_w) {
@@ -240,23 +250,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == kProducerVWarp) {
-    // ================= V producer: the V halo of tile it into ring slot it % kStagesV once PV of
-    // tile it - kStagesV has completed (same head-major incremental tile walk as the Q/K producer)
+    // ================= V producer: the V halo rows of each sub-tile of tile it into ring slot
+    // it % kStagesV once PV of tile it - kStagesV has completed
     const int per = p.tiles_h * p.tiles_w;
     const int u0 = t_begin / per, rem0 = t_begin - u0 * per;
     int h = u0 / p.B, b = u0 - h * p.B, tr = rem0 / p.tiles_w, tcol = rem0 - tr * p.tiles_w;
-    for (int it = 0; it < t_end - t_begin; ++it) {
+    for (int it = 0; it < ntile; ++it) {
       const int s = it % kStagesV;
       mbar_wait_sleep(&empty_v[s], ((it / kStagesV) & 1) ^ 1, 1024);
       const int bh = b * p.heads + h;
       const int i0 = p.q_row0 + tr * kTQH, j0 = tcol * kTQW;
       if (elect_one()) {
-        const int hr0 = wstart(i0, p.H, L);
-        vinfo[2 * s] = wstart(min(i0, q_end - 1), p.H, L) - hr0;
-        vinfo[2 * s + 1] = wstart(min(i0 + 4, q_end - 1), p.H, L) - hr0;
-        mbar_expect_tx(&full_v[s], C::KV_BYTES);
-        tma_load_4d(smem + C::V_OFF + s * C::KV_BYTES, &tm_v, &full_v[s], 0, wstart(j0, p.W, L),
-                    wstart(i0, p.H, L) - p.kv_row0, bh);
+        mbar_expect_tx(&full_v[s], 2 * C::BOX_BYTES);
+#pragma unroll
+        for (int sb = 0; sb < 2; ++sb)
+          tma_load_4d(smem + C::V_OFF + s * C::V_BYTES + sb * C::SUB_BYTES, &tm_v, &full_v[s], 0, wstart(j0, p.W, L),
+                      wstart(min(i0 + 4 * sb, q_end - 1), p.H, L) - p.kv_row0, bh);
       }
       __syncwarp();
       if (++tcol == p.tiles_w) {
@@ -272,265 +281,232 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == kMmaWarp) {
     // ================= QK issuer (whole warp converged, one elected thread issues): S of tile it
-    // into TMEM slot it & 1 once its Q / K have landed and the slot's previous epilogue has read O.
-    // The PV MMAs have their own issuing warp, so neither stream waits behind the other's
-    // dependencies.  Shared-memory descriptors are built once per stage and advanced by
-    // (byte offset >> 4).
+    // into slot it & 1 once its Q / K have landed and the slot's previous PV has read its P
     constexpr uint32_t idesc_qk = idesc_el<F16>(64, C::NSUB, false);
-    for (int it = 0; it < t_end - t_begin; ++it) {
-      const int s = it % kStagesQK, slot = it & 1;
-      mbar_wait(&full[s], (it / kStagesQK) & 1);
-      const int rb0 = tinfo[it % kTInfo].rb[0], rb1 = tinfo[it % kTInfo].rb[1];
+    for (int it = 0; it < ntile; ++it) {
+      const int s = it % kStagesQK, g = it & 1;
+      wait_bar(&full[s], (it / kStagesQK) & 1);
       if (lane == 0) trace_ev(p, it, 1);
-      mbar_wait(&tmem_free[slot], ((it >> 1) & 1) ^ 1);
+      wait_bar(&slot_free[g], ((it >> 1) & 1) ^ 1);
       if (lane == 0) trace_ev(p, it, 2);
       tc_fence_after();
       const uint64_t dq = sdesc_sw64(smem_u32(smem + s * C::QK_BYTES));
-      const uint64_t dk = dq + (C::Q_BYTES >> 4);
-      const uint64_t dk0 = dk + ((rb0 * kHCP * kRowBytes) >> 4), dk1 = dk + ((rb1 * kHCP * kRowBytes) >> 4);
-      const uint32_t d0 = tmem + slot * C::SLOT, d1 = d0 + ((uint32_t)16 << 16);
+      const uint64_t dk0 = dq + (C::Q_BYTES >> 4), dk1 = dk0 + (C::SUB_BYTES >> 4);
+      const uint32_t d0 = tmem + g * C::NSUB, d1 = d0 + ((uint32_t)16 << 16);
       if (elect_one()) {  // two independent accumulation chains (sub-tiles) interleaved
         mma_ss(d0, dq, dk0, idesc_qk, 0);
         mma_ss(d1, dq + (4096 >> 4), dk1, idesc_qk, 0);
         mma_ss(d0, dq + (32 >> 4), dk0 + (32 >> 4), idesc_qk, 1);
         mma_ss(d1, dq + ((4096 + 32) >> 4), dk1 + (32 >> 4), idesc_qk, 1);
-        mma_commit(&s_full[slot]);
+        mma_commit(&s_full[g]);
         mma_commit(&empty[s]);
       }
       __syncwarp();
     }
   } else if (warp == kPvWarp) {
-    // ================= PV issuer: O of tile it (slot it & 1) one union row pair at a time as the
-    // elementwise warps release it (the PV overlaps pass 2)
+    // ================= PV issuer: O of tile it from P in slot it & 1 once its group wrote it and the
+    // epilogue of tile it - 1 (the other group) has read the shared O accumulators
     constexpr uint32_t idesc_pv = idesc_el<F16>(64, kD, true);
-    for (int it = 0; it < t_end - t_begin; ++it) {
-      const int s = it % kStagesV, slot = it & 1;
-      mbar_wait(&full_v[s], (it / kStagesV) & 1);
-      const int rb0 = vinfo[2 * s], rb1 = vinfo[2 * s + 1];
-      const uint64_t dv = sdesc_sw64(smem_u32(smem + C::V_OFF + s * C::KV_BYTES));
-      const uint64_t dv0 = dv + ((rb0 * kHCP * kRowBytes) >> 4), dv1 = dv + ((rb1 * kHCP * kRowBytes) >> 4);
-      const uint32_t b0 = tmem + slot * C::SLOT, b1 = b0 + ((uint32_t)16 << 16);
-#if NA2D_FWD_SHARED_O
+    for (int it = 0; it < ntile; ++it) {
+      const int s = it % kStagesV, g = it & 1;
+      wait_bar(&full_v[s], (it / kStagesV) & 1);
+      const uint64_t dv0 = sdesc_sw64(smem_u32(smem + C::V_OFF + s * C::V_BYTES)), dv1 = dv0 + (C::SUB_BYTES >> 4);
+      const uint32_t b0 = tmem + g * C::NSUB, b1 = b0 + ((uint32_t)16 << 16);
       const uint32_t o0 = tmem + C::O_COL, o1 = o0 + ((uint32_t)16 << 16);
-#else
-      const uint32_t o0 = b0 + C::O_COL, o1 = b1 + C::O_COL;
-#endif
-      // fully unrolled: every descriptor / TMEM address below is the tile's base + an immediate, so
-      // each pair's issue is a short independent burst (no dependent address chain per pair)
-#pragma unroll
-      for (int k = 0; k < C::PAIRS; ++k) {
-#if NA2D_FWD_SHARED_O
-        if (k == 0 && it > 0) mbar_wait(o_free, (it - 1) & 1);  // epilogue of tile it - 1 read O
-#endif
-        mbar_wait(&p_pair[slot * C::PAIRS + k], (it >> 1) & 1);
-        if (lane == 0) trace_ev(p, it, 19 + k);
-        tc_fence_after();
-        // 2 sub-tiles x kOAcc partial accumulators = independent MMA chains, interleaved
-        constexpr uint32_t acc = 1;
-        if (elect_one()) {
-#pragma unroll
-          for (int k3 = 0; k3 < 3; ++k3) {
-            const int ks = 3 * k + k3;
-            const uint32_t voff = (ks * 16 * kRowBytes) >> 4, oc = (ks % C::OACC) * kD;
-            const uint32_t a = ks >= C::OACC ? acc : 0u;
-            mma_ts(o0 + oc, b0 + C::P_COL + ks * 8, dv0 + voff, idesc_pv, a);
-            mma_ts(o1 + oc, b1 + C::P_COL + ks * 8, dv1 + voff, idesc_pv, a);
-          }
-          if (k == C::PAIRS - 1) {
-            mma_commit(&o_full[slot]);
-            mma_commit(&empty_v[s]);
-#if NA2D_FWD_SHARED_O
-            mma_commit(&tmem_free[slot]);  // P read: the slot may take the next QK
-#endif
-          }
-        }
-        __syncwarp();
-      }
+      wait_bar(&p_ready[g], (it >> 1) & 1);
       if (lane == 0) trace_ev(p, it, 3);
+      if (it > 0) wait_bar(o_free, (it - 1) & 1);
+      if (lane == 0) trace_ev(p, it, 4);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int ks = 0; ks < C::KSTEPS; ++ks) {
+          const uint32_t voff = (ks * 16 * kRowBytes) >> 4, oc = (ks % C::OACC) * kD;
+          const uint32_t a = ks >= C::OACC ? 1u : 0u;
+          mma_ts(o0 + oc, b0 + ks * 8, dv0 + voff, idesc_pv, a);
+          mma_ts(o1 + oc, b1 + ks * 8, dv1 + voff, idesc_pv, a);
+        }
+        mma_commit(&o_full[g]);
+        mma_commit(&empty_v[s]);
+        mma_commit(&slot_free[g]);
+      }
+      __syncwarp();
     }
   } else {
-    // ================= softmax + epilogue: 4 groups of 4 warps.  Group g works on TMEM slot g >> 1
-    // (tiles it with it & 1 == slot) and on sub-tile / TMEM lane half h = g & 1 of those tiles; its
-    // warp of lane quarter q reads the 16 lanes [32q + 16h, +16) with the .16x32bx2 shapes, so two
-    // threads share a query: thread t handles query (t & 15) and union columns [6 (t >> 4), +6).
-    const int grp = warp >> 2, slot = grp >> 1, hh = grp & 1;
-    const int quarter = warp & 3;
-    const int hf = lane >> 4, ql = lane & 15, r = ql >> 2, c = ql & 3;
-    float *tbl = tables + slot * 2 * C::TBL_FLOATS;  // the slot's two parity copies (both halves share)
-    const int stid = threadIdx.x - slot * 256;       // 0..255 within the slot's two groups
+    // ================= softmax + epilogue: two groups of 8 warps alternate tiles (group g = tiles
+    // with it & 1 == g, TMEM slot g).  In a group, warp w: lane quarter q = w & 3, union-row half
+    // hf = (w >> 2) & 1.  One thread per query: lane l < 16 is query l of the quarter's 4x4 block of
+    // sub-tile 0, lane l >= 16 of sub-tile 1 (their S rows are relative to their own halo base rb_s,
+    // so both halves share the union columns).  S of the warp's UH union rows goes to registers (one
+    // wait), the two warps of a quarter combine row max and sum through shared memory, and P is
+    // written row by row over the consumed S.
+    // Softmax with an upper-bound shift: m = max(raw s over the union) * scale*log2e + the bias max
+    // over the query's window (per window class, from a small table); m >= the true row max, so every
+    // exp2(x - m) <= 1, and P = exp2(x - m) / sum is exact up to fp32 rounding unless m overshoots by
+    // > 60 (log2) -- detected by sum < 2^-60, then the rows are redone with the exact max.
+    const int g = warp >> 3, hf = (warp >> 2) & 1, quarter = warp & 3;
+    const int sub = lane >> 4, r = (lane >> 2) & 3, c = lane & 3;
+    const int u0 = hf * C::UH;  // first union row of this warp
+    float *tbl = (float *)(smem + C::TBL_OFF) + g * 2 * C::TBL_FLOATS;  // the group's two parity copies
+    float *ex_max = (float *)(smem + C::EX_OFF) + g * 512;             // [quarter][half][lane]
+    float *ex_sum = ex_max + 256;
+    float *rbs = (float *)(smem + C::RB_OFF) + g * C::RB_FLOATS;       // scaled RPB, then window maxima
+    float *tmx = rbs + C::TT * C::TT;
+    const int stid = threadIdx.x - g * 256;
     const int Lh = wlen(p.H, L), Lw = wlen(p.W, L);
     const float2 sl2x2 = make_float2(p.scale_log2, p.scale_log2);
-    const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32 + 16 * hh) << 16) + slot * C::SLOT;
-#if NA2D_FWD_SHARED_O
-    const uint32_t o_addr = tmem + ((uint32_t)(quarter * 32 + 16 * hh) << 16) + C::O_COL;
-#else
-    const uint32_t o_addr = lane_addr + C::O_COL;
-#endif
+    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+    const uint32_t slot_base = lane_base + g * C::NSUB;
+    const int ex_me = (quarter * 2 + hf) * 32 + lane, ex_other = ex_me + (hf ? -32 : 32);
+    const uint32_t bar_q = 3 + g * 4 + quarter;  // named barrier of the quarter's two warps
     int cur_head = -1;
-    for (int it = slot; it < t_end - t_begin; it += 2) {
+    for (int it = g; it < ntile; it += 2) {
       const uint32_t ph = (it >> 1) & 1;
-      // tile description of tile it: its ring slot is rewritten (tile it + 8) only after QK(it + 5),
-      // which needs the epilogue of tile it + 3, whose PV is issued after PV(it + 2), i.e. after this
-      // group has read the description of tile it (and processed tile it + 2)
-      mbar_wait(&ti_full[it % kTInfo], (it / kTInfo) & 1);
+      wait_bar(&ti_full[it % kTInfo], (it / kTInfo) & 1);
       const FTile &ti = tinfo[it % kTInfo];
       const int bh = ti.bh, h = ti.head, i0 = ti.i0, j0 = ti.j0, hr0 = ti.hr0, hc0 = ti.hc0;
-      const int rb = ti.rb[hh], ucr = ti.uc[quarter];
-      if (h != cur_head) {  // (re)build the slot's masked, pre-scaled bias tables (two parity copies:
-        // copy x holds column b at kTblOff + x + b, so every thread's row start is 8-byte aligned)
-        named_bar_sync(1 + slot, 256);
-        for (int e = stid; e < 2 * C::TBL_FLOATS; e += 256) {
-          const int x = e >= C::TBL_FLOATS, e2 = e - x * C::TBL_FLOATS;
-          const int dc = e2 / (C::TROWS * kTblStride);
-          const int rr = (e2 / kTblStride) % C::TROWS;
-          const int cb = e2 % kTblStride - kTblOff - x;
-          float v = -INFINITY;
-          if (rr < C::TT && cb >= dc && cb < dc + Lw) v = p.rpb ? __ldg(&p.rpb[(h * C::TT + rr) * C::TT + cb]) * p.scale_log2 : 0.f;
-          tbl[e] = v;
+      const int ucr = __shfl_sync(0xffffffffu, ti.uc[quarter], 0);
+      const int rb = ti.rb[sub];
+      if (h != cur_head) {  // (re)build the group's masked, pre-scaled bias tables (two parity copies:
+        // copy x holds column b at kTblOff + x + b, so every thread's row start is 8-byte aligned) and
+        // the bias maximum over each window class (dr, dc)
+        named_bar_sync(1 + g, 256);
+        for (int e = stid; e < C::TT * C::TT; e += 256) rbs[e] = p.rpb ? __ldg(&p.rpb[h * C::TT * C::TT + e]) * p.scale_log2 : 0.f;
+        named_bar_sync(1 + g, 256);
+        for (int row = stid; row < 2 * L * C::TROWS; row += 256) {  // one table row per thread
+          const int x = row / (L * C::TROWS), dc = row / C::TROWS % L, rr = row % C::TROWS;
+          float *dst = tbl + row * kTblStride;
+          const float *src = rbs + rr * C::TT;
+          const bool rv = rr < C::TT;
+#pragma unroll 4
+          for (int e = 0; e < kTblStride; ++e) {
+            const int cb = e - kTblOff - x;
+            dst[e] = (rv && cb >= dc && cb < dc + Lw) ? src[cb] : -INFINITY;
+          }
         }
-        named_bar_sync(1 + slot, 256);
+        for (int e = stid; e < L * L; e += 256) {
+          const int dr = e / L, dc = e % L;
+          float m = -INFINITY;
+          for (int a = dr; a < dr + Lh; ++a)
+            for (int b2 = dc; b2 < dc + Lw; ++b2) m = fmaxf(m, rbs[a * C::TT + b2]);
+          tmx[e] = m;
+        }
+        named_bar_sync(1 + g, 256);
         cur_head = h;
       }
       // this thread's query and window geometry
-      const int i = i0 + 4 * hh + r, j = j0 + 4 * quarter + c;
+      const int i = i0 + 4 * sub + r, j = j0 + 4 * quarter + c;
       const int ic = min(i, q_end - 1), jc = min(j, p.W - 1);
       const int si = wstart(ic, p.H, L), sj = wstart(jc, p.W, L);
-      const int uc = ucr & ~1;                                       // even union origin (warp-uniform)
       const int dc = sj - jc + L - 1;                                // column-clamp class
-      const int bcol0 = hc0 + uc - jc + L - 1;                       // bias column of union col 0
-      const int cp = bcol0 & 1;                                      // parity copy: aligned row start
-      const float *tcls = tbl + cp * C::TBL_FLOATS + dc * C::TROWS * kTblStride + kTblOff + cp + bcol0 + 6 * hf;
-
-      const bool tr = grp == 0 && quarter == 2 && lane == 0;
-      if (tr) trace_ev(p, it, 4);
-      mbar_wait(&s_full[slot], ph);
-      if (tr) trace_ev(p, it, 5);
-      tc_fence_after();
-      // ---- pass 1 (union row pair k per step, software-pipelined): x = s*scale*log2e + T in packed
-      // fp32x2 over this thread's 6 columns; row max (FMNMX3); x stored compacted: union row u at
-      // columns [12u, 12u+12) over consumed S columns, freeing [NSUB/2, 256) for O during pass 2
-      float mx = -INFINITY;
-      {
-        uint32_t S[2][16];  // [buffer][row a: 0-7 | row b: 8-15] (columns 6, 7 of each row unused)
-        float2 T[2][6];     // bias pairs: row a 0-2, row b 3-5
-        auto load_tbl = [&](int u, float2(&t)[6]) {
-          const int pr = hr0 + rb + u;  // key row of union row u
-          const bool rva = (unsigned)(pr - si) < (unsigned)Lh, rvb = (unsigned)(pr + 1 - si) < (unsigned)Lh;
-          const float2 *ta = (const float2 *)(tcls + (rva ? pr - ic + L - 1 : C::TT) * kTblStride);
-          const float2 *tb = (const float2 *)(tcls + (rvb ? pr + 1 - ic + L - 1 : C::TT) * kTblStride);
-#pragma unroll
-          for (int z = 0; z < 3; ++z) {
-            t[z] = ta[z];
-            t[3 + z] = tb[z];
-          }
+      const float tmax = tmx[(si - ic + L - 1) * L + dc];            // bias max over the window
+      const bool trc = g == 0 && hf == 0 && quarter == 0 && lane == 0;
+      float sum, mq;
+      // the tile's softmax for an even (ODD = 0: UW loaded columns, all in the union) or odd union
+      // origin (ODD = 1: UW + 2 columns from the even column before it; the first and last are
+      // outside the union).  The origin is per quarter (warp-uniform), and even except at borders.
+      auto softmax = [&](auto odd_tag) {
+        constexpr int ODD = decltype(odd_tag)::value;
+        constexpr int NC = C::UW + 2 * ODD, NPK = NC / 2;
+        const int uc = ucr - ODD;                                    // first loaded (even) column
+        const int bcol0 = hc0 + uc - jc + L - 1;                     // bias column of loaded col 0
+        const int cp = bcol0 & 1;                                    // parity copy: aligned row start
+        const float *tcls = tbl + cp * C::TBL_FLOATS + dc * C::TROWS * kTblStride + kTblOff + cp + bcol0;
+        auto trow = [&](int u) {  // bias row of union row u0 + u (the -inf row outside the window)
+          const int pr = hr0 + rb + u0 + u;
+          return (const float2 *)(tcls + ((unsigned)(pr - si) < (unsigned)Lh ? pr - ic + L - 1 : C::TT) * kTblStride);
         };
-        auto load_s = [&](int u, uint32_t(&d)[16]) {
-          tmem_ld_h8<6>(lane_addr + u * kHCP + uc, *reinterpret_cast<uint32_t(*)[8]>(&d[0]));
-          tmem_ld_h8<6>(lane_addr + (u + 1) * kHCP + uc, *reinterpret_cast<uint32_t(*)[8]>(&d[8]));
-        };
-        load_s(0, S[0]);
-        load_tbl(0, T[0]);
+        if (trc) trace_ev(p, it, 5);
+        wait_bar(&s_full[g], ph);
+        if (trc) trace_ev(p, it, 6);
+        tc_fence_after();
+        uint32_t sv[C::UH][NC];
 #pragma unroll
-        for (int k = 0; k < C::PAIRS; ++k) {
-          const int u = 2 * k;
-          uint32_t(&cur)[16] = S[k & 1];
-          const float2(&tc)[6] = T[k & 1];
-          tc_wait_ld();
-          if (k + 1 < C::PAIRS) {
-            load_s(u + 2, S[(k + 1) & 1]);
-            load_tbl(u + 2, T[(k + 1) & 1]);
-          }
-          float2 x[6];
+        for (int u = 0; u < C::UH; ++u) ld_row<NC>(slot_base + (u0 + u) * C::HP + uc, sv[u]);
+        tc_wait_ld();
+        float ms = -INFINITY;
 #pragma unroll
-          for (int z = 0; z < 3; ++z) {
-            x[z] = __ffma2_rn(make_float2(__uint_as_float(cur[2 * z]), __uint_as_float(cur[2 * z + 1])), sl2x2, tc[z]);
-            x[3 + z] = __ffma2_rn(make_float2(__uint_as_float(cur[8 + 2 * z]), __uint_as_float(cur[9 + 2 * z])), sl2x2,
-                                  tc[3 + z]);
-          }
-          mx = fmax3(mx, fmax3(fmax3(x[0].x, x[0].y, x[1].x), fmax3(x[1].y, x[2].x, x[2].y),
-                               fmax3(x[3].x, x[3].y, x[4].x)),
-                     fmax3(x[4].y, x[5].x, x[5].y));
-          const uint32_t xa4[4] = {__float_as_uint(x[0].x), __float_as_uint(x[0].y), __float_as_uint(x[1].x),
-                                   __float_as_uint(x[1].y)};
-          const uint32_t xa2[2] = {__float_as_uint(x[2].x), __float_as_uint(x[2].y)};
-          const uint32_t xb4[4] = {__float_as_uint(x[3].x), __float_as_uint(x[3].y), __float_as_uint(x[4].x),
-                                   __float_as_uint(x[4].y)};
-          const uint32_t xb2[2] = {__float_as_uint(x[5].x), __float_as_uint(x[5].y)};
-          tmem_st_h4<6>(lane_addr + u * 12, xa4);
-          tmem_st_h2<6>(lane_addr + u * 12 + 4, xa2);
-          tmem_st_h4<6>(lane_addr + u * 12 + 12, xb4);
-          tmem_st_h2<6>(lane_addr + u * 12 + 16, xb2);
-        }
-      }
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));  // the query's other 6 columns
-      tc_wait_st();
-      if (tr) trace_ev(p, it, 6);
-      // ---- pass 2 (row pair k per step, pipelined): P = exp2(x - max) -> bf16 pairs in place (each
-      // halo row of P zeroed, then the union span written); pair k-1 is released to the PV MMAs once
-      // pair k is computed (its stores have drained by then)
-      float2 sum2 = make_float2(0.f, 0.f);
-      const int zb = uc >> 1;  // packed column where the union span starts (warp-uniform)
-      {
-        uint32_t X[2][12];  // [buffer][row a: 0-5 | row b: 6-11]
-        auto load_x = [&](int u, uint32_t(&d)[12]) {
-          tmem_ld_h4<6>(lane_addr + u * 12, *reinterpret_cast<uint32_t(*)[4]>(&d[0]));
-          tmem_ld_h2<6>(lane_addr + u * 12 + 4, *reinterpret_cast<uint32_t(*)[2]>(&d[4]));
-          tmem_ld_h4<6>(lane_addr + u * 12 + 12, *reinterpret_cast<uint32_t(*)[4]>(&d[6]));
-          tmem_ld_h2<6>(lane_addr + u * 12 + 16, *reinterpret_cast<uint32_t(*)[2]>(&d[10]));
-        };
-        load_x(0, X[0]);
-        const float2 nm = make_float2(-mx, -mx);
-        const uint32_t z4[4] = {0u, 0u, 0u, 0u}, z2[2] = {0u, 0u};
+        for (int u = 0; u < C::UH; ++u)
 #pragma unroll
-        for (int k = 0; k < C::PAIRS; ++k) {
-          const int u = 2 * k;
-          uint32_t(&cur)[12] = X[k & 1];
-          tc_wait_ld();
-          if (k + 1 < C::PAIRS) load_x(u + 2, X[(k + 1) & 1]);
-          uint32_t pk[6];
-#pragma unroll
-          for (int z = 0; z < 6; ++z) {
-            const float2 a = __fadd2_rn(make_float2(__uint_as_float(cur[2 * z]), __uint_as_float(cur[2 * z + 1])), nm);
-            const float2 e = make_float2(ex2(a.x), ex2(a.y));
-            sum2 = __fadd2_rn(sum2, e);
-            pk[z] = pack_el<F16>(e.x, e.y);
-          }
-          if (k > 0) {
-            tc_wait_st();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&p_pair[slot * C::PAIRS + k - 1]);
-          }
-          // P row u: 12 packed columns at [12u, 12u+12) -- each half zeroes its 6, then the union span
-          // (6 packed columns from zb; this thread's 3 at zb + 3 hf)
-          const uint32_t prow = lane_addr + C::P_COL + u * (kHCP / 2);
-          tmem_st_h4<6>(prow, z4);
-          tmem_st_h2<6>(prow + 4, z2);
-          tmem_st_h4<6>(prow + 12, z4);
-          tmem_st_h2<6>(prow + 16, z2);
-          const uint32_t pa2[2] = {pk[0], pk[1]}, pb2[2] = {pk[3], pk[4]};
-          tmem_st_h2<3>(prow + zb, pa2);
-          tmem_st_h1<3>(prow + zb + 2, pk[2]);
-          tmem_st_h2<3>(prow + 12 + zb, pb2);
-          tmem_st_h1<3>(prow + 12 + zb + 2, pk[5]);
-        }
+          for (int k = ODD; k < NC - ODD; k += 2)
+            ms = ODD ? fmax3(ms, __uint_as_float(sv[u][k]), k + 1 < NC - ODD ? __uint_as_float(sv[u][k + 1]) : -INFINITY)
+                     : fmax3(ms, __uint_as_float(sv[u][k]), __uint_as_float(sv[u][k + 1]));
+        ex_max[ex_me] = ms;
+        named_bar_sync(bar_q, 64);  // also: both warps' S is in registers, P may overwrite S
+        ms = fmaxf(ms, ex_max[ex_other]);
+        if (trc) trace_ev(p, it, 7);
+        // P rows: the warp's packed rows zeroed (the second warp also the K-step padding), then each
+        // row's NPK packed union columns written at the quarter's (even) union origin
+        const uint32_t p_addr = slot_base + u0 * C::PROW;
+        if (hf == 0) st_zero<C::UH * C::PROW>(p_addr);
+        else st_zero<C::NSUB / 2 - C::UH * C::PROW>(p_addr);
         tc_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_pair[slot * C::PAIRS + C::PAIRS - 1]);
-      }
-      float sum = sum2.x + sum2.y;
-      sum += __shfl_xor_sync(0xffffffffu, sum, 16);
-      if (tr) trace_ev(p, it, 7);
-      // ---- epilogue: O / sum -> bf16 (this thread: head dims [16 hf, 16 hf + 16)), LSE
-      mbar_wait(&o_full[slot], ph);
-      if (tr) trace_ev(p, it, 8);
+        auto exp_rows = [&](float m) {
+          const float2 nm = make_float2(-m, -m);
+          float2 sum2 = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int u = 0; u < C::UH; ++u) {
+            const float2 *t = trow(u);
+            float2 tv[NPK];
+#pragma unroll
+            for (int k = 0; k < NPK; ++k) tv[k] = t[k];
+            uint32_t pk[NPK];
+#pragma unroll
+            for (int k = 0; k < NPK; ++k) {
+              const float2 xx = __ffma2_rn(make_float2(__uint_as_float(sv[u][2 * k]), __uint_as_float(sv[u][2 * k + 1])),
+                                           sl2x2, tv[k]);
+              const float2 a = __fadd2_rn(xx, nm);
+              const float2 e = make_float2(ODD && k == 0 ? 0.f : ex2(a.x), ODD && k == NPK - 1 ? 0.f : ex2(a.y));
+              sum2 = __fadd2_rn(sum2, e);
+              pk[k] = pack_el<F16>(e.x, e.y);
+            }
+            st_row<NPK>(p_addr + u * C::PROW + (uc >> 1), pk);
+          }
+          const float sm = sum2.x + sum2.y;
+          ex_sum[ex_me] = sm;
+          named_bar_sync(bar_q, 64);
+          return sm + ex_sum[ex_other];
+        };
+        mq = fmaf(ms, p.scale_log2, tmax);
+        while (true) {
+          sum = exp_rows(mq);
+          if (!__any_sync(0xffffffffu, !(sum >= 0x1p-60f))) break;
+          // rare (bias range > ~60 in log2 units inside one window): redo with the exact row max of x.
+          // Both warps of the quarter take this branch together (same queries, same sums); after it
+          // the row maximum contributes exp2(0) = 1 to the sum, so the loop ends.
+          float mx = -INFINITY;
+#pragma unroll
+          for (int u = 0; u < C::UH; ++u) {
+            const float2 *t = trow(u);
+#pragma unroll
+            for (int k = 0; k < NPK; ++k) {
+              const float2 xx = __ffma2_rn(make_float2(__uint_as_float(sv[u][2 * k]), __uint_as_float(sv[u][2 * k + 1])),
+                                           sl2x2, t[k]);
+              mx = fmax3(mx, ODD && k == 0 ? -INFINITY : xx.x, ODD && k == NPK - 1 ? -INFINITY : xx.y);
+            }
+          }
+          ex_max[ex_me] = mx;
+          named_bar_sync(bar_q, 64);  // (the other warp read ex_sum before arriving here)
+          mx = fmaxf(mx, ex_max[ex_other]);
+          if (!(sum >= 0x1p-60f)) mq = mx;
+        }
+      };
+      if (ucr & 1) softmax(std::integral_constant<int, 1>());
+      else softmax(std::integral_constant<int, 0>());
+      tc_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_ready[g]);
+      if (trc) trace_ev(p, it, 9);
+      // ---- epilogue: O / sum -> 16-bit (this warp: head dims [16 hf, 16 hf + 16)), LSE
+      wait_bar(&o_full[g], ph);
+      if (trc) trace_ev(p, it, 10);
       tc_fence_after();
       float o[16];
       {
         uint32_t oa[C::OACC][16];
 #pragma unroll
-        for (int a = 0; a < C::OACC; ++a) tmem_ld_h16<16>(o_addr + a * kD, oa[a]);
+        for (int a = 0; a < C::OACC; ++a) tmem_ld16(lane_base + C::O_COL + a * kD + 16 * hf, oa[a]);
         tc_wait_ld();
 #pragma unroll
         for (int z = 0; z < 16; ++z) {
@@ -542,7 +518,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(NA2D_FWD_SHARED_O ? o_free : &tmem_free[slot]);
+      if (lane == 0) mbar_arrive(o_free);
+      if (trc) trace_ev(p, it, 12);
       if (i < q_end && j < p.W) {
         const float inv = 1.f / sum;
         const size_t qi = ((size_t)bh * p.q_rows + (i - p.q_row0)) * p.W + j;
@@ -551,22 +528,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int z = 0; z < 16; z += 8)
           dst[z / 8] = make_uint4(pack_el<F16>(o[z] * inv, o[z + 1] * inv), pack_el<F16>(o[z + 2] * inv, o[z + 3] * inv),
                                   pack_el<F16>(o[z + 4] * inv, o[z + 5] * inv), pack_el<F16>(o[z + 6] * inv, o[z + 7] * inv));
-        if (p.lse && hf == 0) p.lse[qi] = (mx + __log2f(sum)) * 0.69314718055994531f;
+        if (p.lse && hf == 0) p.lse[qi] = (mq + __log2f(sum)) * 0.69314718055994531f;
       }
-      if (tr) trace_ev(p, it, 9);
+      if (trc) trace_ev(p, it, 13);
     }
   }
   __syncthreads();
   if (warp == kProducerWarp) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
-#ifdef NA2D_TRACE
-    if (lane == 0 && p.trace) {
-      uint64_t gt;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-      p.trace[16384 + 2 * blockIdx.x + 1] = (long long)gt;
-    }
-#endif
   }
 }
 
@@ -579,8 +549,8 @@ cudaError_t launch_fwd(const Geo &g, const void *q, const void *k, const void *v
   CUtensorMap tq, tk, tv;
   const int BH = g.B * g.heads;
   if (!make_tmap_e16_4d(F16, &tq, q, kD, g.W, g.q_rows, BH, 4, 4) ||
-      !make_tmap_e16_4d(F16, &tk, k, kD, g.W, g.kv_rows, BH, kHCP, C::HR) ||
-      !make_tmap_e16_4d(F16, &tv, v, kD, g.W, g.kv_rows, BH, kHCP, C::HR))
+      !make_tmap_e16_4d(F16, &tk, k, kD, g.W, g.kv_rows, BH, C::HP, C::UR) ||
+      !make_tmap_e16_4d(F16, &tv, v, kD, g.W, g.kv_rows, BH, C::HP, C::UR))
     return cudaErrorInvalidValue;
   FwdParams p;
   p.B = g.B;

@@ -44,6 +44,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// try_wait with a suspend-time hint: the thread sleeps in hardware until the phase completes (or
+// the hint elapses) instead of re-polling, so a waiting warp issues a handful of instructions
+// instead of a spin loop that steals issue slots from the busy warps of its sub-partition.
+__device__ __forceinline__ bool mbar_try_wait_hint(uint64_t *bar, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(ns)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_hint(uint64_t *bar, uint32_t parity) {
+  while (!mbar_try_wait_hint(bar, parity, 0x100000u)) {
+  }
+}
 // Wait with exponential back-off sleeps: for producer/issuer warps whose spinning would steal
 // issue slots from the compute warps sharing their SM sub-partition.
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity, uint32_t max_ns = 256) {

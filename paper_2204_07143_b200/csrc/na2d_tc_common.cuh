@@ -105,6 +105,33 @@ __device__ __forceinline__ void st_row(uint32_t addr, const uint32_t (&v)[N]) {
   }
   if constexpr (N % 2 == 1) tmem_st1(addr + N - 1, v[N - 1]);
 }
+// zeros into N consecutive TMEM columns of this warp's 32 lanes
+template <int N>
+__device__ __forceinline__ void st_zero(uint32_t addr) {
+  const uint32_t z = 0;
+  if constexpr (N >= 32) {
+    tmem_st32_zero(addr);
+    st_zero<N - 32>(addr + 32);
+  } else if constexpr (N >= 16) {
+    const uint32_t a[16] = {z, z, z, z, z, z, z, z, z, z, z, z, z, z, z, z};
+    tmem_st16(addr, a);
+    st_zero<N - 16>(addr + 16);
+  } else if constexpr (N >= 8) {
+    const uint32_t a[8] = {z, z, z, z, z, z, z, z};
+    tmem_st8(addr, a);
+    st_zero<N - 8>(addr + 8);
+  } else if constexpr (N >= 4) {
+    const uint32_t a[4] = {z, z, z, z};
+    tmem_st4(addr, a);
+    st_zero<N - 4>(addr + 4);
+  } else if constexpr (N >= 2) {
+    const uint32_t a[2] = {z, z};
+    tmem_st2(addr, a);
+    st_zero<N - 2>(addr + 2);
+  } else if constexpr (N == 1) {
+    tmem_st1(addr, z);
+  }
+}
 __device__ __forceinline__ void st_zero12(uint32_t addr) {
   const uint32_t z8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const uint32_t z4[4] = {0, 0, 0, 0};

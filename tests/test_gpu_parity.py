@@ -143,6 +143,25 @@ def test_drpb_cell_probe(L):
         assert abs(ref["drpb"][h, a, c]) > 1e-4 and np.sign(drpb[h, a, c]) == np.sign(ref["drpb"][h, a, c])
 
 
+@pytest.mark.parametrize("L", [3, 5, 7])
+def test_large_bias_range(L):
+    """A bias range of ~10^2 (log2 units) inside one window: the forward's upper-bound softmax shift
+    (raw-S max + window bias max) underflows the row sum there, and its exact-max redo must give
+    the oracle's result (forward and backward)."""
+    shape = Shape(f"bigbias{L}", 2, 2, 19, 37, 32, L)
+    inp = make_inputs(shape, seed=21 + L)
+    # a near one-hot softmax passes |v| straight to O: V, dO halved (exact in bf16) keep |O| < 4, where
+    # the bf16 output rounding alone stays below 2^-8 (the north-star inputs' regime)
+    inp["v"], inp["dout"] = inp["v"] * 0.5, inp["dout"] * 0.5
+    scale = shape.d ** -0.5
+    base = inp["rpb"]
+    for mul, bwd in [(25.0, False), (10.0, True)]:  # window bias ranges ~160 / ~65 (log2 units)
+        inp["rpb"] = (base * mul).astype(np.float32)
+        ref = run_oracle(inp, L, scale, backward=bwd)
+        got = run_cuda(inp, L, scale, "bf16", backward=bwd)
+        log_errors(f"{shape.name}x{mul:g}", "bf16", compare(got, ref, "bf16"))
+
+
 @pytest.mark.parametrize("dtype", ["bf16", "f32", "f16"])
 def test_row_band(dtype):
     """Band call (global coordinates) == oracle band call, incl. dk/dv partials."""
