@@ -200,18 +200,134 @@ def run_reference(args, shape: Shape):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_dict(shape, args.gpus),
+            "config": config_dict(shape, args.gpus, default_mode(shape) if args.mode == "auto" else args.mode),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def config_dict(shape: Shape, n: int) -> dict:
+MODES = {"weak": "per-rank batch fixed: every rank runs the config's batch (its own batch shard)",
+         "units": "fixed problem split by (b, h) units across ranks (heads split when B < ranks)",
+         "band": "fixed problem split by query-row bands, (k-1)/2-row K/V halo exchange with the neighbours"}
+
+
+def default_mode(shape: Shape) -> str:
+    """BASELINE configs: NAT-Tiny stages weak-scale by batch; ADE 128^2 is split by batch x heads; the
+    COCO map by row bands."""
+    if shape.name.startswith("cfg4"):
+        return "units"
+    if shape.name.startswith("cfg5"):
+        return "band"
+    return "weak"
+
+
+def config_dict(shape: Shape, n: int, mode: str = "weak", l2: str | None = None) -> dict:
+    par = {"weak": f"dp{n} batch shards, dRPB NCCL all-reduce",
+           "units": f"{n} ranks x contiguous (b,h) units, dRPB per-head fold + NCCL all-reduce",
+           "band": f"{n} row bands, NCCL send/recv K/V halos + dK/dV halo partials, dRPB all-reduce"}[mode]
     return {"workload": shape.name, "model": "NA2D (NAT-Tiny stage-1 shapes)" if shape.name == DEFAULT_CONFIG else "NA2D",
-            "per_rank_batch": shape.B, "global_batch": shape.B * n, "heads": shape.heads, "H": shape.H, "W": shape.W,
+            "per_rank_batch": shape.B if mode == "weak" else None, "global_batch": shape.B * n if mode == "weak" else shape.B,
+            "heads": shape.heads, "H": shape.H, "W": shape.W,
             "head_dim": shape.d, "kernel_size": shape.kernel_size, "rpb": "trunc-normal(0,0.02) table",
-            "parallelism": f"dp{n} batch shards, dRPB NCCL all-reduce" if n > 1 else "single GPU",
-            "l2": "two alternating input sets of 4 x B*heads*H*W*d bf16 (> 126 MB L2 each); no flush"}
+            "mode": mode, "parallelism": "single GPU" if n == 1 else par,
+            "l2": l2 or "two alternating input sets of 4 x B*heads*H*W*d bf16 (> 126 MB L2 each); no flush"}
+
+
+def relaunch_distributed(n: int) -> int:
+    """`bench.py --gpus N` without a torchrun environment: run this script under torchrun (one rank
+    per GPU, rendezvous on 127.0.0.1) and return its exit status."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+class Work:
+    """One rank's share of a step: inputs resident in HBM, preallocated outputs, step(i)."""
+
+    def __init__(self, args, shape: Shape, mode: str, world: int, rank: int, dev, dist, share: bool):
+        import torch
+        import paper_2204_07143_b200 as na2d
+        from paper_2204_07143_b200 import dist as nd
+        self.mode, self.shape, self.world = mode, shape, world
+        el = torch.float16 if args.dtype == "f16" else torch.bfloat16
+        L, scale = shape.kernel_size, shape.d ** -0.5
+        self.L, self.scale = L, scale
+        g = shape.replace(B=shape.B * world) if mode == "weak" else shape
+        if mode == "weak":
+            inp = make_inputs(g, dtype=args.dtype, rpb="swin", batch_offset=rank * shape.B, batch_count=shape.B)
+        else:
+            inp = make_inputs(g, dtype=args.dtype, rpb="swin")
+        full_rpb = torch.from_numpy(inp["rpb"]).to(dev)
+        to = lambda x: torch.from_numpy(x).to(dev).to(el)  # noqa: E731
+        if mode == "weak":
+            t = {n: to(inp[n]) for n in ("q", "k", "v", "dout")}
+            self.rpb = full_rpb
+        elif mode == "units":
+            t = {n: nd.unit_shard(torch.from_numpy(inp[n]), world, rank).to(dev).to(el) for n in ("q", "k", "v", "dout")}
+            self.rpb = nd.unit_rpb(full_rpb, shape.B, world, rank)
+        else:
+            self.band = nd.band_plan(shape.H, world, L)[rank]
+            b = self.band
+            t = {n: to(np.ascontiguousarray(inp[n][:, :, b.r0:b.r1])) for n in ("q", "dout")}
+            for n in ("k", "v"):  # K / V live in the extended band buffer (own rows at [top, top + rows))
+                t[n] = to(np.ascontiguousarray(inp[n][:, :, b.k0:b.k1]))
+            self.rpb = full_rpb
+            self.halo_bufs = [{}, {}]
+        del inp
+        self.full_rpb = full_rpb
+        set_bytes = sum(x.numel() * x.element_size() for x in t.values())
+        # L2 hygiene: two alternating input sets when one set exceeds the 126 MB L2, else an L2 flush
+        # (256 MB write) before every timed step
+        self.flush = None
+        if set_bytes >= 150e6:
+            self.sets = [t, {n: x.flip(0).contiguous() for n, x in t.items()}]
+            self.l2 = f"two alternating input sets of {set_bytes / 1e6:.0f} MB (> 126 MB L2 each); no flush"
+        else:
+            self.sets = [t]
+            self.flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+            self.l2 = f"input set {set_bytes / 1e6:.1f} MB < L2: 256 MB L2 flush before each step, steps timed one by one"
+        q = t["q"]
+        self.out = torch.empty_like(q)
+        self.lse = torch.empty(q.shape[:4], device=dev, dtype=torch.float32)
+        self.dq = torch.empty_like(q)
+        self.dk, self.dv = torch.empty_like(t["k"]), torch.empty_like(t["v"])
+        self.drpb = torch.empty_like(self.rpb)
+        self.drpb_heads = torch.empty_like(full_rpb)
+        kw = {}
+        if mode == "band":
+            kw = dict(map_height=shape.H, q_row0=self.band.r0, kv_row0=self.band.k0)
+        self.kw = kw
+        self.p = na2d.problem_for(q, t["k"], L, scale, **kw)
+        self.ws = torch.empty(max(16, na2d.na2d_backward_workspace_bytes(self.p)), device=dev, dtype=torch.uint8)
+        self.nq = q.shape[0] * q.shape[1] * q.shape[2] * q.shape[3]  # this rank's query-heads
+        f_fwd, f_bwd = flops(shape)
+        self.flops_job = (f_fwd + f_bwd) * (world if mode == "weak" else 1)
+        self.dist, self.rank, self.na2d, self.nd = dist, rank, na2d, nd
+
+    def step(self, i):
+        na2d, nd, dist = self.na2d, self.nd, self.dist
+        s = self.sets[i % len(self.sets)]
+        L, scale = self.L, self.scale
+        if self.mode == "band":
+            nd.exchange_halo(s["k"], self.band, bufs=self.halo_bufs[0])
+            nd.exchange_halo(s["v"], self.band, bufs=self.halo_bufs[1])
+        na2d.forward(s["q"], s["k"], s["v"], self.rpb, L, scale, out=self.out, lse=self.lse, **self.kw)
+        na2d.backward(s["q"], s["k"], s["v"], self.rpb, self.out, self.lse, s["dout"], L, scale, workspace=self.ws,
+                      grads=(self.dq, self.dk, self.dv, self.drpb), **self.kw)
+        if self.mode == "band":
+            if self.world > 1:
+                self.dk_own = nd._return_partials(self.dk, self.band).to(self.dk.dtype)
+                self.dv_own = nd._return_partials(self.dv, self.band).to(self.dv.dtype)
+            nd.allreduce_drpb(self.drpb)
+        elif self.mode == "units":
+            nd.unit_drpb_to_heads(self.drpb, self.shape.heads, self.shape.B, self.world, self.rank, out=self.drpb_heads)
+        elif self.world > 1:
+            dist.all_reduce(self.drpb)
 
 
 def main():
@@ -220,12 +336,22 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
+    ap.add_argument("--mode", default="auto", choices=["auto"] + sorted(MODES),
+                    help="multi-GPU partition (auto: the config's; " + "; ".join(f"{k}: {v}" for k, v in MODES.items()) + ")")
     ap.add_argument("--impl", default="na2d", choices=["na2d", "reference"])
     ap.add_argument("--no-extras", action="store_true", help="skip cpu baseline / e2e / clocks (profiling runs)")
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "f16"],
                     help="16-bit I/O type of the tensor-core path (BASELINE's metric is bf16)")
     args = ap.parse_args()
     shape = CONFIGS[args.config]
+    mode = default_mode(shape) if args.mode == "auto" else args.mode
+
+    env_world = os.environ.get("WORLD_SIZE")
+    if args.gpus > 1 and env_world is None:
+        sys.exit(relaunch_distributed(args.gpus))
+    if env_world is not None and int(env_world) != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env_world}", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args, shape)
         return
@@ -250,32 +376,8 @@ def main():
         else:
             dist.init_process_group("nccl", device_id=dev)
     na2d.load_library()
-
-    # ---- inputs: this rank's batch shard of the global synthetic batch, resident in HBM
-    g = shape.replace(B=shape.B * world)
-    inp = make_inputs(g, dtype=args.dtype, rpb="swin", batch_offset=rank * shape.B, batch_count=shape.B)
-    el = torch.float16 if args.dtype == "f16" else torch.bfloat16
-    sets = []
-    t = {n: torch.from_numpy(inp[n]).to(dev).to(el) for n in ("q", "k", "v", "dout")}
-    sets.append(t)
-    sets.append({n: x.flip(0).contiguous() for n, x in t.items()})
-    rpb = torch.from_numpy(inp["rpb"]).to(dev)
-    del inp
-    L, scale = shape.kernel_size, shape.d ** -0.5
-    out = torch.empty_like(t["q"])
-    lse = torch.empty(t["q"].shape[:4], device=dev, dtype=torch.float32)
-    dq, dk, dv = torch.empty_like(out), torch.empty_like(out), torch.empty_like(out)
-    drpb = torch.empty_like(rpb)
-    p = na2d.problem_for(t["q"], t["k"], L, scale)
-    ws = torch.empty(max(16, na2d.na2d_backward_workspace_bytes(p)), device=dev, dtype=torch.uint8)
-
-    def step(i):
-        s = sets[i % 2]
-        na2d.forward(s["q"], s["k"], s["v"], rpb, L, scale, out=out, lse=lse)
-        na2d.backward(s["q"], s["k"], s["v"], rpb, out, lse, s["dout"], L, scale, workspace=ws,
-                      grads=(dq, dk, dv, drpb))
-        if world > 1:
-            dist.all_reduce(drpb)
+    w = Work(args, shape, mode, world, rank, dev, dist, share)
+    p, L, scale = w.p, w.L, w.scale
 
     def barrier():
         if world > 1:
@@ -283,39 +385,53 @@ def main():
         torch.cuda.synchronize()
 
     for i in range(args.warmup):
-        step(i)
+        if w.flush is not None:
+            w.flush.fill_(i & 0xff)
+        w.step(i)
     barrier()
     sampler = ClockSampler(local) if not args.no_extras else None
     if sampler:
         sampler.__enter__()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
-    e0.record()
-    for i in range(args.steps):
-        step(i)
-    e1.record()
-    barrier()
+    if w.flush is None:
+        e0.record()
+        for i in range(args.steps):
+            w.step(i)
+        e1.record()
+        barrier()
+        ms = e0.elapsed_time(e1) / args.steps
+    else:  # steps timed one by one, an untimed L2 flush before each
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        for i in range(args.steps):
+            w.flush.fill_(i & 0xff)
+            evs[i][0].record()
+            w.step(i)
+            evs[i][1].record()
+        barrier()
+        ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
     if sampler:
         sampler.__exit__()
-    ms = e0.elapsed_time(e1) / args.steps
     if world > 1:
         tt = torch.tensor([ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     f_fwd, f_bwd = flops(shape)
-    value = (f_fwd + f_bwd) * world / (ms * 1e-3) / 1e12
+    value = w.flops_job / (ms * 1e-3) / 1e12
     launches_per_step = na2d.na2d_launch_count(p, 0) + na2d.na2d_launch_count(p, 1)
 
     # ---- per-kernel CUDA-event timing (same steps, recorded by the library on its stream)
     na2d.na2d_profile_enable(True)
     for i in range(args.steps):
-        step(i)
+        if w.flush is not None:
+            w.flush.fill_(i & 0xff)
+        w.step(i)
     torch.cuda.synchronize()
     prof = na2d.na2d_profile_read()
     na2d.na2d_profile_enable(False)
     peaks = measured_peaks()
     kernels = {}
-    nq = shape.units * shape.H * shape.W
+    nq = w.nq
     for name, (tot, cnt) in prof.items():
         per = alg_bytes_per_query(name, shape.d, 2)
         avg_ms = tot / cnt
@@ -329,23 +445,26 @@ def main():
     roofline = None
     if dom:
         ach = kernels[dom]["achieved_gbs"]
+        rank_ms = sum(k["avg_us"] * k["launches"] for k in kernels.values()) / 1e3 / args.steps
         roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                     "frac": ach / peaks["hbm_gbs"] if ach else None, "traffic": traffic,
                     "alg_bytes_per_launch": alg_bytes_per_query(dom, shape.d, 2) * nq,
                     "peak_source": peaks["_source"], "kernels": kernels,
                     "step_frac_hbm": ((260 + 516) * nq / (ms * 1e-3) / 1e9) / peaks["hbm_gbs"],
-                    "step_frac_tensor": (f_fwd + f_bwd) / (ms * 1e-3) / 1e12 / peaks.get("bf16_tflops", 1659.7)}
+                    "kernels_frac_hbm": ((260 + 516) * nq / (rank_ms * 1e-3) / 1e9) / peaks["hbm_gbs"],
+                    "step_frac_tensor": w.flops_job / world / (ms * 1e-3) / 1e12 / peaks.get("bf16_tflops", 1659.7)}
 
     # ---- context: the paper's own decomposition (QK+RPB kernel writing the attention
     # weights, softmax, AV, and their gradients) on the same inputs, same device
     paper = None
-    if not args.no_extras and args.dtype == "bf16":  # the comparison path has no fp16 I/O
-        s0 = sets[0]
+    if not args.no_extras and args.dtype == "bf16" and mode == "weak" and world == 1:
+        s0 = w.sets[0]
+        rpb = w.rpb
         _, _, attn = na2d.paper_forward(s0["q"], s0["k"], s0["v"], rpb, L, scale)
         dsb = torch.empty_like(attn)
 
         def pstep(i):
-            s = sets[i % 2]
+            s = w.sets[i % len(w.sets)]
             na2d.paper_forward(s["q"], s["k"], s["v"], rpb, L, scale)
             na2d.paper_backward(s["q"], s["k"], s["v"], rpb, attn, s["dout"], L, scale, dS=dsb)
 
@@ -364,16 +483,16 @@ def main():
                  "what": "paper's unfused decomposition on this GPU (na2d_paper_forward/backward, CUDA-core kernels)"}
         del attn, dsb
 
-    # ---- end to end through the host-buffer C-ABI entry (pinned host memory)
+    # ---- end to end through the host-buffer C-ABI entry (pinned host memory); whole maps only
     e2e = None
-    if not args.no_extras:
-        host = {n: sets[0][n].cpu().pin_memory() for n in ("q", "k", "v", "dout")}
-        hrpb = rpb.cpu().pin_memory()
+    if not args.no_extras and mode != "band":
+        host = {n: w.sets[0][n].cpu().pin_memory() for n in ("q", "k", "v", "dout")}
+        hrpb = w.rpb.cpu().pin_memory()
         hout = {n: torch.empty_like(host["q"]).pin_memory() for n in ("out", "dq", "dk", "dv")}
         hlse = torch.empty(host["q"].shape[:4]).pin_memory()
         hdrpb = torch.empty_like(hrpb).pin_memory()
         nb = na2d.na2d_step_host_workspace_bytes(p)
-        del sets
+        w.sets = None
         torch.cuda.empty_cache()
         hws = torch.empty(nb, device=dev, dtype=torch.uint8)
         st = torch.cuda.current_stream().cuda_stream
@@ -385,8 +504,11 @@ def main():
                                 hdrpb.data_ptr(), hws.data_ptr(), nb, st)
             if world > 1:
                 d = hdrpb.to(dev)
-                dist.all_reduce(d)
-                hdrpb.copy_(d)
+                if mode == "units":
+                    d = w.nd.unit_drpb_to_heads(d, shape.heads, shape.B, world, rank)
+                else:
+                    dist.all_reduce(d)
+                d.cpu()
 
         hstep()
         barrier()
@@ -402,8 +524,8 @@ def main():
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ems = float(tt.item())
         tb = host["q"].numel() * 2
-        TT = (2 * L - 1) ** 2 * shape.heads * 4
-        e2e = {"value": (f_fwd + f_bwd) * world / (ems * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ems,
+        TT = hrpb.numel() * 4
+        e2e = {"value": w.flops_job / (ems * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ems,
                "h2d_bytes_per_step": 4 * tb + TT, "d2h_bytes_per_step": 4 * tb + hlse.numel() * 4 + TT,
                "path": "na2d_step_host (pinned host buffers; H2D + fwd + bwd + D2H pipelined over up to 16 batch chunks on three library streams)"}
 
@@ -413,8 +535,10 @@ def main():
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": args.dtype, "data": "synthetic", "config": config_dict(shape, world),
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "weak" if mode == "weak" else "strong",
+                "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+                "config": config_dict(shape, world, mode, w.l2),
                 "impl": "na2d", "gpu_launches": launches_per_step * args.steps,
                 "kernel_families": [na2d.na2d_kernel_family(p, 0), na2d.na2d_kernel_family(p, 1)],
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "paper_design": paper,

@@ -37,6 +37,42 @@ def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
     return n * rank // world, n * (rank + 1) // world
 
 
+def unit_shard(x: torch.Tensor, world: int, rank: int) -> torch.Tensor:
+    """x: [B, heads, ...] -> this rank's contiguous range of the B*heads (b, h) units as
+    [1, units, ...].  Units are independent maps, so the kernels treat the range as one
+    batch of `units` heads; this splits heads too when B < world (e.g. B=2, 2 heads on 4 ranks)."""
+    B, heads = x.shape[:2]
+    u0, u1 = shard_range(B * heads, world, rank)
+    return x.reshape(B * heads, *x.shape[2:])[u0:u1].unsqueeze(0).contiguous()
+
+
+def unit_heads(B: int, heads: int, world: int, rank: int) -> torch.Tensor:
+    """Head index of each unit of this rank's shard (for the per-unit RPB tables and dRPB)."""
+    u0, u1 = shard_range(B * heads, world, rank)
+    return torch.arange(u0, u1) % heads
+
+
+def unit_rpb(rpb: torch.Tensor | None, B: int, world: int, rank: int) -> torch.Tensor | None:
+    """The RPB table of every unit of the shard: [units, 2L-1, 2L-1] (a gather of the heads' tables)."""
+    if rpb is None:
+        return None
+    idx = unit_heads(B, rpb.shape[0], world, rank).to(rpb.device)
+    return rpb.index_select(0, idx).contiguous()
+
+
+def unit_drpb_to_heads(drpb_units: torch.Tensor | None, heads: int, B: int, world: int, rank: int,
+                       out: torch.Tensor | None = None, group=None) -> torch.Tensor | None:
+    """Per-unit dRPB partials -> per-head sums over this rank's units, then the all-reduce over ranks
+    (fixed order inside a rank: index_add over units in ascending order)."""
+    if drpb_units is None:
+        return None
+    idx = unit_heads(B, heads, world, rank).to(drpb_units.device)
+    acc = torch.zeros((heads,) + tuple(drpb_units.shape[1:]), device=drpb_units.device, dtype=drpb_units.dtype) \
+        if out is None else out.zero_()
+    acc.index_add_(0, idx, drpb_units)
+    return allreduce_drpb(acc, group)
+
+
 def allreduce_drpb(drpb: torch.Tensor | None, group=None) -> torch.Tensor | None:
     """Sum the dRPB partials of all ranks in place (the only exchange of the sharded backward)."""
     if drpb is not None and dist.is_initialized() and dist.get_world_size(group) > 1:
@@ -81,59 +117,100 @@ def band_plan(H: int, world: int, L: int) -> list[Band]:
     return bands
 
 
+def _p2p(ops_spec, group=None):
+    """Run [(isend|irecv, tensor, peer)] as one batch; with gloo (CPU tests, ranks sharing one GPU)
+    CUDA tensors are staged through host memory, since gloo's point-to-point ops are CPU-only."""
+    if not ops_spec:
+        return
+    gloo = dist.get_backend(group) == "gloo"
+    staged, ops = [], []
+    for kind, t, peer in ops_spec:
+        x = t
+        if gloo and t.is_cuda:
+            x = t.cpu() if kind == "send" else torch.empty(t.shape, dtype=t.dtype)
+            staged.append((t, x, kind))
+        ops.append(dist.P2POp(dist.isend if kind == "send" else dist.irecv, x, peer, group))
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+    for t, x, kind in staged:
+        if kind == "recv":
+            t.copy_(x)
+
+
 def _exchange_rows(own: torch.Tensor, band: Band, group=None) -> torch.Tensor:
     """own: [..., r1-r0, W, d] rows of this rank -> [..., k1-k0, W, d] with neighbour halos."""
-    rows = own.shape[-3]
-    ops, recv_top, recv_bot = [], None, None
+    ext = torch.empty(own.shape[:-3] + (band.k1 - band.k0,) + own.shape[-2:], device=own.device, dtype=own.dtype)
+    ext[..., band.top:band.top + own.shape[-3], :, :] = own
+    exchange_halo(ext, band, group)
+    return ext
+
+
+def exchange_halo(ext: torch.Tensor, band: Band, group=None, bufs: dict | None = None) -> None:
+    """ext: [..., k1-k0, W, d] holding this rank's own rows at [top, top + r1 - r0): fill its halo rows
+    from the neighbours (and send them theirs).  NCCL point-to-point on NCCL's stream; the caller's
+    stream waits for it (no host sync on GPUs).  `bufs` caches the contiguous send / receive buffers
+    (a band's halo rows are strided across the outer B x heads dimension)."""
+    rows = band.r1 - band.r0
+    bufs = {} if bufs is None else bufs
+
+    def buf(name, like):
+        b = bufs.get(name)
+        if b is None or b.shape != like.shape or b.dtype != like.dtype or b.device != like.device:
+            b = bufs[name] = torch.empty(like.shape, dtype=like.dtype, device=like.device)
+        return b
+
+    spec, recvs = [], []
     prev, nxt = band.rank - 1, band.rank + 1
     # what the neighbours need from us: rank-1's bottom halo = our first rows; rank+1's top = our last
     if prev >= 0:
         need_prev = _neighbour(band, prev).bottom
         if need_prev:
-            ops.append(dist.P2POp(dist.isend, own[..., :need_prev, :, :].contiguous(), prev, group))
+            src = ext[..., band.top:band.top + need_prev, :, :]
+            spec.append(("send", buf("s_prev", src).copy_(src), prev))
         if band.top:
-            recv_top = torch.empty_like(own[..., :band.top, :, :])
-            ops.append(dist.P2POp(dist.irecv, recv_top, prev, group))
+            dst = ext[..., :band.top, :, :]
+            r = buf("r_prev", dst)
+            spec.append(("recv", r, prev))
+            recvs.append((dst, r))
     if nxt < band.world:
         need_next = _neighbour(band, nxt).top
         if need_next:
-            ops.append(dist.P2POp(dist.isend, own[..., rows - need_next:, :, :].contiguous(), nxt, group))
+            src = ext[..., band.top + rows - need_next:band.top + rows, :, :]
+            spec.append(("send", buf("s_next", src).copy_(src), nxt))
         if band.bottom:
-            recv_bot = torch.empty_like(own[..., :band.bottom, :, :])
-            ops.append(dist.P2POp(dist.irecv, recv_bot, nxt, group))
-    if ops:
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
-    parts = [x for x in (recv_top, own, recv_bot) if x is not None]
-    return torch.cat(parts, dim=-3) if len(parts) > 1 else own
+            dst = ext[..., band.top + rows:, :, :]
+            r = buf("r_next", dst)
+            spec.append(("recv", r, nxt))
+            recvs.append((dst, r))
+    _p2p(spec, group)
+    for dst, r in recvs:
+        dst.copy_(r)
 
 
 def _return_partials(ext: torch.Tensor, band: Band, group=None) -> torch.Tensor:
     """ext: [..., k1-k0, W, d] partial gradients for the extended rows; send the halo rows back to
     their owners, add what the neighbours computed for our rows; returns [..., r1-r0, W, d] (>= fp32)."""
-    ext = ext if ext.dtype == torch.float64 else ext.float()  # accumulate partials in >= fp32
-    own = ext[..., band.top:band.top + (band.r1 - band.r0), :, :].clone()
-    ops, recvs = [], []
+    acc_t = ext.dtype if ext.dtype == torch.float64 else torch.float32  # halo partials summed in >= fp32
+    own = ext[..., band.top:band.top + (band.r1 - band.r0), :, :].to(acc_t)
+    spec, recvs = [], []
     prev, nxt = band.rank - 1, band.rank + 1
     if prev >= 0:
         if band.top:
-            ops.append(dist.P2POp(dist.isend, ext[..., :band.top, :, :].contiguous(), prev, group))
+            spec.append(("send", ext[..., :band.top, :, :].to(acc_t).contiguous(), prev))
         nb = _neighbour(band, prev).bottom  # rank-1 computed partials for our first nb rows
         if nb:
             buf = torch.empty_like(own[..., :nb, :, :])
-            ops.append(dist.P2POp(dist.irecv, buf, prev, group))
+            spec.append(("recv", buf, prev))
             recvs.append((0, buf))
     if nxt < band.world:
         if band.bottom:
-            ops.append(dist.P2POp(dist.isend, ext[..., ext.shape[-3] - band.bottom:, :, :].contiguous(), nxt, group))
+            spec.append(("send", ext[..., ext.shape[-3] - band.bottom:, :, :].to(acc_t).contiguous(), nxt))
         nt = _neighbour(band, nxt).top  # rank+1 computed partials for our last nt rows
         if nt:
             buf = torch.empty_like(own[..., :nt, :, :])
-            ops.append(dist.P2POp(dist.irecv, buf, nxt, group))
+            spec.append(("recv", buf, nxt))
             recvs.append((own.shape[-3] - nt, buf))
-    if ops:
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
+    _p2p(spec, group)
     for off, buf in recvs:
         own[..., off:off + buf.shape[-3], :, :] += buf
     return own
@@ -166,11 +243,13 @@ def band_forward(q, k, v, rpb, L: int, scale: float | None, band: Band, group=No
 def band_backward(q, k_ext, v_ext, rpb, out, lse, dout, L: int, scale: float | None, band: Band, group=None,
                   backward_fn=None):
     """Backward of a band given the extended K/V from band_forward.  Returns (dq, dk, dv, drpb) for
-    own rows (dk, dv in fp32 after the halo-partial exchange; drpb all-reduced)."""
+    own rows, in q's dtype: the halo rows' dK / dV partials (this rank's queries) go back to their
+    owners and are summed with the owners' own partials in fp32 before the one rounding to the
+    output type; drpb all-reduced."""
     fn = backward_fn or _cuda_backward
     dq, dk_ext, dv_ext, drpb = fn(q, k_ext, v_ext, rpb, out, lse, dout, L, scale, map_height=band.H,
                                   q_row0=band.r0, kv_row0=band.k0)
-    dk = _return_partials(dk_ext, band, group)
-    dv = _return_partials(dv_ext, band, group)
+    dk = _return_partials(dk_ext, band, group).to(q.dtype)
+    dv = _return_partials(dv_ext, band, group).to(q.dtype)
     allreduce_drpb(drpb, group)
     return dq, dk, dv, drpb

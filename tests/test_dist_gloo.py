@@ -132,3 +132,46 @@ def test_band_plan_and_shards():
     with pytest.raises(ValueError):
         nd.band_plan(20, 4, 7)
     assert [nd.shard_range(10, 3, r) for r in range(3)] == [(0, 3), (3, 6), (6, 10)]
+
+
+def _unit_worker(rank, world, port, shape, q_res):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2204_07143_b200 import dist as nd
+    B, heads, H, W, d, L = shape
+    (q, k, v, do), rpb = _inputs(B, heads, H, W, d, L, seed=29)
+    qs, ks, vs, dos = (nd.unit_shard(x, world, rank) for x in (q, k, v, do))
+    urpb = nd.unit_rpb(rpb, B, world, rank)
+    dq, dk, dv, du = _oracle_backward(qs, ks, vs, urpb, None, None, dos, L, d ** -0.5, map_height=H, q_row0=0,
+                                      kv_row0=0)
+    drpb = nd.unit_drpb_to_heads(du, heads, B, world, rank)
+    u0, u1 = nd.shard_range(B * heads, world, rank)
+    q_res.put((rank, u0, u1, dq.numpy()[0], dk.numpy()[0], drpb.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("shape,world", [((3, 2, 9, 8, 4, 5), 2), ((1, 2, 10, 9, 4, 3), 2), ((2, 2, 9, 7, 4, 5), 3)])
+def test_unit_shards_split_heads(shape, world):
+    """batch x heads sharding by (b, h) units: a rank's units run as one batch of
+    'heads' with per-unit RPB tables; per-unit dRPB folds back onto the heads and all-reduces.  The
+    cases include B < world (heads split across ranks) and unit ranges starting mid-batch."""
+    import oracle
+    ctx = mp.get_context("spawn")
+    q_res = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_unit_worker, args=(r, world, port, shape, q_res)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q_res.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    B, heads, H, W, d, L = shape
+    (q, k, v, do), rpb = _inputs(B, heads, H, W, d, L, seed=29)
+    whole = oracle.na2d_backward(q.numpy(), k.numpy(), v.numpy(), rpb.numpy(), do.numpy(), L, d ** -0.5)
+    flat = lambda x: x.reshape((B * heads,) + x.shape[2:])  # noqa: E731
+    for rank, u0, u1, dq, dk, drpb in res:
+        np.testing.assert_allclose(dq, flat(whole["dq"])[u0:u1], atol=1e-12)
+        np.testing.assert_allclose(dk, flat(whole["dk"])[u0:u1], atol=1e-12)
+        np.testing.assert_allclose(drpb, whole["drpb"], atol=1e-10)
