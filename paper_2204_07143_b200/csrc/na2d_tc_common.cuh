@@ -29,7 +29,8 @@ struct BiasTable {
   static constexpr int TT = 2 * L - 1;
   static constexpr int TROWS = TT + 1;
   static constexpr int FLOATS = L * TROWS * kTblStride;
-  __device__ static void build(float *tbl, const float *rpb, int h, int Lw, float mul, int tid, int nthreads) {
+  // element-parallel build (one global load per entry)
+  __device__ static void build_elems(float *tbl, const float *rpb, int h, int Lw, float mul, int tid, int nthreads) {
     for (int e = tid; e < FLOATS; e += nthreads) {
       const int dc = e / (TROWS * kTblStride);
       const int rr = (e / kTblStride) % TROWS;
@@ -37,6 +38,26 @@ struct BiasTable {
       float v = -INFINITY;
       if (rr < TT && cb >= dc && cb < dc + Lw) v = rpb ? __ldg(&rpb[(h * TT + rr) * TT + cb]) * mul : 0.f;
       tbl[e] = v;
+    }
+  }
+  // one table row per thread: the row's 2L-1 bias values are loaded together (independent loads),
+  // then the row's kTblStride entries written
+  __device__ static void build_rows(float *tbl, const float *rpb, int h, int Lw, float mul, int tid, int nthreads) {
+    for (int row = tid; row < L * TROWS; row += nthreads) {
+      const int dc = row / TROWS, rr = row % TROWS;
+      float b[TT];
+#pragma unroll
+      for (int k = 0; k < TT; ++k) b[k] = (rpb && rr < TT) ? __ldg(&rpb[(h * TT + rr) * TT + k]) * mul : 0.f;
+      float *dst = tbl + row * kTblStride;
+#pragma unroll
+      for (int e = 0; e < kTblStride; ++e) {
+        const int cb = e - kTblOff;
+        float v = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < TT; ++k)
+          if (cb == k && rr < TT && k >= dc && k < dc + Lw) v = b[k];
+        dst[e] = v;
+      }
     }
   }
 };
