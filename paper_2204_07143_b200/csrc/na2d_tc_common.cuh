@@ -95,7 +95,7 @@ __device__ __forceinline__ void ld_row(uint32_t addr, uint32_t (&v)[N]) {
     v[B] = a[0];
     v[B + 1] = a[1];
   }
-  static_assert(N % 2 == 0, "row width");
+  if constexpr (N % 2 == 1) tmem_ld1(addr + N - 1, v[N - 1]);
 }
 template <int N>
 __device__ __forceinline__ void st_row(uint32_t addr, const uint32_t (&v)[N]) {

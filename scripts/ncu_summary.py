@@ -21,6 +21,10 @@ KEYS = {
     "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active": "alu_pct",
     "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active": "fma_pct",
     "lts__t_sector_hit_rate.pct": "l2_hit_pct",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active": "tensor_pct",
+    "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed": "tensor_rt_pct",
+    "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active": "shared_pipe_pct",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum": "lds_conflicts",
     "launch__registers_per_thread": "regs",
     "launch__block_size": "block",
     "launch__grid_size": "grid",
@@ -41,21 +45,35 @@ def load(rep):
             except ValueError:
                 continue
             d[KEYS[n]] = x * UNIT.get(u[i], 1)
+        elif "pipe_tensor" in n and "pct" in n and "tensor_any" not in d:
+            try:
+                d["tensor_any"] = (n, float(v[i].replace(",", "")))
+            except ValueError:
+                pass
     return d
+
+
+def tensor_cell(d):
+    """tensor-pipe activity: % of active cycles (and % of elapsed realtime cycles when captured)"""
+    if "tensor_pct" in d or "tensor_rt_pct" in d:
+        return "{:.1f} / {:.1f}".format(d.get("tensor_pct", float("nan")), d.get("tensor_rt_pct", float("nan")))
+    if "tensor_any" in d:
+        return "{:.1f} ({})".format(d["tensor_any"][1], d["tensor_any"][0])
+    return "n/a"
 
 
 def main():
     out_md, cfg, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
     rows = [load(r) for r in reps]
-    lines = ["| kernel | us | DRAM read MB | DRAM write MB | DRAM GB/s | SM % | mem % | issue % | XU % | ALU % | FMA % | L2 hit % | regs |",
-             "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
+    lines = ["| kernel | us | DRAM read MB | DRAM write MB | DRAM GB/s | SM % | mem % | issue % | XU % | ALU % | FMA % | L2 hit % | tensor % | regs |",
+             "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for d in rows:
         t = d.get("duration", 0)
         tot = d.get("dram_read", 0) + d.get("dram_write", 0)
-        lines.append("| {} | {:.1f} | {:.1f} | {:.1f} | {:.0f} | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {:.0f} |".format(
+        lines.append("| {} | {:.1f} | {:.1f} | {:.1f} | {:.0f} | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {} | {:.0f} |".format(
             d["kernel"], t, d.get("dram_read", 0) / 1e6, d.get("dram_write", 0) / 1e6, tot / (t * 1e-6) / 1e9 if t else 0,
             d.get("sm_pct", 0), d.get("mem_pct", 0), d.get("issue_pct", 0), d.get("xu_pct", 0), d.get("alu_pct", 0),
-            d.get("fma_pct", 0), d.get("l2_hit_pct", 0), d.get("regs", 0)))
+            d.get("fma_pct", 0), d.get("l2_hit_pct", 0), tensor_cell(d), d.get("regs", 0)))
     open(out_md, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
     tpath = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "ncu_traffic.json")
