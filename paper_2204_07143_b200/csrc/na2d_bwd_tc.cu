@@ -14,9 +14,12 @@ TileOrder make_tile_order(const Geo &g, int L) {
   o.q_row0 = g.q_row0;
   const int ns = (L - 1) / 2, q_end = g.q_row0 + g.q_rows;
   const int tiles_h = (g.q_rows + tc::kTQH - 1) / tc::kTQH, tiles_w = (g.W + tc::kTQW - 1) / tc::kTQW;
-  auto groups = [&](int n, int tile, int first, int end, int axis, int *start, int *count) {
+  // groups of tile rows (columns): one run of interior tiles, every other tile alone; returns the count
+  // and the interior group's index (-1 if none)
+  auto groups = [&](int n, int tile, int first, int end, int axis, int *start, int *count, int *interior_group) {
     int ng = 0;
     int tr = 0;
+    *interior_group = -1;
     while (tr < n) {
       auto interior = [&](int t) {
         const int a = first + t * tile, b = a + tile - 1;
@@ -27,6 +30,7 @@ TileOrder make_tile_order(const Geo &g, int L) {
         while (e < n && interior(e)) ++e;
         start[ng] = tr;
         count[ng] = e - tr;
+        *interior_group = ng;
         tr = e;
       } else {
         start[ng] = tr;
@@ -37,8 +41,8 @@ TileOrder make_tile_order(const Geo &g, int L) {
     }
     return ng;
   };
-  o.n_rg = groups(tiles_h, tc::kTQH, g.q_row0, q_end, g.H, o.rg_start, o.rg_count);
-  o.n_cg = groups(tiles_w, tc::kTQW, 0, g.W, g.W, o.cg_start, o.cg_count);
+  o.n_rg = groups(tiles_h, tc::kTQH, g.q_row0, q_end, g.H, o.rg_start, o.rg_count, &o.int_rg);
+  o.n_cg = groups(tiles_w, tc::kTQW, 0, g.W, g.W, o.cg_start, o.cg_count, &o.int_cg);
   o.num_tiles = g.B * g.heads * tiles_h * tiles_w;
   return o;
 }

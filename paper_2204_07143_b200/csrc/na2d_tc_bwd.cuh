@@ -10,35 +10,57 @@ namespace na2d {
 
 // Tile visiting order grouped by geometry class.  Tile rows (columns) whose 8 (16) query rows
 // (columns) are all unclamped and inside the map form one "interior" group; every other tile row
-// (column) is a group of its own.  A class is a (row group, column group) pair; tiles are
-// enumerated class-major, then head, then batch, then row, then column, so the per-lane union
-// geometry is identical for consecutive tiles of a class.
+// (column) is a group of its own.  A class is a (row group, column group) pair.  The interior class
+// comes first, head-major (then batch, row, column); then, per head, every border class in class
+// order (then batch, row, column).  So the per-lane union geometry is identical for consecutive tiles
+// of a class, and a head change (a bias-table rebuild and dRPB commit) happens about once per head
+// even when the border classes hold a handful of tiles per map and there are many heads.
 struct TileOrder {
   static constexpr int kMaxGroups = 16;
   int B, heads, q_row0, num_tiles;
   int n_rg, n_cg;
+  int int_rg, int_cg;  // the interior row / column group (-1: none)
   int rg_start[kMaxGroups], rg_count[kMaxGroups], cg_start[kMaxGroups], cg_count[kMaxGroups];
   struct Tile {
     int bh, i0, j0, cls;
   };
+  __device__ __forceinline__ Tile make(int a, int b, int h, int bb, int rem) const {
+    Tile x;
+    x.bh = bb * heads + h;
+    x.i0 = q_row0 + (rg_start[a] + rem / cg_count[b]) * tc::kTQH;
+    x.j0 = (cg_start[b] + rem % cg_count[b]) * tc::kTQW;
+    x.cls = a * n_cg + b;
+    return x;
+  }
   __device__ __forceinline__ Tile decode(int t) const {
-    Tile x{0, 0, 0, 0};
+    if (int_rg >= 0 && int_cg >= 0) {
+      const int per_map = rg_count[int_rg] * cg_count[int_cg];
+      const int cnt = B * heads * per_map;
+      if (t < cnt) {
+        const int hb = t / per_map, rem = t - hb * per_map;
+        const int h = hb / B;
+        return make(int_rg, int_cg, h, hb - h * B, rem);
+      }
+      t -= cnt;
+    }
+    int border = 0;  // border tiles per head (all batches)
+    for (int a = 0; a < n_rg; ++a)
+      for (int b = 0; b < n_cg; ++b)
+        if (a != int_rg || b != int_cg) border += B * rg_count[a] * cg_count[b];
+    const int h = t / border;
+    t -= h * border;
     for (int a = 0; a < n_rg; ++a)
       for (int b = 0; b < n_cg; ++b) {
+        if (a == int_rg && b == int_cg) continue;
         const int per_map = rg_count[a] * cg_count[b];
-        const int cnt = B * heads * per_map;
+        const int cnt = B * per_map;
         if (t < cnt) {
-          const int hb = t / per_map, rem = t - hb * per_map;
-          const int h = hb / B, bb = hb - h * B;
-          x.bh = bb * heads + h;
-          x.i0 = q_row0 + (rg_start[a] + rem / cg_count[b]) * tc::kTQH;
-          x.j0 = (cg_start[b] + rem % cg_count[b]) * tc::kTQW;
-          x.cls = a * n_cg + b;
-          return x;
+          const int bb = t / per_map;
+          return make(a, b, h, bb, t - bb * per_map);
         }
         t -= cnt;
       }
-    return x;
+    return make(0, 0, 0, 0, 0);
   }
 };
 
