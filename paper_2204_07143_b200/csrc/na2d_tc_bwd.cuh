@@ -10,16 +10,21 @@ namespace na2d {
 
 // Tile visiting order grouped by geometry class.  Tile rows (columns) whose 8 (16) query rows
 // (columns) are all unclamped and inside the map form one "interior" group; every other tile row
-// (column) is a group of its own.  A class is a (row group, column group) pair.  The interior class
-// comes first, head-major (then batch, row, column); then, per head, every border class in class
-// order (then batch, row, column).  So the per-lane union geometry is identical for consecutive tiles
-// of a class, and a head change (a bias-table rebuild and dRPB commit) happens about once per head
-// even when the border classes hold a handful of tiles per map and there are many heads.
+// (column) is a group of its own.  A class is a (row group, column group) pair; consecutive tiles of
+// a class share the per-lane union geometry.  Two orders (make_tile_order picks one):
+//  * class-major: class, then head, batch, row, column -- when every class holds at least a CTA's
+//    share of tiles per head (e.g. NAT-Tiny stage 1: 128 maps per head);
+//  * interior first: the interior class head-major, then per head every border class in class order
+//    -- when the border classes hold only a few tiles per head (few maps, many heads, e.g. the ADE
+//    map split into 32 (b,h) units), where class-major would switch heads (bias-table rebuild, dRPB
+//    commit) at nearly every border tile.  Measured (cfg2 / cfg4-units B1): class-major 143 / 213 us,
+//    interior first 167 / 115 us.
 struct TileOrder {
   static constexpr int kMaxGroups = 16;
   int B, heads, q_row0, num_tiles;
   int n_rg, n_cg;
   int int_rg, int_cg;  // the interior row / column group (-1: none)
+  int class_major;     // plain class-major order (class, head, batch, row, column)
   int rg_start[kMaxGroups], rg_count[kMaxGroups], cg_start[kMaxGroups], cg_count[kMaxGroups];
   struct Tile {
     int bh, i0, j0, cls;
@@ -33,6 +38,19 @@ struct TileOrder {
     return x;
   }
   __device__ __forceinline__ Tile decode(int t) const {
+    if (class_major) {
+      for (int a = 0; a < n_rg; ++a)
+        for (int b = 0; b < n_cg; ++b) {
+          const int per_map = rg_count[a] * cg_count[b];
+          const int cnt = B * heads * per_map;
+          if (t < cnt) {
+            const int hb = t / per_map, rem = t - hb * per_map;
+            const int h = hb / B;
+            return make(a, b, h, hb - h * B, rem);
+          }
+          t -= cnt;
+        }
+    }
     if (int_rg >= 0 && int_cg >= 0) {
       const int per_map = rg_count[int_rg] * cg_count[int_cg];
       const int cnt = B * heads * per_map;
