@@ -44,7 +44,8 @@ TileOrder make_tile_order(const Geo &g, int L) {
   o.n_rg = groups(tiles_h, tc::kTQH, g.q_row0, q_end, g.H, o.rg_start, o.rg_count, &o.int_rg);
   o.n_cg = groups(tiles_w, tc::kTQW, 0, g.W, g.W, o.cg_start, o.cg_count, &o.int_cg);
   o.num_tiles = g.B * g.heads * tiles_h * tiles_w;
-  // class-major when the smallest class still holds a CTA's share of tiles per head
+  // class-major unless the smallest class holds so few tiles per head that a CTA's contiguous share
+  // would cross more than ~4 heads there
   int min_class = 1 << 30;
   for (int a = 0; a < o.n_rg; ++a)
     for (int b = 0; b < o.n_cg; ++b) {
@@ -52,7 +53,7 @@ TileOrder make_tile_order(const Geo &g, int L) {
       min_class = c < min_class ? c : min_class;
     }
   const int grid = o.num_tiles < tc::num_sms() ? o.num_tiles : tc::num_sms();
-  o.class_major = min_class * grid >= o.num_tiles ? 1 : 0;
+  o.class_major = 4 * min_class * grid >= o.num_tiles ? 1 : 0;
   return o;
 }
 

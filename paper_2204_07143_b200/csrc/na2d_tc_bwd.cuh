@@ -12,8 +12,9 @@ namespace na2d {
 // (columns) are all unclamped and inside the map form one "interior" group; every other tile row
 // (column) is a group of its own.  A class is a (row group, column group) pair; consecutive tiles of
 // a class share the per-lane union geometry.  Two orders (make_tile_order picks one):
-//  * class-major: class, then head, batch, row, column -- when every class holds at least a CTA's
-//    share of tiles per head (e.g. NAT-Tiny stage 1: 128 maps per head);
+//  * class-major: class, then head, batch, row, column -- when every class holds enough tiles per
+//    head that a CTA's contiguous share crosses at most ~4 heads (e.g. NAT-Tiny stage 1: 128 maps
+//    per head; ADE 128^2: 16);
 //  * interior first: the interior class head-major, then per head every border class in class order
 //    -- when the border classes hold only a few tiles per head (few maps, many heads, e.g. the ADE
 //    map split into 32 (b,h) units), where class-major would switch heads (bias-table rebuild, dRPB

@@ -37,12 +37,21 @@ def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
     return n * rank // world, n * (rank + 1) // world
 
 
+def whole_batches(B: int, heads: int, world: int, rank: int) -> bool:
+    """True if this rank's contiguous range of the B*heads (b, h) units is a range of whole batches."""
+    u0, u1 = shard_range(B * heads, world, rank)
+    return u0 % heads == 0 and u1 % heads == 0
+
+
 def unit_shard(x: torch.Tensor, world: int, rank: int) -> torch.Tensor:
-    """x: [B, heads, ...] -> this rank's contiguous range of the B*heads (b, h) units as
-    [1, units, ...].  Units are independent maps, so the kernels treat the range as one
-    batch of `units` heads; this splits heads too when B < world (e.g. B=2, 2 heads on 4 ranks)."""
+    """x: [B, heads, ...] -> this rank's contiguous range of the B*heads (b, h) units.  Units are
+    independent maps.  A range of whole batches keeps the [B', heads, ...] layout (one bias
+    table per head, shared by the batches); otherwise (heads split, e.g. B=2, 2 heads on 4 ranks) the
+    range is returned as [1, units, ...], one "head" per unit with its own table (unit_rpb)."""
     B, heads = x.shape[:2]
     u0, u1 = shard_range(B * heads, world, rank)
+    if whole_batches(B, heads, world, rank):
+        return x[u0 // heads:u1 // heads].contiguous()
     return x.reshape(B * heads, *x.shape[2:])[u0:u1].unsqueeze(0).contiguous()
 
 
@@ -53,19 +62,25 @@ def unit_heads(B: int, heads: int, world: int, rank: int) -> torch.Tensor:
 
 
 def unit_rpb(rpb: torch.Tensor | None, B: int, world: int, rank: int) -> torch.Tensor | None:
-    """The RPB table of every unit of the shard: [units, 2L-1, 2L-1] (a gather of the heads' tables)."""
+    """The RPB tables the shard's kernels take: the heads' own [heads, 2L-1, 2L-1] for a range of
+    whole batches, else one per unit [units, 2L-1, 2L-1] (a gather of the heads' tables)."""
     if rpb is None:
         return None
+    if whole_batches(B, rpb.shape[0], world, rank):
+        return rpb
     idx = unit_heads(B, rpb.shape[0], world, rank).to(rpb.device)
     return rpb.index_select(0, idx).contiguous()
 
 
 def unit_drpb_to_heads(drpb_units: torch.Tensor | None, heads: int, B: int, world: int, rank: int,
                        out: torch.Tensor | None = None, group=None) -> torch.Tensor | None:
-    """Per-unit dRPB partials -> per-head sums over this rank's units, then the all-reduce over ranks
-    (fixed order inside a rank: index_add over units in ascending order)."""
+    """The shard's dRPB -> per-head sums (per-unit partials folded over this rank's units in ascending
+    order; already per head for a range of whole batches), then the all-reduce over ranks."""
     if drpb_units is None:
         return None
+    if whole_batches(B, heads, world, rank):
+        acc = drpb_units if out is None else out.copy_(drpb_units)
+        return allreduce_drpb(acc, group)
     idx = unit_heads(B, heads, world, rank).to(drpb_units.device)
     acc = torch.zeros((heads,) + tuple(drpb_units.shape[1:]), device=drpb_units.device, dtype=drpb_units.dtype) \
         if out is None else out.zero_()

@@ -146,16 +146,19 @@ def _unit_worker(rank, world, port, shape, q_res):
                                       kv_row0=0)
     drpb = nd.unit_drpb_to_heads(du, heads, B, world, rank)
     u0, u1 = nd.shard_range(B * heads, world, rank)
-    q_res.put((rank, u0, u1, dq.numpy()[0], dk.numpy()[0], drpb.numpy()))
+    units = lambda x: x.numpy().reshape((-1,) + tuple(x.shape[2:]))  # noqa: E731  ([B', heads] or [1, units])
+    q_res.put((rank, u0, u1, units(dq), units(dk), drpb.numpy()))
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("shape,world", [((3, 2, 9, 8, 4, 5), 2), ((1, 2, 10, 9, 4, 3), 2), ((2, 2, 9, 7, 4, 5), 3)])
+@pytest.mark.parametrize("shape,world", [((3, 2, 9, 8, 4, 5), 2), ((1, 2, 10, 9, 4, 3), 2), ((2, 2, 9, 7, 4, 5), 3),
+                                         ((4, 2, 9, 8, 4, 5), 2)])
 def test_unit_shards_split_heads(shape, world):
     """batch x heads sharding by (b, h) units: a rank's units run as one batch of
-    'heads' with per-unit RPB tables; per-unit dRPB folds back onto the heads and all-reduces.  The
-    cases include B < world (heads split across ranks) and unit ranges starting mid-batch."""
+    'heads' with per-unit RPB tables, or keep the [B', heads] layout when the range is whole batches;
+    per-unit dRPB folds back onto the heads and all-reduces.  The cases include B < world (heads
+    split across ranks), unit ranges starting mid-batch, and whole-batch ranges."""
     import oracle
     ctx = mp.get_context("spawn")
     q_res = ctx.Queue()

@@ -51,7 +51,8 @@ def _worker(rank, world, port, shape, mode, q_res):
         out, lse = na2d.forward(q, k, v, urpb, L, scale)
         dq, dk, dv, du = na2d.backward(q, k, v, urpb, out, lse, do, L, scale)
         drpb = nd.unit_drpb_to_heads(du, shape.heads, shape.B, world, rank)
-        res = dict(out=out[0], lse=lse[0], dq=dq[0], dk=dk[0], dv=dv[0], drpb=drpb)
+        units = lambda x: x.reshape((-1,) + tuple(x.shape[2:]))  # noqa: E731  ([B', heads] or [1, units])
+        res = dict(out=units(out), lse=units(lse), dq=units(dq), dk=units(dk), dv=units(dv), drpb=drpb)
         u0, u1 = nd.shard_range(shape.B * shape.heads, world, rank)
         q_res.put((rank, u0, u1, {n: x.float().cpu().numpy() for n, x in res.items()}))
     dist.barrier()
