@@ -1,1 +1,1 @@
-TRACES="trace_fwd" bash scripts/trace_run.sh; cat gpurun_out/trace_fwd.log
+TRACES="trace_dq" bash scripts/trace_run.sh; cat gpurun_out/trace_dq.log
