@@ -55,8 +55,10 @@ def load(rep):
 
 def tensor_cell(d):
     """tensor-pipe activity: % of active cycles (and % of elapsed realtime cycles when captured)"""
+    if "tensor_pct" in d and "tensor_rt_pct" in d:
+        return "{:.1f} / {:.1f}".format(d["tensor_pct"], d["tensor_rt_pct"])
     if "tensor_pct" in d or "tensor_rt_pct" in d:
-        return "{:.1f} / {:.1f}".format(d.get("tensor_pct", float("nan")), d.get("tensor_rt_pct", float("nan")))
+        return "{:.1f}".format(d.get("tensor_pct", d.get("tensor_rt_pct")))
     if "tensor_any" in d:
         return "{:.1f} ({})".format(d["tensor_any"][1], d["tensor_any"][0])
     return "n/a"
@@ -65,7 +67,7 @@ def tensor_cell(d):
 def main():
     out_md, cfg, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
     rows = [load(r) for r in reps]
-    lines = ["| kernel | us | DRAM read MB | DRAM write MB | DRAM GB/s | SM % | mem % | issue % | XU % | ALU % | FMA % | L2 hit % | tensor % | regs |",
+    lines = ["| kernel | us | DRAM read MB | DRAM write MB | DRAM GB/s | SM % | mem % | issue % | XU % | ALU % | FMA % | L2 hit % | tensor pipe % | regs |",
              "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for d in rows:
         t = d.get("duration", 0)
