@@ -53,8 +53,6 @@ __device__ __forceinline__ void wait_bar(uint64_t *bar, uint32_t parity) { mbar_
 __device__ __forceinline__ void wait_bar(uint64_t *bar, uint32_t parity) { mbar_wait(bar, parity); }
 #endif
 
-constexpr int kStagesQK = 2;      // Q + K halo ring (released when the QK MMAs complete)
-constexpr int kStagesV = 2;       // V halo ring (released when the PV MMAs complete)
 constexpr int kTInfo = 8;         // tile-description ring (>= 5: see the producer)
 constexpr int kThreads = 640;     // 20 warps: 16 elementwise (two groups of 8), 4 producer / MMA-issue
 // The SM sub-partition scheduler favours the highest warp id among eligible warps: the producer and
@@ -62,8 +60,13 @@ constexpr int kThreads = 640;     // 20 warps: 16 elementwise (two groups of 8),
 // (warp % 4) never delay a TMA or MMA issue.
 constexpr int kProducerWarp = 16, kMmaWarp = 17, kProducerVWarp = 18, kPvWarp = 19;
 
-template <int L>
+template <int L, int D>
 struct Cfg {
+  static_assert(D == 16 || D == 32 || D == 64, "head dim");
+  static constexpr int ROWB = 2 * D;            // bytes per 16-bit row: one swizzle atom (32 / 64 / 128 B)
+  // Q + K halo ring (released when the QK MMAs complete), V halo ring (released when PV completes);
+  // single-stage at D = 64 (shared memory)
+  static constexpr int SQK = D <= 32 ? 2 : 1, SV = D <= 32 ? 2 : 1;
   static constexpr int HP = kTQW + L - 1;       // halo width = row pitch of the K / V sub-tile buffers
   static constexpr int UR = 4 + L - 1;          // halo rows of a sub-tile (4 query rows)
   static constexpr int UH = UR / 2;             // union rows per elementwise warp (two warps per lane quarter)
@@ -74,22 +77,22 @@ struct Cfg {
   // padded to whole PV K-steps of 16 keys; the tail keys are zero rows of K / V
   static constexpr int NSUB = (UR * HP + 2 + 15) / 16 * 16;
   static constexpr int KSTEPS = NSUB / 16;
-  static constexpr int BOX_BYTES = UR * HP * kRowBytes;  // one sub-tile's TMA box
-  static constexpr int SUB_BYTES = NSUB * kRowBytes;     // one sub-tile's K or V buffer
+  static constexpr int BOX_BYTES = UR * HP * ROWB;       // one sub-tile's TMA box
+  static constexpr int SUB_BYTES = (NSUB * ROWB + 1023) / 1024 * 1024;  // one sub-tile's K or V buffer
   static_assert(SUB_BYTES % 1024 == 0, "sub-tile buffers stay 1 KB aligned (swizzled TMA / UMMA)");
   // TMEM: two slots (one per elementwise group) of NSUB columns: S, then P (NSUB/2 packed columns)
   // over the consumed S; O accumulators past both, shared by the groups' alternating tiles
   static constexpr int O_COL = 2 * NSUB;
-  static constexpr int OACC = (512 - O_COL) / kD < 4 ? (512 - O_COL) / kD : 4;  // PV chains per sub-tile
-  static_assert(OACC >= 2, "TMEM budget");
-  static constexpr int Q_BYTES = 128 * kRowBytes;
+  static constexpr int OACC = (512 - O_COL) / D < 4 ? (512 - O_COL) / D : 4;  // PV chains per sub-tile
+  static_assert(OACC >= 1, "TMEM budget");
+  static constexpr int Q_BYTES = 128 * ROWB;
   static constexpr int QK_BYTES = Q_BYTES + 2 * SUB_BYTES;
   static constexpr int V_BYTES = 2 * SUB_BYTES;
-  static constexpr int V_OFF = kStagesQK * QK_BYTES;
+  static constexpr int V_OFF = SQK * QK_BYTES;
   static constexpr int TT = 2 * L - 1;
   static constexpr int TROWS = TT + 1;                             // + all -inf row
   static constexpr int TBL_FLOATS = L * TROWS * kTblStride;        // one table copy
-  static constexpr int TBL_OFF = V_OFF + kStagesV * V_BYTES;       // 2 groups x 2 parity copies
+  static constexpr int TBL_OFF = V_OFF + SV * V_BYTES;             // 2 groups x 2 parity copies
   static constexpr int EX_OFF = TBL_OFF + 4 * TBL_FLOATS * 4;      // row max / sum exchange [2][2][4][2][32]
   static constexpr int RB_OFF = EX_OFF + 2 * 2 * 4 * 2 * 32 * 4;   // per group: scaled RPB + window max
   static constexpr int RB_FLOATS = 256;
@@ -129,11 +132,12 @@ struct FTile {
 };
 static_assert(sizeof(FTile) <= 64, "FTile");
 
-template <int L, bool F16>
+template <int L, int D, bool F16>
 __global__ void __launch_bounds__(kThreads, 1)
     na2d_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                        const __grid_constant__ CUtensorMap tm_v, const FwdParams p) {
-  using C = Cfg<L>;
+  using C = Cfg<L, D>;
+  constexpr int kStagesQK = C::SQK, kStagesV = C::SV, kRB = C::ROWB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   FTile *tinfo = (FTile *)(smem + C::TI_OFF);
@@ -232,7 +236,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int sb = 0; sb < 2; ++sb)
 #pragma unroll
           for (int qb = 0; qb < 4; ++qb)
-            tma_load_4d(st + (64 * sb + 16 * qb) * kRowBytes, &tm_q, &full[s], 0, j0 + 4 * qb, i0 - p.q_row0 + 4 * sb, bh);
+            tma_load_4d(st + (64 * sb + 16 * qb) * kRB, &tm_q, &full[s], 0, j0 + 4 * qb, i0 - p.q_row0 + 4 * sb, bh);
 #pragma unroll
         for (int sb = 0; sb < 2; ++sb)
           tma_load_4d(st + C::Q_BYTES + sb * C::SUB_BYTES, &tm_k, &full[s], 0, hc0, hr0 + ti->rb[sb] - p.kv_row0, bh);
@@ -290,14 +294,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       wait_bar(&slot_free[g], ((it >> 1) & 1) ^ 1);
       if (lane == 0) trace_ev(p, it, 2);
       tc_fence_after();
-      const uint64_t dq = sdesc_sw64(smem_u32(smem + s * C::QK_BYTES));
+      const uint64_t dq = sdesc_sw<kRB>(smem_u32(smem + s * C::QK_BYTES));
       const uint64_t dk0 = dq + (C::Q_BYTES >> 4), dk1 = dk0 + (C::SUB_BYTES >> 4);
       const uint32_t d0 = tmem + g * C::NSUB, d1 = d0 + ((uint32_t)16 << 16);
-      if (elect_one()) {  // two independent accumulation chains (sub-tiles) interleaved
-        mma_ss(d0, dq, dk0, idesc_qk, 0);
-        mma_ss(d1, dq + (4096 >> 4), dk1, idesc_qk, 0);
-        mma_ss(d0, dq + (32 >> 4), dk0 + (32 >> 4), idesc_qk, 1);
-        mma_ss(d1, dq + ((4096 + 32) >> 4), dk1 + (32 >> 4), idesc_qk, 1);
+      if (elect_one()) {  // two independent accumulation chains (sub-tiles) interleaved; K-steps of 16
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t ko = (k * 32) >> 4;
+          mma_ss(d0, dq + ko, dk0 + ko, idesc_qk, k);
+          mma_ss(d1, dq + ((64 * kRB) >> 4) + ko, dk1 + ko, idesc_qk, k);
+        }
         mma_commit(&s_full[g]);
         mma_commit(&empty[s]);
       }
@@ -306,11 +312,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == kPvWarp) {
     // ================= PV issuer: O of tile it from P in slot it & 1 once its group wrote it and the
     // epilogue of tile it - 1 (the other group) has read the shared O accumulators
-    constexpr uint32_t idesc_pv = idesc_el<F16>(64, kD, true);
+    constexpr uint32_t idesc_pv = idesc_el<F16>(64, D, true);
     for (int it = 0; it < ntile; ++it) {
       const int s = it % kStagesV, g = it & 1;
       wait_bar(&full_v[s], (it / kStagesV) & 1);
-      const uint64_t dv0 = sdesc_sw64(smem_u32(smem + C::V_OFF + s * C::V_BYTES)), dv1 = dv0 + (C::SUB_BYTES >> 4);
+      const uint64_t dv0 = sdesc_sw<kRB>(smem_u32(smem + C::V_OFF + s * C::V_BYTES)), dv1 = dv0 + (C::SUB_BYTES >> 4);
       const uint32_t b0 = tmem + g * C::NSUB, b1 = b0 + ((uint32_t)16 << 16);
       const uint32_t o0 = tmem + C::O_COL, o1 = o0 + ((uint32_t)16 << 16);
       wait_bar(&p_ready[g], (it >> 1) & 1);
@@ -321,7 +327,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (elect_one()) {
 #pragma unroll
         for (int ks = 0; ks < C::KSTEPS; ++ks) {
-          const uint32_t voff = (ks * 16 * kRowBytes) >> 4, oc = (ks % C::OACC) * kD;
+          const uint32_t voff = (ks * 16 * kRB) >> 4, oc = (ks % C::OACC) * D;
           const uint32_t a = ks >= C::OACC ? 1u : 0u;
           mma_ts(o0 + oc, b0 + ks * 8, dv0 + voff, idesc_pv, a);
           mma_ts(o1 + oc, b1 + ks * 8, dv1 + voff, idesc_pv, a);
@@ -502,14 +508,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       wait_bar(&o_full[g], ph);
       if (trc) trace_ev(p, it, 10);
       tc_fence_after();
-      float o[16];
+      constexpr int DH = D / 2;  // head dims of this thread (two warps per lane quarter)
+      float o[DH];
       {
-        uint32_t oa[C::OACC][16];
+        uint32_t oa[C::OACC][DH];
 #pragma unroll
-        for (int a = 0; a < C::OACC; ++a) tmem_ld16(lane_base + C::O_COL + a * kD + 16 * hf, oa[a]);
+        for (int a = 0; a < C::OACC; ++a) ld_row<DH>(lane_base + C::O_COL + a * D + DH * hf, oa[a]);
         tc_wait_ld();
 #pragma unroll
-        for (int z = 0; z < 16; ++z) {
+        for (int z = 0; z < DH; ++z) {
           float acc = __uint_as_float(oa[0][z]);
 #pragma unroll
           for (int a = 1; a < C::OACC; ++a) acc += __uint_as_float(oa[a][z]);
@@ -523,9 +530,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (i < q_end && j < p.W) {
         const float inv = 1.f / sum;
         const size_t qi = ((size_t)bh * p.q_rows + (i - p.q_row0)) * p.W + j;
-        uint4 *dst = (uint4 *)(p.out + qi * kD + 16 * hf);
+        uint4 *dst = (uint4 *)(p.out + qi * D + DH * hf);
 #pragma unroll
-        for (int z = 0; z < 16; z += 8)
+        for (int z = 0; z < DH; z += 8)
           dst[z / 8] = make_uint4(pack_el<F16>(o[z] * inv, o[z + 1] * inv), pack_el<F16>(o[z + 2] * inv, o[z + 3] * inv),
                                   pack_el<F16>(o[z + 4] * inv, o[z + 5] * inv), pack_el<F16>(o[z + 6] * inv, o[z + 7] * inv));
         if (p.lse && hf == 0) p.lse[qi] = (mq + __log2f(sum)) * 0.69314718055994531f;
@@ -540,17 +547,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int L, bool F16>
+template <int L, int D, bool F16>
 cudaError_t launch_fwd(const Geo &g, const void *q, const void *k, const void *v, const float *rpb, void *out,
                        float *lse, cudaStream_t st) {
-  using C = Cfg<L>;
-  const cudaError_t attr_err = tc::ensure_smem_attr((const void *)na2d_fwd_tc_kernel<L, F16>, C::SMEM);
+  using C = Cfg<L, D>;
+  const cudaError_t attr_err = tc::ensure_smem_attr((const void *)na2d_fwd_tc_kernel<L, D, F16>, C::SMEM);
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap tq, tk, tv;
   const int BH = g.B * g.heads;
-  if (!make_tmap_e16_4d(F16, &tq, q, kD, g.W, g.q_rows, BH, 4, 4) ||
-      !make_tmap_e16_4d(F16, &tk, k, kD, g.W, g.kv_rows, BH, C::HP, C::UR) ||
-      !make_tmap_e16_4d(F16, &tv, v, kD, g.W, g.kv_rows, BH, C::HP, C::UR))
+  if (!make_tmap_e16_4d(F16, &tq, q, D, g.W, g.q_rows, BH, 4, 4) ||
+      !make_tmap_e16_4d(F16, &tk, k, D, g.W, g.kv_rows, BH, C::HP, C::UR) ||
+      !make_tmap_e16_4d(F16, &tv, v, D, g.W, g.kv_rows, BH, C::HP, C::UR))
     return cudaErrorInvalidValue;
   FwdParams p;
   p.B = g.B;
@@ -570,28 +577,44 @@ cudaError_t launch_fwd(const Geo &g, const void *q, const void *k, const void *v
   p.trace = (long long *)debug_trace_buffer();
   const int grid = p.num_tiles < num_sms() ? p.num_tiles : num_sms();
   ProfScope ps("na2d_fwd_tc", st);
-  const cudaError_t e = launch_pdl(na2d_fwd_tc_kernel<L, F16>, grid, kThreads, C::SMEM, st, tq, tk, tv, p);
+  const cudaError_t e = launch_pdl(na2d_fwd_tc_kernel<L, D, F16>, grid, kThreads, C::SMEM, st, tq, tk, tv, p);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace
 
 bool tc_forward_supported(const Geo &g) {
-  return (g.dtype == NA2D_BF16 || g.dtype == NA2D_F16) && g.d == kD && (g.L == 3 || g.L == 5 || g.L == 7) && tmap_available();
+  return (g.dtype == NA2D_BF16 || g.dtype == NA2D_F16) && (g.d == 16 || g.d == 32 || g.d == 64) &&
+         (g.L == 3 || g.L == 5 || g.L == 7) && tmap_available();
 }
+
+namespace {
+template <int D, bool F16>
+cudaError_t fwd_for_d(const Geo &g, const void *q, const void *k, const void *v, const float *rpb, void *out,
+                      float *lse, cudaStream_t st) {
+  switch (g.L) {
+    case 3: return launch_fwd<3, D, F16>(g, q, k, v, rpb, out, lse, st);
+    case 5: return launch_fwd<5, D, F16>(g, q, k, v, rpb, out, lse, st);
+    case 7: return launch_fwd<7, D, F16>(g, q, k, v, rpb, out, lse, st);
+  }
+  return cudaErrorInvalidValue;
+}
+template <bool F16>
+cudaError_t fwd_for_el(const Geo &g, const void *q, const void *k, const void *v, const float *rpb, void *out,
+                       float *lse, cudaStream_t st) {
+  switch (g.d) {
+    case 16: return fwd_for_d<16, F16>(g, q, k, v, rpb, out, lse, st);
+    case 32: return fwd_for_d<32, F16>(g, q, k, v, rpb, out, lse, st);
+    case 64: return fwd_for_d<64, F16>(g, q, k, v, rpb, out, lse, st);
+  }
+  return cudaErrorInvalidValue;
+}
+}  // namespace
 
 cudaError_t tc_forward(const Geo &g, const void *q, const void *k, const void *v, const float *rpb, void *out,
                        float *lse, cudaStream_t st) {
-  const bool f16 = g.dtype == NA2D_F16;
-  switch (g.L) {
-    case 3: return f16 ? launch_fwd<3, true>(g, q, k, v, rpb, out, lse, st)
-                 : launch_fwd<3, false>(g, q, k, v, rpb, out, lse, st);
-    case 5: return f16 ? launch_fwd<5, true>(g, q, k, v, rpb, out, lse, st)
-                 : launch_fwd<5, false>(g, q, k, v, rpb, out, lse, st);
-    case 7: return f16 ? launch_fwd<7, true>(g, q, k, v, rpb, out, lse, st)
-                 : launch_fwd<7, false>(g, q, k, v, rpb, out, lse, st);
-  }
-  return cudaErrorInvalidValue;
+  return g.dtype == NA2D_F16 ? fwd_for_el<true>(g, q, k, v, rpb, out, lse, st)
+                             : fwd_for_el<false>(g, q, k, v, rpb, out, lse, st);
 }
 
 }  // namespace na2d

@@ -272,6 +272,20 @@ __device__ __forceinline__ uint64_t sdesc_sw64(uint32_t saddr) {
   return d;
 }
 
+// The same for rows of ROWB = 32 / 64 / 128 bytes with the matching swizzle (one atom per row):
+// SBO = 8 rows, layout code 6 / 4 / 2 (SWIZZLE_32B / 64B / 128B).
+template <int ROWB>
+__device__ __forceinline__ uint64_t sdesc_sw(uint32_t saddr) {
+  static_assert(ROWB == 32 || ROWB == 64 || ROWB == 128, "row width");
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)((8 * ROWB) >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)(ROWB == 32 ? 6 : ROWB == 64 ? 4 : 2) << 61;
+  return d;
+}
+
 // kind::f16 instruction descriptor: bf16 A/B, fp32 D.
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool b_mn_major) {
   return (1u << 4)                          // D format fp32

@@ -42,7 +42,10 @@ bool make_tmap_bf16_4d(CUtensorMap *m, const void *base, int dim, int W, int row
 bool make_tmap_e16_4d(bool f16, CUtensorMap *m, const void *base, int dim, int W, int rows, int outer, int box_w,
                       int box_h) {
   EncodeFn fn = encode_fn();
-  if (!fn || dim * 2 != 64) return false;
+  // rows of dim 16-bit elements: 32 / 64 / 128 bytes, one swizzle atom wide (the UMMA operand layouts)
+  if (!fn || (dim != 16 && dim != 32 && dim != 64)) return false;
+  const CUtensorMapSwizzle sw = dim == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : dim == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                                      : CU_TENSOR_MAP_SWIZZLE_128B;
   const cuuint64_t gdim[4] = {(cuuint64_t)dim, (cuuint64_t)W, (cuuint64_t)rows, (cuuint64_t)outer};
   const cuuint64_t gstride[3] = {(cuuint64_t)dim * 2, (cuuint64_t)W * dim * 2, (cuuint64_t)rows * W * dim * 2};
   const cuuint32_t box[4] = {(cuuint32_t)dim, (cuuint32_t)box_w, (cuuint32_t)box_h, 1};
@@ -50,7 +53,7 @@ bool make_tmap_e16_4d(bool f16, CUtensorMap *m, const void *base, int dim, int W
   auto encode = [&] {
     return fn(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(base),
               gdim, gstride, box, estride,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   };
   CUresult r = encode();

@@ -10,8 +10,9 @@ namespace na2d {
 bool tmap_available();
 
 // 4-D bf16 tensor [outer][rows][W][dim] (dim innermost, contiguous) with a box of
-// {dim, box_w, box_h, 1} elements and 64-byte swizzle (dim * 2 must be 64).  Out-of-bounds box
-// elements are zero-filled by the hardware.  Returns false on failure.
+// {dim, box_w, box_h, 1} elements; dim in {16, 32, 64}, i.e. rows of 32 / 64 / 128 bytes with the
+// swizzle of that width (one swizzle atom per row: the UMMA K-major / MN-major operand layouts).
+// Out-of-bounds box elements are zero-filled by the hardware.  Returns false on failure.
 bool make_tmap_bf16_4d(CUtensorMap *m, const void *base, int dim, int W, int rows, int outer, int box_w, int box_h);
 // the same for a 16-bit element type: fp16 if f16, else bf16
 bool make_tmap_e16_4d(bool f16, CUtensorMap *m, const void *base, int dim, int W, int rows, int outer, int box_w,

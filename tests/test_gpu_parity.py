@@ -71,6 +71,29 @@ def test_other_dims_and_kernel_sizes(d, L, dtype):
     check(Shape(f"d{d}k{L}", 2, 2, 17, 21, d, L), dtype)
 
 
+TC_DIMS = [Shape(f"tc_d{d}_{n}", *dims[:4], d, dims[4]) for d in (16, 64)
+           for n, dims in (("ragged13x29k7", (2, 2, 13, 29, 7)), ("ragged30x17k5", (1, 3, 30, 17, 5)),
+                           ("17x21k3", (2, 2, 17, 21, 3)), ("sa7x7k7", (3, 2, 7, 7, 7)), ("w37k7", (1, 2, 11, 37, 7)))]
+
+
+@pytest.mark.parametrize("shape", TC_DIMS, ids=lambda s: s.name)
+@pytest.mark.parametrize("dtype", ["bf16", "f16"])
+def test_tensor_core_forward_other_head_dims(shape, dtype):
+    """f3: head dims 16 and 64 run the tcgen05 forward (32 / 128-byte swizzled operand
+    rows); element-by-element parity of out and LSE, the backward (SIMT for these d) checked too."""
+    assert family(shape, dtype)[0] == "tcgen05", family(shape, dtype)
+    check(shape, dtype)
+
+
+@pytest.mark.parametrize("d", [16, 64])
+def test_tensor_core_forward_other_head_dims_full_size(d):
+    """NAT-Tiny stage-1 geometry with head dim d (B = 16): the tcgen05 forward at size, element by
+    element against the oracle (forward only: the oracle's backward at this size takes minutes)."""
+    shape = Shape(f"tc_d{d}_s1", 16, 2, 56, 56, d, 7)
+    assert family(shape)[0] == "tcgen05"
+    check(shape, backward=False)
+
+
 @pytest.mark.parametrize("L", [3, 5, 7])
 def test_rpb_one_hot_probe(L):
     """Q = 0, one large table cell: every query whose window holds that offset copies V there.
