@@ -17,6 +17,7 @@
 #include <math.h>
 
 #include <mutex>
+#include <type_traits>
 
 #include "na2d_internal.cuh"
 #include "na2d_profile.cuh"
@@ -42,8 +43,9 @@ constexpr int kSlot = 192;     // TMEM columns per chunk slot: S^T [0,96), dP^T 
 constexpr int kACC_COL = 384;  // dV / dK accumulators: buffer b at 384 + 64b (dV), + 32 (dK)
 constexpr int kTileInfoBytes = 512;
 
-template <int L, int QP>
+template <int L, int QP, int D = 32>
 struct CfgK {
+  static constexpr int ROWB = 2 * D;  // bytes per 16-bit row: one swizzle atom (32 / 64 / 128 B)
   static constexpr int NS = (L - 1) / 2;
   static constexpr int CR = kNCH / QP;             // query rows per chunk
   static constexpr int QRH = kTQH + 3 * NS;        // halo rows loaded (max needed)
@@ -53,13 +55,13 @@ struct CfgK {
   // interior quarters (every union column of clamp class NS): union of 4 keys' inverse neighbourhoods
   // is 4 + 2NS columns, + 1 for the even origin
   static constexpr int UCWF = ((4 + 2 * NS + 1) + 1) / 2 * 2;
-  static constexpr int Q_BYTES = (QRA * QP * kRowBytes + 1023) / 1024 * 1024;  // 1 KB aligned (swizzle)
-  static constexpr int KT_BYTES = 128 * kRowBytes;
+  static constexpr int Q_BYTES = (QRA * QP * ROWB + 1023) / 1024 * 1024;  // 1 KB aligned (swizzle)
+  static constexpr int KT_BYTES = 128 * ROWB;
   // LSE and D halo values: pitch LP = QP + 4 so the TMA box can start at a 16-byte aligned column
   static constexpr int LP = QP + 4;
   static constexpr int LD_FLOATS = (QRA * LP + 31) / 32 * 32;  // 128 B aligned
   static constexpr int STAGE_BYTES = (2 * Q_BYTES + 2 * KT_BYTES + 2 * LD_FLOATS * 4 + 1023) / 1024 * 1024;
-  static constexpr int TX_BYTES = 2 * QRH * QP * kRowBytes + 2 * KT_BYTES;
+  static constexpr int TX_BYTES = 2 * QRH * QP * ROWB + 2 * KT_BYTES;
   static_assert(STAGE_BYTES % 1024 == 0 && Q_BYTES % 1024 == 0, "1 KB alignment");
   static constexpr int TT = 2 * L - 1;
   static constexpr int TROWS = TT + 1;
@@ -67,7 +69,8 @@ struct CfgK {
   static constexpr int TBL_OFF = kStages * STAGE_BYTES;
   // dV / dK output staging: 2 groups x 4 warps x 4 KB (SW64 boxes, 1 KB aligned)
   static constexpr int OUT_OFF = (TBL_OFF + TBL_FLOATS * 4 + 1023) / 1024 * 1024;
-  static constexpr int TI_OFF = OUT_OFF + 8 * 4096;
+  static constexpr int OUT_W = 4 * 16 * ROWB;  // per warp: dV, dK x two 4 x 4-key blocks (TMA store boxes)
+  static constexpr int TI_OFF = OUT_OFF + 8 * OUT_W;
   static constexpr int BAR_OFF = TI_OFF + kStages * kTileInfoBytes;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
   static_assert(SMEM <= 232448, "shared memory");
@@ -237,14 +240,15 @@ struct TileInfo {
 };
 static_assert(sizeof(TileInfo) <= kTileInfoBytes, "TileInfo size");
 
-template <int L, int QP, bool F16>
+template <int L, int QP, int D, bool F16>
 __global__ void __launch_bounds__(kThreads, 1)
     na2d_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                          const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                          const __grid_constant__ CUtensorMap tm_lse, const __grid_constant__ CUtensorMap tm_d,
                          const __grid_constant__ CUtensorMap tm_dk, const __grid_constant__ CUtensorMap tm_dv,
                          const BwdKParams p) {
-  using C = CfgK<L, QP>;
+  using C = CfgK<L, QP, D>;
+  constexpr int kRB = C::ROWB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   float *tbl = (float *)(smem + C::TBL_OFF);
@@ -261,8 +265,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   // zero the never-loaded tail rows of the Q / dO halos (read by partial chunks)
   for (int s = 0; s < kStages; ++s)
     for (int q2 = 0; q2 < 2; ++q2) {
-      uint8_t *base = smem + s * C::STAGE_BYTES + q2 * C::Q_BYTES + C::QRH * QP * kRowBytes;
-      for (int off = threadIdx.x * 16; off < (C::QRA - C::QRH) * QP * kRowBytes; off += kThreads * 16)
+      uint8_t *base = smem + s * C::STAGE_BYTES + q2 * C::Q_BYTES + C::QRH * QP * kRB;
+      for (int off = threadIdx.x * 16; off < (C::QRA - C::QRH) * QP * kRB; off += kThreads * 16)
         *(uint4 *)(base + off) = make_uint4(0, 0, 0, 0);
     }
   for (int s = 0; s < kStages; ++s) {  // LSE / D halo rows the TMA box never covers
@@ -389,7 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int sb = 0; sb < 2; ++sb)
 #pragma unroll
           for (int qb = 0; qb < 4; ++qb) {
-            const int r0 = (64 * sb + 16 * qb) * kRowBytes;
+            const int r0 = (64 * sb + 16 * qb) * kRB;
             tma_load_4d(kt + r0, &tm_k, &full[s], 0, g.kc0 + 4 * qb, g.kr0 - p.kv_row0 + 4 * sb, g.bh);
             tma_load_4d(kt + C::KT_BYTES + r0, &tm_v, &full[s], 0, g.kc0 + 4 * qb, g.kr0 - p.kv_row0 + 4 * sb, g.bh);
           }
@@ -444,7 +448,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (ti.bh < 0) break;
       const int nch = ti.nchunks, row0a = ti.qs_lo[0] - ti.qr0, row0b = ti.qs_lo[1] - ti.qr0;
       const int qn0 = ti.qs_n[0], qn1 = ti.qs_n[1];
-      const uint64_t dqs = sdesc_sw64(smem_u32(smem + stage * C::STAGE_BYTES));
+      const uint64_t dqs = sdesc_sw<kRB>(smem_u32(smem + stage * C::STAGE_BYTES));
       const uint64_t dkt = dqs + ((2 * C::Q_BYTES) >> 4), dvt = dkt + (C::KT_BYTES >> 4);
       for (int k = 0; k < nch; ++k, ++c) {
         const int x = c & 1;
@@ -452,17 +456,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (c >= 2) mbar_wait(&slot_free[x], ((c >> 1) - 1) & 1);
         tc_fence_after();
         // descriptors: per-stage bases + immediate offsets (short issue bursts, no per-MMA chains)
-        const uint64_t dq0 = dqs + (((row0a + C::CR * k) * QP * kRowBytes) >> 4);
-        const uint64_t dq1 = dqs + (((row0b + C::CR * k) * QP * kRowBytes) >> 4);
+        const uint64_t dq0 = dqs + (((row0a + C::CR * k) * QP * kRB) >> 4);
+        const uint64_t dq1 = dqs + (((row0b + C::CR * k) * QP * kRB) >> 4);
         const uint32_t s0 = tmem + x * kSlot, s1 = s0 + ((uint32_t)16 << 16);
         if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < kD / 16; ++kk) {
+          for (int kk = 0; kk < D / 16; ++kk) {
             const uint32_t ko = (kk * 32) >> 4;
             mma_ss(s0, dkt + ko, dq0 + ko, ids, kk);
             mma_ss(s0 + kNCH, dvt + ko, dq0 + (C::Q_BYTES >> 4) + ko, ids, kk);
-            mma_ss(s1, dkt + (4096 >> 4) + ko, dq1 + ko, ids, kk);
-            mma_ss(s1 + kNCH, dvt + (4096 >> 4) + ko, dq1 + (C::Q_BYTES >> 4) + ko, ids, kk);
+            mma_ss(s1, dkt + ((64 * kRB) >> 4) + ko, dq1 + ko, ids, kk);
+            mma_ss(s1 + kNCH, dvt + ((64 * kRB) >> 4) + ko, dq1 + (C::Q_BYTES >> 4) + ko, ids, kk);
           }
           mma_commit(&s_full[x]);
         }
@@ -473,7 +477,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == kMmaKvWarp) {
     // ================= dV / dK issuer: chunk c once its P^T / dS^T are in TMEM; accumulates in TMEM
     // buffer (tile & 1), so a tile's MMAs never wait for the previous tile's epilogue
-    constexpr uint32_t idesc_o = idesc_el<F16>(64, kD, true);
+    constexpr uint32_t idesc_o = idesc_el<F16>(64, D, true);
     int c = 0;
     for (int it = 0;; ++it) {
       const int stage = it % kStages, b = it & 1;
@@ -483,8 +487,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (ti.bh < 0) break;
       const int nch = ti.nchunks, row0a = ti.qs_lo[0] - ti.qr0, row0b = ti.qs_lo[1] - ti.qr0;
       const int qn0 = ti.qs_n[0], qn1 = ti.qs_n[1];
-      const uint64_t dqs = sdesc_sw64(smem_u32(smem + stage * C::STAGE_BYTES));
-      const uint32_t o0 = tmem + kACC_COL + b * 2 * kD, o1 = o0 + ((uint32_t)16 << 16);
+      const uint64_t dqs = sdesc_sw<kRB>(smem_u32(smem + stage * C::STAGE_BYTES));
+      const uint32_t o0 = tmem + kACC_COL + b * 2 * D, o1 = o0 + ((uint32_t)16 << 16);
       for (int k = 0; k < nch; ++k, ++c) {
         const int x = c & 1;
         mbar_wait(&ds_full[x], (c >> 1) & 1);
@@ -492,8 +496,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (k == 0) mbar_wait(&acc_free[b], ((it >> 1) & 1) ^ 1);
         if (lane == 0) ktrace(p, c, 2);
         tc_fence_after();
-        const uint64_t dq0 = dqs + (((row0a + C::CR * k) * QP * kRowBytes) >> 4);
-        const uint64_t dq1 = dqs + (((row0b + C::CR * k) * QP * kRowBytes) >> 4);
+        const uint64_t dq0 = dqs + (((row0a + C::CR * k) * QP * kRB) >> 4);
+        const uint64_t dq1 = dqs + (((row0b + C::CR * k) * QP * kRB) >> 4);
         const uint32_t a0 = tmem + x * kSlot, a1 = a0 + ((uint32_t)16 << 16);
         const uint32_t acc0 = k == 0 ? 0u : 1u;
         const int nks = chunk_rows_even<C::CR>(qn0, qn1, k) * QP / 16;  // K-steps actually holding P / dS
@@ -502,11 +506,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int ks = 0; ks < kNCH / 16; ++ks) {
             if (ks >= nks) break;
             const uint32_t acc = ks == 0 ? acc0 : 1u;
-            const uint32_t bo = (ks * 16 * kRowBytes) >> 4, doo = (C::Q_BYTES >> 4) + bo;
+            const uint32_t bo = (ks * 16 * kRB) >> 4, doo = (C::Q_BYTES >> 4) + bo;
             mma_ts(o0, a0 + ks * 8, dq0 + doo, idesc_o, acc);              // dV += P^T dO
-            mma_ts(o0 + kD, a0 + kNCH + ks * 8, dq0 + bo, idesc_o, acc);   // dK += dS^T Q
+            mma_ts(o0 + D, a0 + kNCH + ks * 8, dq0 + bo, idesc_o, acc);    // dK += dS^T Q
             mma_ts(o1, a1 + ks * 8, dq1 + doo, idesc_o, acc);
-            mma_ts(o1 + kD, a1 + kNCH + ks * 8, dq1 + bo, idesc_o, acc);
+            mma_ts(o1 + D, a1 + kNCH + ks * 8, dq1 + bo, idesc_o, acc);
           }
           mma_commit(&slot_free[x]);
           if (k == nch - 1) {
@@ -526,7 +530,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_q = tmem + ((uint32_t)(quarter * 32) << 16);
     const float sl2 = p.scale * log2e;
     // output staging of this warp (dV, dK: two 4x4-key blocks each, SW64 layout of the TMA store)
-    uint8_t *ostage = smem + C::OUT_OFF + (grp * 4 + quarter) * 4096;
+    uint8_t *ostage = smem + C::OUT_OFF + (grp * 4 + quarter) * C::OUT_W;
     const bool trq = quarter == 2 && lane == 0;
     // ---- epilogue of a tile: dV, dK (scale) from accumulator buffer (tile & 1), TMA-stored via
     // smem.  Deferred until the group has processed its next chunk, so it never waits for the
@@ -535,21 +539,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int b = eit & 1;
         mbar_wait(&acc_full[b], (eit >> 1) & 1);
         tc_fence_after();
-        uint32_t a0[32], a1[32];
-        tmem_ld32(lane_q + kACC_COL + b * 2 * kD, a0);
-        tmem_ld32(lane_q + kACC_COL + b * 2 * kD + kD, a1);
+        uint32_t a0[D], a1[D];
+        ld_row<D>(lane_q + kACC_COL + b * 2 * D, a0);
+        ld_row<D>(lane_q + kACC_COL + b * 2 * D + D, a1);
         tc_wait_ld();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_free[b]);
         if (lane == 0) bulk_wait_read0();  // this warp's previous stores have left the staging
         __syncwarp();
-        // key (r, cc) of block `half` is row R of the 1 KB box; SW64: 16-byte chunk z at z ^ (R/2 % 4)
+        // key (r, cc) of block `half` is row R of its box; 16-byte chunk z at the TMA swizzle position of
+        // rows of kRB bytes
         const int R = r * 4 + cc;
-        uint8_t *rv = ostage + half * 1024 + R * 64, *rk = rv + 2048;
+        uint8_t *rv = ostage + half * 16 * kRB + R * kRB, *rk = rv + 2 * 16 * kRB;
 #pragma unroll
-        for (int z = 0; z < 4; ++z) {
-          const int zz = (z ^ (R >> 1)) & 3;
+        for (int z = 0; z < D / 8; ++z) {
+          const int zz = kRB == 32 ? (z ^ ((R >> 2) & 1)) : kRB == 64 ? (z ^ ((R >> 1) & 3)) : (z ^ (R & 7));
           *(uint4 *)(rv + 16 * zz) = make_uint4(
               pack_el<F16>(__uint_as_float(a0[8 * z]), __uint_as_float(a0[8 * z + 1])),
               pack_el<F16>(__uint_as_float(a0[8 * z + 2]), __uint_as_float(a0[8 * z + 3])),
@@ -566,8 +571,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {  // out-of-range keys (map / band edge) are clipped by the TMA unit
 #pragma unroll
           for (int sb = 0; sb < 2; ++sb) {
-            tma_store_4d(&tm_dv, ostage + sb * 1024, 0, kc0 + 4 * quarter, kr0 - p.kv_row0 + 4 * sb, bh);
-            tma_store_4d(&tm_dk, ostage + 2048 + sb * 1024, 0, kc0 + 4 * quarter, kr0 - p.kv_row0 + 4 * sb, bh);
+            tma_store_4d(&tm_dv, ostage + sb * 16 * kRB, 0, kc0 + 4 * quarter, kr0 - p.kv_row0 + 4 * sb, bh);
+            tma_store_4d(&tm_dk, ostage + (2 + sb) * 16 * kRB, 0, kc0 + 4 * quarter, kr0 - p.kv_row0 + 4 * sb, bh);
           }
           bulk_commit();
         }
@@ -660,22 +665,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int L, int QP, bool F16>
+template <int L, int QP, int HD, bool F16>
 cudaError_t launch_dkdv_t(const Geo &g, const void *q, const void *k, const void *v, const float *rpb,
                           const float *lse, const void *dout, const float *D, void *dk, void *dv,
                           const float *drpb_part, int part_ctas, float *drpb, int *tile_counter,
                           cudaStream_t st) {
-  using C = CfgK<L, QP>;
-  const cudaError_t attr_err = tc::ensure_smem_attr((const void *)na2d_bwd_dkdv_kernel<L, QP, F16>, C::SMEM);
+  using C = CfgK<L, QP, HD>;
+  const cudaError_t attr_err = tc::ensure_smem_attr((const void *)na2d_bwd_dkdv_kernel<L, QP, HD, F16>, C::SMEM);
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap tq, tdo, tk, tv, tdk, tdv;
   const int BH = g.B * g.heads;
-  if (!make_tmap_e16_4d(F16, &tq, q, kD, g.W, g.q_rows, BH, QP, C::QRH) ||
-      !make_tmap_e16_4d(F16, &tdo, dout, kD, g.W, g.q_rows, BH, QP, C::QRH) ||
-      !make_tmap_e16_4d(F16, &tk, k, kD, g.W, g.kv_rows, BH, 4, 4) ||
-      !make_tmap_e16_4d(F16, &tv, v, kD, g.W, g.kv_rows, BH, 4, 4) ||
-      !make_tmap_e16_4d(F16, &tdk, dk, kD, g.W, g.kv_rows, BH, 4, 4) ||
-      !make_tmap_e16_4d(F16, &tdv, dv, kD, g.W, g.kv_rows, BH, 4, 4))
+  if (!make_tmap_e16_4d(F16, &tq, q, HD, g.W, g.q_rows, BH, QP, C::QRH) ||
+      !make_tmap_e16_4d(F16, &tdo, dout, HD, g.W, g.q_rows, BH, QP, C::QRH) ||
+      !make_tmap_e16_4d(F16, &tk, k, HD, g.W, g.kv_rows, BH, 4, 4) ||
+      !make_tmap_e16_4d(F16, &tv, v, HD, g.W, g.kv_rows, BH, 4, 4) ||
+      !make_tmap_e16_4d(F16, &tdk, dk, HD, g.W, g.kv_rows, BH, 4, 4) ||
+      !make_tmap_e16_4d(F16, &tdv, dv, HD, g.W, g.kv_rows, BH, 4, 4))
     return cudaErrorInvalidValue;
   CUtensorMap tl, td;
   const bool tma_lsd = (g.W * 4) % 16 == 0 && make_tmap_f32_3d(&tl, lse, g.W, g.q_rows, BH, C::LP, C::QRH) &&
@@ -709,7 +714,7 @@ cudaError_t launch_dkdv_t(const Geo &g, const void *q, const void *k, const void
   p.trace = (long long *)debug_trace_buffer();
   const int grid = p.num_tiles < tc::num_sms() ? p.num_tiles : tc::num_sms();
   ProfScope ps("na2d_bwd_dkdv_tc", st);
-  const cudaError_t e = launch_pdl(na2d_bwd_dkdv_kernel<L, QP, F16>, grid, kThreads, C::SMEM, st, tq, tdo, tk, tv, tl, td, tdk, tdv, p);
+  const cudaError_t e = launch_pdl(na2d_bwd_dkdv_kernel<L, QP, HD, F16>, grid, kThreads, C::SMEM, st, tq, tdo, tk, tv, tl, td, tdk, tdv, p);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
@@ -753,15 +758,21 @@ cudaError_t tc_backward_dkdv(const Geo &g, const void *q, const void *k, const v
   // the query halo of a 16-column key tile is at most 16 + 2NS + 1 <= 23 columns away from the right
   // clamp zone; tiles reaching it are shifted (key_col0)
   if (!tc_dkdv_supported(g)) return cudaErrorNotSupported;
+  auto for_d = [&](auto hd_tag, auto f16_tag) -> cudaError_t {
+    constexpr int HD = decltype(hd_tag)::value;
+    constexpr bool F16 = decltype(f16_tag)::value;
+    switch (g.L) {
+      case 3: return launch_dkdv_t<3, 24, HD, F16>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, tile_counter, st);
+      case 5: return launch_dkdv_t<5, 24, HD, F16>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, tile_counter, st);
+      case 7: return launch_dkdv_t<7, 24, HD, F16>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, tile_counter, st);
+    }
+    return cudaErrorInvalidValue;
+  };
+  using T = std::true_type;
+  using Fa = std::false_type;
   const bool f16 = g.dtype == NA2D_F16;
-  switch (g.L) {
-    case 3: return f16 ? launch_dkdv_t<3, 24, true>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, tile_counter, st)
-                 : launch_dkdv_t<3, 24, false>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, tile_counter, st);
-    case 5: return f16 ? launch_dkdv_t<5, 24, true>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, tile_counter, st)
-                 : launch_dkdv_t<5, 24, false>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, tile_counter, st);
-    case 7: return f16 ? launch_dkdv_t<7, 24, true>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, tile_counter, st)
-                 : launch_dkdv_t<7, 24, false>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, tile_counter, st);
-  }
+  if (g.d == 16) return f16 ? for_d(std::integral_constant<int, 16>(), T()) : for_d(std::integral_constant<int, 16>(), Fa());
+  if (g.d == 32) return f16 ? for_d(std::integral_constant<int, 32>(), T()) : for_d(std::integral_constant<int, 32>(), Fa());
   return cudaErrorInvalidValue;
 }
 

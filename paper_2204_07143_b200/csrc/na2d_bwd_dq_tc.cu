@@ -57,8 +57,9 @@ struct TileInfoQ {
   int uc[4];  // even first union column of lane quarter q (relative to hc0)
 };
 
-template <int L>
+template <int L, int D>
 struct CfgQ {
+  static constexpr int ROWB = 2 * D;  // bytes per 16-bit row: one swizzle atom (32 / 64 / 128 B)
   static constexpr int HR = kTQH + L - 1;
   static constexpr int UR = 4 + L - 1;
   static constexpr int NSUB = UR * kHCP;
@@ -82,19 +83,21 @@ struct CfgQ {
   // dQ read-out (epilogue) leaves the critical path.
   static constexpr int DP_COL = NSUB;
   static constexpr int Q_COL = 2 * NSUB;
-  static constexpr int QACC = (512 - Q_COL) / kD < 3 ? (512 - Q_COL) / kD : 3;  // independent dQ chains
+  static constexpr int QACC = (512 - Q_COL) / D < 3 ? (512 - Q_COL) / D : 3;  // independent dQ chains
   static_assert(QACC >= 1, "TMEM budget");
   static constexpr int KV_ROWS = HR * kHCP;
-  static constexpr int Q_BYTES = 128 * kRowBytes;
-  static constexpr int KV_BYTES = KV_ROWS * kRowBytes;
-  static constexpr int TX_BYTES = 2 * Q_BYTES + 2 * KV_BYTES;     // Q, dO, K, V by TMA
-  static constexpr int LSE_OFF = TX_BYTES;                          // + the tile's 128 LSE (log2)
-  static constexpr int STAGE_BYTES = TX_BYTES + 1024;
+  static constexpr int Q_BYTES = 128 * ROWB;
+  static constexpr int KV_BYTES = (KV_ROWS * ROWB + 1023) / 1024 * 1024;
+  static constexpr int TX_BYTES = 2 * Q_BYTES + 2 * KV_ROWS * ROWB;  // Q, dO, K, V by TMA
+  static constexpr int LD_BYTES = 2 * Q_BYTES + 2 * KV_BYTES;          // their (padded) buffers
+  static constexpr int LSE_OFF = LD_BYTES;                          // + the tile's 128 LSE (log2)
+  static constexpr int STAGE_BYTES = LD_BYTES + 1024;
   static_assert(STAGE_BYTES % 1024 == 0, "stages must stay 1 KB aligned (swizzled TMA / UMMA)");
   static constexpr int TT = 2 * L - 1;
   static constexpr int TBL_OFF = kStages * STAGE_BYTES;
   static constexpr int OUT_OFF = (TBL_OFF + BiasTable<L>::FLOATS * 4 + 1023) / 1024 * 1024;  // dQ staging
-  static constexpr int DB_OFF = OUT_OFF + 4 * 2048;
+  static constexpr int HALF_B = 16 * ROWB;                 // one 4 x 4 block of dQ rows (TMA store box)
+  static constexpr int DB_OFF = OUT_OFF + 4 * 2 * HALF_B;
   static constexpr int DP_OFF = DB_OFF + ((8 * kGroups * TT * TT * 4 + 255) / 256) * 256;  // partial D
   static constexpr int TI_OFF = DP_OFF + kGroups * 128 * 4;
   static constexpr int BAR_OFF = TI_OFF + kStages * 64;
@@ -123,12 +126,13 @@ __device__ __forceinline__ void qtrace(const BwdQParams &p, int it, int ev) {
   if (p.trace && blockIdx.x % 37 == 0 && it < 32) p.trace[4096 + ((size_t)(blockIdx.x / 37) * 32 + it) * 32 + ev] = clock64();
 }
 
-template <int L, bool F16>
+template <int L, int D, bool F16>
 __global__ void __launch_bounds__(kThreads, 1)
     na2d_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                        const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                        const __grid_constant__ CUtensorMap tm_dq, const BwdQParams p) {
-  using C = CfgQ<L>;
+  using C = CfgQ<L, D>;
+  constexpr int kRB = C::ROWB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   float *tbl = (float *)(smem + C::TBL_OFF);
@@ -212,7 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int sb = 0; sb < 2; ++sb)
 #pragma unroll
           for (int qb = 0; qb < 4; ++qb) {
-            const int r0 = (64 * sb + 16 * qb) * kRowBytes;
+            const int r0 = (64 * sb + 16 * qb) * kRB;
             tma_load_4d(st + r0, &tm_q, &full[s], 0, g.j0 + 4 * qb, g.i0 - p.q_row0 + 4 * sb, g.bh);
             tma_load_4d(st + C::Q_BYTES + r0, &tm_do, &full[s], 0, g.j0 + 4 * qb, g.i0 - p.q_row0 + 4 * sb, g.bh);
           }
@@ -242,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // while the epilogue reads dQ.
     constexpr uint32_t idesc_s = idesc_el<F16>(64, C::NSUB, false);
     constexpr uint32_t idesc_p1 = idesc_el<F16>(64, 2 * kHCP, false), idesc_p2 = idesc_el<F16>(64, 4 * kHCP, false);
-    constexpr uint32_t idesc_q = idesc_el<F16>(64, kD, true);
+    constexpr uint32_t idesc_q = idesc_el<F16>(64, D, true);
     const int n = t_end - t_begin;
     const uint32_t t0 = tmem, t1 = tmem + ((uint32_t)16 << 16);
     auto issue_sdp = [&](int it) {
@@ -252,9 +256,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int rb0 = tinfo[s].rb[0], rb1 = tinfo[s].rb[1];
       tc_fence_after();
       // descriptors: per-stage bases + immediate offsets (short issue bursts, no per-MMA chains)
-      const uint64_t dqs = sdesc_sw64(smem_u32(smem + s * C::STAGE_BYTES));
-      const uint64_t dk0 = dqs + ((2 * C::Q_BYTES + rb0 * kHCP * kRowBytes) >> 4);
-      const uint64_t dk1 = dqs + ((2 * C::Q_BYTES + rb1 * kHCP * kRowBytes) >> 4);
+      const uint64_t dqs = sdesc_sw<kRB>(smem_u32(smem + s * C::STAGE_BYTES));
+      const uint64_t dk0 = dqs + ((2 * C::Q_BYTES + rb0 * kHCP * kRB) >> 4);
+      const uint64_t dk1 = dqs + ((2 * C::Q_BYTES + rb1 * kHCP * kRB) >> 4);
       if (elect_one()) {
 #if NA2D_B1_SPLIT
         // group g's row pairs = S / dP columns [48 pr0(g), 48 pr0(g+1)) = keys of the same range
@@ -262,25 +266,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int g = kGroups - 1; g >= 0; --g) {
           const int c0 = 2 * kHCP * C::pr0(g), nc = 2 * kHCP * (C::pr0(g + 1) - C::pr0(g));
           const uint32_t id = nc == 2 * kHCP ? idesc_p1 : idesc_p2;
-          const uint32_t bo = (c0 * kRowBytes) >> 4;  // key offset of the part in the K / V halos
+          const uint32_t bo = (c0 * kRB) >> 4;  // key offset of the part in the K / V halos
 #pragma unroll
-          for (int k = 0; k < kD / 16; ++k) {
+          for (int k = 0; k < D / 16; ++k) {
             const uint32_t ko = (k * 32) >> 4;
             mma_ss(t0 + c0, dqs + ko, dk0 + bo + ko, id, k);
             mma_ss(t0 + C::DP_COL + c0, dqs + (C::Q_BYTES >> 4) + ko, dk0 + (C::KV_BYTES >> 4) + bo + ko, id, k);
-            mma_ss(t1 + c0, dqs + (4096 >> 4) + ko, dk1 + bo + ko, id, k);
-            mma_ss(t1 + C::DP_COL + c0, dqs + ((C::Q_BYTES + 4096) >> 4) + ko, dk1 + (C::KV_BYTES >> 4) + bo + ko, id, k);
+            mma_ss(t1 + c0, dqs + ((64 * kRB) >> 4) + ko, dk1 + bo + ko, id, k);
+            mma_ss(t1 + C::DP_COL + c0, dqs + ((C::Q_BYTES + 64 * kRB) >> 4) + ko, dk1 + (C::KV_BYTES >> 4) + bo + ko, id, k);
           }
           mma_commit(&sp_part[g]);
         }
 #else
 #pragma unroll
-        for (int k = 0; k < kD / 16; ++k) {
+        for (int k = 0; k < D / 16; ++k) {
           const uint32_t ko = (k * 32) >> 4;
           mma_ss(t0, dqs + ko, dk0 + ko, idesc_s, k);
           mma_ss(t0 + C::DP_COL, dqs + (C::Q_BYTES >> 4) + ko, dk0 + (C::KV_BYTES >> 4) + ko, idesc_s, k);
-          mma_ss(t1, dqs + (4096 >> 4) + ko, dk1 + ko, idesc_s, k);
-          mma_ss(t1 + C::DP_COL, dqs + ((C::Q_BYTES + 4096) >> 4) + ko, dk1 + (C::KV_BYTES >> 4) + ko, idesc_s, k);
+          mma_ss(t1, dqs + ((64 * kRB) >> 4) + ko, dk1 + ko, idesc_s, k);
+          mma_ss(t1 + C::DP_COL, dqs + ((C::Q_BYTES + 64 * kRB) >> 4) + ko, dk1 + (C::KV_BYTES >> 4) + ko, idesc_s, k);
         }
         mma_commit(sp_full);
 #endif
@@ -298,13 +302,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) qtrace(p, it, 1);
       tc_fence_after();
       const int rb0 = tinfo[s].rb[0], rb1 = tinfo[s].rb[1];
-      const uint64_t dk0 = sdesc_sw64(smem_u32(smem + s * C::STAGE_BYTES) + 2 * C::Q_BYTES + rb0 * kHCP * kRowBytes);
-      const uint64_t dk1 = dk0 + (((rb1 - rb0) * kHCP * kRowBytes) >> 4);
+      const uint64_t dk0 = sdesc_sw<kRB>(smem_u32(smem + s * C::STAGE_BYTES) + 2 * C::Q_BYTES + rb0 * kHCP * kRB);
+      const uint64_t dk1 = dk0 + (((rb1 - rb0) * kHCP * kRB) >> 4);
       if (elect_one()) {
 #pragma unroll
         for (int ks = 0; ks < C::NSUB / 16; ++ks) {
-          const uint32_t ko = (ks * 16 * kRowBytes) >> 4;
-          const uint32_t ao = C::DS_COL + ks * 8 + C::ds_shift_of_ks(ks), qo = C::Q_COL + (ks % C::QACC) * kD;
+          const uint32_t ko = (ks * 16 * kRB) >> 4;
+          const uint32_t ao = C::DS_COL + ks * 8 + C::ds_shift_of_ks(ks), qo = C::Q_COL + (ks % C::QACC) * D;
           mma_ts(t0 + qo, t0 + ao, dk0 + ko, idesc_q, ks >= C::QACC);
           mma_ts(t1 + qo, t1 + ao, dk1 + ko, idesc_q, ks >= C::QACC);
         }
@@ -332,7 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // different (u, z) of different lanes do meet, so the adds stay atomic (RED to shared)
     float *my_db = s_db + ((grp * 4 + quarter) * 2 + half) * C::TT * C::TT;
     constexpr int kEw = kGroups * 128;  // elementwise threads
-    uint8_t *ostage = smem + C::OUT_OFF + quarter * 2048;
+    uint8_t *ostage = smem + C::OUT_OFF + quarter * 2 * C::HALF_B;
     // dRPB accumulator in union coordinates for the current (class, head) and its geometry
     float2 acc[2 * C::PA][C::UCW / 2];  // local rows: union row 2 * pr0 + u
 #pragma unroll
@@ -509,19 +513,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(dq_full, ph);
       if (tq) qtrace(p, it, 12);
       tc_fence_after();
-      // dQ in two 16-column halves (register pressure): partial accumulators summed, scaled,
-      // packed into the SW64 staging row of query (r, c) of block `half` (row R of the 1 KB box;
-      // 16-byte chunk z at z ^ (R/2 % 4))
+      // dQ in 16-column parts (register pressure): partial accumulators summed, scaled, packed into the
+      // swizzled staging row of query (r, c) of block `half` (row R of the box; 16-byte chunk z at
+      // the TMA swizzle position of rows of kRB bytes)
       const int R = r * 4 + c;
-      uint8_t *orow = ostage + half * 1024 + R * 64;
-      uint32_t o[2][16];
+      uint8_t *orow = ostage + half * C::HALF_B + R * kRB;
+      uint32_t o[D / 16][16];
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
+      for (int hh = 0; hh < D / 16; ++hh) {
         tmem_ld16(lane_addr + C::Q_COL + 16 * hh, o[hh]);
 #pragma unroll
         for (int a = 1; a < C::QACC; ++a) {
           uint32_t oa[16];
-          tmem_ld16(lane_addr + C::Q_COL + a * kD + 16 * hh, oa);
+          tmem_ld16(lane_addr + C::Q_COL + a * D + 16 * hh, oa);
           tc_wait_ld();
 #pragma unroll
           for (int z = 0; z < 16; ++z) o[hh][z] = __float_as_uint(__uint_as_float(o[hh][z]) + __uint_as_float(oa[z]));
@@ -535,12 +539,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) bulk_wait_read0();  // this warp's previous store has left the staging
       __syncwarp();
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh)
+      for (int hh = 0; hh < D / 16; ++hh)
 #pragma unroll
         for (int z2 = 0; z2 < 2; ++z2) {
           const int z = 2 * hh + z2;
+          const int zs = kRB == 32 ? (z ^ ((R >> 2) & 1)) : kRB == 64 ? (z ^ ((R >> 1) & 3)) : (z ^ (R & 7));
           const uint32_t *v = o[hh] + 8 * z2;
-          *(uint4 *)(orow + 16 * ((z ^ (R >> 1)) & 3)) = make_uint4(
+          *(uint4 *)(orow + 16 * zs) = make_uint4(
               pack_el<F16>(__uint_as_float(v[0]) * p.scale, __uint_as_float(v[1]) * p.scale),
               pack_el<F16>(__uint_as_float(v[2]) * p.scale, __uint_as_float(v[3]) * p.scale),
               pack_el<F16>(__uint_as_float(v[4]) * p.scale, __uint_as_float(v[5]) * p.scale),
@@ -550,7 +555,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) {  // queries past the map / band edge are clipped by the TMA unit
         tma_store_4d(&tm_dq, ostage, 0, j0 + 4 * quarter, i0 - p.q_row0, bh);
-        tma_store_4d(&tm_dq, ostage + 1024, 0, j0 + 4 * quarter, i0 - p.q_row0 + 4, bh);
+        tma_store_4d(&tm_dq, ostage + C::HALF_B, 0, j0 + 4 * quarter, i0 - p.q_row0 + 4, bh);
         bulk_commit();
       }
       if (tq) qtrace(p, it, 14);
@@ -577,20 +582,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int L, bool F16>
+template <int L, int HD, bool F16>
 cudaError_t launch_dq(const Geo &g, const void *q, const void *k, const void *v, const float *rpb, const void *out,
                       const float *lse, const void *dout, void *dq, float *drpb, float *D, float *part,
                       int *b2_tile_counter, cudaStream_t st) {
-  using C = CfgQ<L>;
-  const cudaError_t attr_err = tc::ensure_smem_attr((const void *)na2d_bwd_dq_kernel<L, F16>, C::SMEM);
+  using C = CfgQ<L, HD>;
+  const cudaError_t attr_err = tc::ensure_smem_attr((const void *)na2d_bwd_dq_kernel<L, HD, F16>, C::SMEM);
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap tq, tdo, tk, tv, tdq;
   const int BH = g.B * g.heads;
-  if (!make_tmap_e16_4d(F16, &tq, q, kD, g.W, g.q_rows, BH, 4, 4) ||
-      !make_tmap_e16_4d(F16, &tdo, dout, kD, g.W, g.q_rows, BH, 4, 4) ||
-      !make_tmap_e16_4d(F16, &tk, k, kD, g.W, g.kv_rows, BH, kHCP, C::HR) ||
-      !make_tmap_e16_4d(F16, &tv, v, kD, g.W, g.kv_rows, BH, kHCP, C::HR) ||
-      !make_tmap_e16_4d(F16, &tdq, dq, kD, g.W, g.q_rows, BH, 4, 4))
+  if (!make_tmap_e16_4d(F16, &tq, q, HD, g.W, g.q_rows, BH, 4, 4) ||
+      !make_tmap_e16_4d(F16, &tdo, dout, HD, g.W, g.q_rows, BH, 4, 4) ||
+      !make_tmap_e16_4d(F16, &tk, k, HD, g.W, g.kv_rows, BH, kHCP, C::HR) ||
+      !make_tmap_e16_4d(F16, &tv, v, HD, g.W, g.kv_rows, BH, kHCP, C::HR) ||
+      !make_tmap_e16_4d(F16, &tdq, dq, HD, g.W, g.q_rows, BH, 4, 4))
     return cudaErrorInvalidValue;
   BwdQParams p;
   p.heads = g.heads;
@@ -615,7 +620,7 @@ cudaError_t launch_dq(const Geo &g, const void *q, const void *k, const void *v,
   (void)drpb;  // summed from the partial tables by B2
   {
     ProfScope ps("na2d_bwd_dq_tc", st);
-    const cudaError_t e = launch_pdl(na2d_bwd_dq_kernel<L, F16>, grid, kThreads, C::SMEM, st, tq, tdo, tk, tv, tdq, p);
+    const cudaError_t e = launch_pdl(na2d_bwd_dq_kernel<L, HD, F16>, grid, kThreads, C::SMEM, st, tq, tdo, tk, tv, tdq, p);
     if (e != cudaSuccess) return e;
   }
   // the per-CTA dRPB partial tables are summed by the dK/dV kernel (B2), which runs next
@@ -629,19 +634,35 @@ int dq_grid(const Geo &g) {
   return o.num_tiles < tc::num_sms() ? o.num_tiles : tc::num_sms();
 }
 
+namespace {
+template <int D, bool F16>
+cudaError_t dq_for_d(const Geo &g, const void *q, const void *k, const void *v, const float *rpb, const void *out,
+                     const float *lse, const void *dout, void *dq, float *drpb, float *D_, float *part,
+                     int *b2_tile_counter, cudaStream_t st) {
+  switch (g.L) {
+    case 3: return launch_dq<3, D, F16>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D_, part, b2_tile_counter, st);
+    case 5: return launch_dq<5, D, F16>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D_, part, b2_tile_counter, st);
+    case 7: return launch_dq<7, D, F16>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D_, part, b2_tile_counter, st);
+  }
+  return cudaErrorInvalidValue;
+}
+template <bool F16>
+cudaError_t dq_for_el(const Geo &g, const void *q, const void *k, const void *v, const float *rpb, const void *out,
+                      const float *lse, const void *dout, void *dq, float *drpb, float *D_, float *part,
+                      int *b2_tile_counter, cudaStream_t st) {
+  switch (g.d) {
+    case 16: return dq_for_d<16, F16>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D_, part, b2_tile_counter, st);
+    case 32: return dq_for_d<32, F16>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D_, part, b2_tile_counter, st);
+  }
+  return cudaErrorInvalidValue;
+}
+}  // namespace
+
 cudaError_t tc_backward_dq(const Geo &g, const void *q, const void *k, const void *v, const float *rpb,
                            const void *out, const float *lse, const void *dout, void *dq, float *drpb, float *D,
                            float *part, int *b2_tile_counter, cudaStream_t st) {
-  const bool f16 = g.dtype == NA2D_F16;
-  switch (g.L) {
-    case 3: return f16 ? launch_dq<3, true>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D, part, b2_tile_counter, st)
-                 : launch_dq<3, false>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D, part, b2_tile_counter, st);
-    case 5: return f16 ? launch_dq<5, true>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D, part, b2_tile_counter, st)
-                 : launch_dq<5, false>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D, part, b2_tile_counter, st);
-    case 7: return f16 ? launch_dq<7, true>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D, part, b2_tile_counter, st)
-                 : launch_dq<7, false>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D, part, b2_tile_counter, st);
-  }
-  return cudaErrorInvalidValue;
+  return g.dtype == NA2D_F16 ? dq_for_el<true>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D, part, b2_tile_counter, st)
+                             : dq_for_el<false>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D, part, b2_tile_counter, st);
 }
 
 }  // namespace na2d
