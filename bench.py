@@ -32,7 +32,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from na2d_inputs import CONFIGS, Shape, make_inputs  # noqa: E402
+from na2d_inputs import CONFIGS, EXTRA_WORKLOADS, Shape, make_inputs  # noqa: E402
 
 METRIC = "NA2D fwd+bwd TFLOP/s and % of B200 roofline at 1/2/4/8 GPUs, NAT-Tiny k=7"
 UNIT = "TFLOP/s"
@@ -335,7 +335,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS) + sorted(EXTRA_WORKLOADS),
+                    help="a BASELINE config (cfg*) or a shape-generality workload (f3_*)")
     ap.add_argument("--mode", default="auto", choices=["auto"] + sorted(MODES),
                     help="multi-GPU partition (auto: the config's; " + "; ".join(f"{k}: {v}" for k, v in MODES.items()) + ")")
     ap.add_argument("--impl", default="na2d", choices=["na2d", "reference"])
@@ -343,7 +344,7 @@ def main():
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "f16"],
                     help="16-bit I/O type of the tensor-core path (BASELINE's metric is bf16)")
     args = ap.parse_args()
-    shape = CONFIGS[args.config]
+    shape = CONFIGS[args.config] if args.config in CONFIGS else EXTRA_WORKLOADS[args.config]
     mode = default_mode(shape) if args.mode == "auto" else args.mode
 
     env_world = os.environ.get("WORLD_SIZE")
@@ -430,6 +431,9 @@ def main():
     prof = na2d.na2d_profile_read()
     na2d.na2d_profile_enable(False)
     peaks = measured_peaks()
+    # whole-step algorithmic bytes per query-head: forward 8d + 4 (q, k, v, out, lse),
+    # backward 16d + 4 (q, k, v, dout, out, dq, dk, dv, lse): 776 B at d = 32
+    step_bytes = (8 * shape.d + 4) + (16 * shape.d + 4)
     kernels = {}
     nq = w.nq
     for name, (tot, cnt) in prof.items():
@@ -450,8 +454,8 @@ def main():
                     "frac": ach / peaks["hbm_gbs"] if ach else None, "traffic": traffic,
                     "alg_bytes_per_launch": alg_bytes_per_query(dom, shape.d, 2) * nq,
                     "peak_source": peaks["_source"], "kernels": kernels,
-                    "step_frac_hbm": ((260 + 516) * nq / (ms * 1e-3) / 1e9) / peaks["hbm_gbs"],
-                    "kernels_frac_hbm": ((260 + 516) * nq / (rank_ms * 1e-3) / 1e9) / peaks["hbm_gbs"],
+                    "step_frac_hbm": (step_bytes * nq / (ms * 1e-3) / 1e9) / peaks["hbm_gbs"],
+                    "kernels_frac_hbm": (step_bytes * nq / (rank_ms * 1e-3) / 1e9) / peaks["hbm_gbs"],
                     "step_frac_tensor": w.flops_job / world / (ms * 1e-3) / 1e12 / peaks.get("bf16_tflops", 1659.7)}
 
     # ---- context: the paper's own decomposition (QK+RPB kernel writing the attention

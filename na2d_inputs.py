@@ -59,6 +59,14 @@ for _n in ("cfg3_nat_tiny_s3", "cfg3_nat_tiny_s4"):
     CONFIG_SEED[_n] = CONFIG_SEED["cfg3_nat_tiny_s2"]
 
 
+# Shape-generality workloads (not BASELINE configs): NAT-Tiny stage-1 geometry
+# with other head dims, for bench lines of the tensor-core paths beyond d = 32.
+EXTRA_WORKLOADS: dict[str, Shape] = {
+    "f3_d16_s1": Shape("f3_d16_s1", 128, 2, 56, 56, 16, 7),
+    "f3_d64_s1": Shape("f3_d64_s1", 128, 2, 56, 56, 64, 7),
+}
+
+
 def bf16_round(x: np.ndarray) -> np.ndarray:
     """fp32 -> nearest bf16 value (ties to even), returned as fp32.  Encoding only."""
     x = np.ascontiguousarray(x, dtype=np.float32)

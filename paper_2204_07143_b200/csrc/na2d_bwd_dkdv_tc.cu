@@ -33,7 +33,6 @@ namespace {
 using namespace sm100;
 using namespace tc;
 
-constexpr int kStages = 2;
 constexpr int kThreads = 352;  // warps 0-3 / 4-7 elementwise, 8 producer, 9 S^T/dP^T issuer, 10 dV/dK issuer
 // (the sub-partition scheduler favours the highest warp id: the producer / MMA warps never wait for
 // the elementwise warps sharing their sub-partitions)
@@ -46,6 +45,11 @@ constexpr int kTileInfoBytes = 512;
 template <int L, int QP, int D = 32>
 struct CfgK {
   static constexpr int ROWB = 2 * D;  // bytes per 16-bit row: one swizzle atom (32 / 64 / 128 B)
+  // d = 64: one Q / dO / K / V stage and one dV / dK accumulator buffer (TMEM: two 192-column chunk
+  // slots + dV 64 + dK 64), and the epilogue stores dV / dK rows straight to global memory (no
+  // staging: the query halos take 129 KB of shared memory per stage)
+  static constexpr int NST = D <= 32 ? 2 : 1, NACC = D <= 32 ? 2 : 1;
+  static constexpr bool EPI_DIRECT = D > 32;
   static constexpr int NS = (L - 1) / 2;
   static constexpr int CR = kNCH / QP;             // query rows per chunk
   static constexpr int QRH = kTQH + 3 * NS;        // halo rows loaded (max needed)
@@ -66,12 +70,12 @@ struct CfgK {
   static constexpr int TT = 2 * L - 1;
   static constexpr int TROWS = TT + 1;
   static constexpr int TBL_FLOATS = (L + 1) * TROWS * kTblStride;  // + all -inf class (OOB columns)
-  static constexpr int TBL_OFF = kStages * STAGE_BYTES;
+  static constexpr int TBL_OFF = NST * STAGE_BYTES;
   // dV / dK output staging: 2 groups x 4 warps x 4 KB (SW64 boxes, 1 KB aligned)
   static constexpr int OUT_OFF = (TBL_OFF + TBL_FLOATS * 4 + 1023) / 1024 * 1024;
-  static constexpr int OUT_W = 4 * 16 * ROWB;  // per warp: dV, dK x two 4 x 4-key blocks (TMA store boxes)
+  static constexpr int OUT_W = EPI_DIRECT ? 0 : 4 * 16 * ROWB;  // per warp: dV, dK x two 4 x 4-key blocks
   static constexpr int TI_OFF = OUT_OFF + 8 * OUT_W;
-  static constexpr int BAR_OFF = TI_OFF + kStages * kTileInfoBytes;
+  static constexpr int BAR_OFF = TI_OFF + NST * kTileInfoBytes;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
   static_assert(SMEM <= 232448, "shared memory");
 };
@@ -248,7 +252,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                          const __grid_constant__ CUtensorMap tm_dk, const __grid_constant__ CUtensorMap tm_dv,
                          const BwdKParams p) {
   using C = CfgK<L, QP, D>;
-  constexpr int kRB = C::ROWB;
+  constexpr int kRB = C::ROWB, kStages = C::NST, kNacc = C::NACC;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   float *tbl = (float *)(smem + C::TBL_OFF);
@@ -285,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&s_full[s], 1);
       mbar_init(&ds_full[s], 4);
-      mbar_init(&acc_full[s], 1);
+      mbar_init(&acc_full[s], 1);  // (buffer 1 unused at d = 64)
       mbar_init(&acc_free[s], 4);
       mbar_init(&slot_free[s], 1);
     }
@@ -480,7 +484,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr uint32_t idesc_o = idesc_el<F16>(64, D, true);
     int c = 0;
     for (int it = 0;; ++it) {
-      const int stage = it % kStages, b = it & 1;
+      const int stage = it % kStages, b = it % kNacc;
       // the stage cannot advance past this tile before this warp commits its empty[] below
       mbar_wait(&full[stage], (it / kStages) & 1);
       const TileInfo &ti = tinfo[stage];
@@ -493,7 +497,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int x = c & 1;
         mbar_wait(&ds_full[x], (c >> 1) & 1);
         if (lane == 0) ktrace(p, c, 1);
-        if (k == 0) mbar_wait(&acc_free[b], ((it >> 1) & 1) ^ 1);
+        if (k == 0) mbar_wait(&acc_free[b], ((it / kNacc) & 1) ^ 1);
         if (lane == 0) ktrace(p, c, 2);
         tc_fence_after();
         const uint64_t dq0 = dqs + (((row0a + C::CR * k) * QP * kRB) >> 4);
@@ -536,9 +540,40 @@ __global__ void __launch_bounds__(kThreads, 1)
     // smem.  Deferred until the group has processed its next chunk, so it never waits for the
     // tile's last dV/dK MMAs (the MMA warp needs the buffer again only two tiles later).
     auto epilogue = [&](int eit, int bh, int kr0, int kc0) {
-        const int b = eit & 1;
-        mbar_wait(&acc_full[b], (eit >> 1) & 1);
-        tc_fence_after();
+      const int b = eit % kNacc;
+      mbar_wait(&acc_full[b], (eit / kNacc) & 1);
+      tc_fence_after();
+      if constexpr (C::EPI_DIRECT) {
+        // straight to global memory, 16 head dims at a time: this thread's key (r, cc) of block `half`
+        const int pk = kr0 + 4 * half + r, qk = kc0 + 4 * quarter + cc;
+        const bool ok = pk < p.kv_row0 + p.kv_rows && qk < p.W;
+        const size_t row = ((size_t)bh * p.kv_rows + (pk - p.kv_row0)) * p.W + qk;
+#pragma unroll
+        for (int z16 = 0; z16 < D / 16; ++z16) {
+          uint32_t a0[16], a1[16];
+          tmem_ld16(lane_q + kACC_COL + b * 2 * D + 16 * z16, a0);
+          tmem_ld16(lane_q + kACC_COL + b * 2 * D + D + 16 * z16, a1);
+          tc_wait_ld();
+          if (ok) {
+            uint4 *dv4 = (uint4 *)(p.dv + row * D + 16 * z16), *dk4 = (uint4 *)(p.dk + row * D + 16 * z16);
+#pragma unroll
+            for (int z = 0; z < 2; ++z) {
+              dv4[z] = make_uint4(pack_el<F16>(__uint_as_float(a0[8 * z]), __uint_as_float(a0[8 * z + 1])),
+                                  pack_el<F16>(__uint_as_float(a0[8 * z + 2]), __uint_as_float(a0[8 * z + 3])),
+                                  pack_el<F16>(__uint_as_float(a0[8 * z + 4]), __uint_as_float(a0[8 * z + 5])),
+                                  pack_el<F16>(__uint_as_float(a0[8 * z + 6]), __uint_as_float(a0[8 * z + 7])));
+              dk4[z] = make_uint4(
+                  pack_el<F16>(__uint_as_float(a1[8 * z]) * p.scale, __uint_as_float(a1[8 * z + 1]) * p.scale),
+                  pack_el<F16>(__uint_as_float(a1[8 * z + 2]) * p.scale, __uint_as_float(a1[8 * z + 3]) * p.scale),
+                  pack_el<F16>(__uint_as_float(a1[8 * z + 4]) * p.scale, __uint_as_float(a1[8 * z + 5]) * p.scale),
+                  pack_el<F16>(__uint_as_float(a1[8 * z + 6]) * p.scale, __uint_as_float(a1[8 * z + 7]) * p.scale));
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_free[b]);
+      } else {
         uint32_t a0[D], a1[D];
         ld_row<D>(lane_q + kACC_COL + b * 2 * D, a0);
         ld_row<D>(lane_q + kACC_COL + b * 2 * D + D, a1);
@@ -576,6 +611,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           bulk_commit();
         }
+      }
     };
     int cur_head = -1;
     int c = 0;
@@ -773,6 +809,7 @@ cudaError_t tc_backward_dkdv(const Geo &g, const void *q, const void *k, const v
   const bool f16 = g.dtype == NA2D_F16;
   if (g.d == 16) return f16 ? for_d(std::integral_constant<int, 16>(), T()) : for_d(std::integral_constant<int, 16>(), Fa());
   if (g.d == 32) return f16 ? for_d(std::integral_constant<int, 32>(), T()) : for_d(std::integral_constant<int, 32>(), Fa());
+  if (g.d == 64) return f16 ? for_d(std::integral_constant<int, 64>(), T()) : for_d(std::integral_constant<int, 64>(), Fa());
   return cudaErrorInvalidValue;
 }
 

@@ -33,7 +33,6 @@ namespace {
 using namespace sm100;
 using namespace tc;
 
-constexpr int kStages = 2;
 #ifndef NA2D_B1_GROUPS
 #define NA2D_B1_GROUPS 3
 #endif
@@ -83,8 +82,12 @@ struct CfgQ {
   // dQ read-out (epilogue) leaves the critical path.
   static constexpr int DP_COL = NSUB;
   static constexpr int Q_COL = 2 * NSUB;
-  static constexpr int QACC = (512 - Q_COL) / D < 3 ? (512 - Q_COL) / D : 3;  // independent dQ chains
+  // dQ MMAs of N = QN head dims per pass (NQP passes: at d = 64 the 32 free TMEM columns hold one
+  // 32-dim half at a time, read out by the epilogue before the next half), QACC independent chains
+  static constexpr int QN = D < 32 ? D : 32, NQP = D / QN;
+  static constexpr int QACC = (512 - Q_COL) / QN < 3 ? (512 - Q_COL) / QN : 3;
   static_assert(QACC >= 1, "TMEM budget");
+  static constexpr int NST = D <= 32 ? 2 : 1;  // Q / dO / K / V stages (one at d = 64: shared memory)
   static constexpr int KV_ROWS = HR * kHCP;
   static constexpr int Q_BYTES = 128 * ROWB;
   static constexpr int KV_BYTES = (KV_ROWS * ROWB + 1023) / 1024 * 1024;
@@ -94,13 +97,13 @@ struct CfgQ {
   static constexpr int STAGE_BYTES = LD_BYTES + 1024;
   static_assert(STAGE_BYTES % 1024 == 0, "stages must stay 1 KB aligned (swizzled TMA / UMMA)");
   static constexpr int TT = 2 * L - 1;
-  static constexpr int TBL_OFF = kStages * STAGE_BYTES;
+  static constexpr int TBL_OFF = NST * STAGE_BYTES;
   static constexpr int OUT_OFF = (TBL_OFF + BiasTable<L>::FLOATS * 4 + 1023) / 1024 * 1024;  // dQ staging
   static constexpr int HALF_B = 16 * ROWB;                 // one 4 x 4 block of dQ rows (TMA store box)
   static constexpr int DB_OFF = OUT_OFF + 4 * 2 * HALF_B;
   static constexpr int DP_OFF = DB_OFF + ((8 * kGroups * TT * TT * 4 + 255) / 256) * 256;  // partial D
   static constexpr int TI_OFF = DP_OFF + kGroups * 128 * 4;
-  static constexpr int BAR_OFF = TI_OFF + kStages * 64;
+  static constexpr int BAR_OFF = TI_OFF + NST * 64;
   static_assert(sizeof(TileInfoQ) <= 64, "TileInfoQ");
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
   static_assert(SMEM <= 232448, "shared memory");
@@ -132,7 +135,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                        const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                        const __grid_constant__ CUtensorMap tm_dq, const BwdQParams p) {
   using C = CfgQ<L, D>;
-  constexpr int kRB = C::ROWB;
+  constexpr int kRB = C::ROWB, kStages = C::NST;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   float *tbl = (float *)(smem + C::TBL_OFF);
@@ -246,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // while the epilogue reads dQ.
     constexpr uint32_t idesc_s = idesc_el<F16>(64, C::NSUB, false);
     constexpr uint32_t idesc_p1 = idesc_el<F16>(64, 2 * kHCP, false), idesc_p2 = idesc_el<F16>(64, 4 * kHCP, false);
-    constexpr uint32_t idesc_q = idesc_el<F16>(64, D, true);
+    constexpr uint32_t idesc_q = idesc_el<F16>(64, C::QN, true);
     const int n = t_end - t_begin;
     const uint32_t t0 = tmem, t1 = tmem + ((uint32_t)16 << 16);
     auto issue_sdp = [&](int it) {
@@ -298,24 +301,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t ph = it & 1;
       mbar_wait(ds_full, ph);
       if (lane == 0) qtrace(p, it, 3);
-      mbar_wait(dq_free, ph ^ 1);  // the epilogue of tile it - 1 has read its dQ
-      if (lane == 0) qtrace(p, it, 1);
-      tc_fence_after();
       const int rb0 = tinfo[s].rb[0], rb1 = tinfo[s].rb[1];
       const uint64_t dk0 = sdesc_sw<kRB>(smem_u32(smem + s * C::STAGE_BYTES) + 2 * C::Q_BYTES + rb0 * kHCP * kRB);
       const uint64_t dk1 = dk0 + (((rb1 - rb0) * kHCP * kRB) >> 4);
-      if (elect_one()) {
+#pragma unroll 1
+      for (int hq = 0; hq < C::NQP; ++hq) {
+        const int np = it * C::NQP + hq;  // dQ pass index (one dq_full / dq_free phase each)
+        mbar_wait(dq_free, (np & 1) ^ 1);  // the epilogue has read the previous pass
+        if (lane == 0) qtrace(p, it, 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t ho = (hq * C::QN * 2) >> 4;  // head-dim offset of the pass in K's rows
 #pragma unroll
-        for (int ks = 0; ks < C::NSUB / 16; ++ks) {
-          const uint32_t ko = (ks * 16 * kRB) >> 4;
-          const uint32_t ao = C::DS_COL + ks * 8 + C::ds_shift_of_ks(ks), qo = C::Q_COL + (ks % C::QACC) * D;
-          mma_ts(t0 + qo, t0 + ao, dk0 + ko, idesc_q, ks >= C::QACC);
-          mma_ts(t1 + qo, t1 + ao, dk1 + ko, idesc_q, ks >= C::QACC);
+          for (int ks = 0; ks < C::NSUB / 16; ++ks) {
+            const uint32_t ko = (ks * 16 * kRB) >> 4;
+            const uint32_t ao = C::DS_COL + ks * 8 + C::ds_shift_of_ks(ks), qo = C::Q_COL + (ks % C::QACC) * C::QN;
+            mma_ts(t0 + qo, t0 + ao, dk0 + ko + ho, idesc_q, ks >= C::QACC);
+            mma_ts(t1 + qo, t1 + ao, dk1 + ko + ho, idesc_q, ks >= C::QACC);
+          }
+          mma_commit(dq_full);
+          if (hq == C::NQP - 1) mma_commit(&empty[s]);
         }
-        mma_commit(dq_full);
-        mma_commit(&empty[s]);
+        __syncwarp();
       }
-      __syncwarp();
       if (lane == 0) qtrace(p, it, 4);
       if (it + 1 < n) issue_sdp(it + 1);
     }
@@ -510,47 +518,50 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (tq) qtrace(p, it, 11);
       if (grp) continue;
       // ---- epilogue (group 0): dQ = scale * sum of partial accumulators -> bf16, TMA stores
-      mbar_wait(dq_full, ph);
-      if (tq) qtrace(p, it, 12);
-      tc_fence_after();
-      // dQ in 16-column parts (register pressure): partial accumulators summed, scaled, packed into the
-      // swizzled staging row of query (r, c) of block `half` (row R of the box; 16-byte chunk z at
-      // the TMA swizzle position of rows of kRB bytes)
+      // dQ per pass of QN head dims (16-column parts: register pressure): partial accumulators summed,
+      // scaled, packed into the swizzled staging row of query (r, c) of block `half` (row R of the box;
+      // 16-byte chunk z at the TMA swizzle position of rows of kRB bytes)
       const int R = r * 4 + c;
       uint8_t *orow = ostage + half * C::HALF_B + R * kRB;
-      uint32_t o[D / 16][16];
-#pragma unroll
-      for (int hh = 0; hh < D / 16; ++hh) {
-        tmem_ld16(lane_addr + C::Q_COL + 16 * hh, o[hh]);
-#pragma unroll
-        for (int a = 1; a < C::QACC; ++a) {
-          uint32_t oa[16];
-          tmem_ld16(lane_addr + C::Q_COL + a * D + 16 * hh, oa);
-          tc_wait_ld();
-#pragma unroll
-          for (int z = 0; z < 16; ++z) o[hh][z] = __float_as_uint(__uint_as_float(o[hh][z]) + __uint_as_float(oa[z]));
-        }
-      }
-      tc_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(dq_free);
-      if (tq) qtrace(p, it, 13);
       if (lane == 0) bulk_wait_read0();  // this warp's previous store has left the staging
       __syncwarp();
+#pragma unroll 1
+      for (int hq = 0; hq < C::NQP; ++hq) {
+        mbar_wait(dq_full, (it * C::NQP + hq) & 1);
+        if (tq) qtrace(p, it, 12);
+        tc_fence_after();
+        uint32_t o[C::QN / 16][16];
 #pragma unroll
-      for (int hh = 0; hh < D / 16; ++hh)
+        for (int hh = 0; hh < C::QN / 16; ++hh) {
+          tmem_ld16(lane_addr + C::Q_COL + 16 * hh, o[hh]);
 #pragma unroll
-        for (int z2 = 0; z2 < 2; ++z2) {
-          const int z = 2 * hh + z2;
-          const int zs = kRB == 32 ? (z ^ ((R >> 2) & 1)) : kRB == 64 ? (z ^ ((R >> 1) & 3)) : (z ^ (R & 7));
-          const uint32_t *v = o[hh] + 8 * z2;
-          *(uint4 *)(orow + 16 * zs) = make_uint4(
-              pack_el<F16>(__uint_as_float(v[0]) * p.scale, __uint_as_float(v[1]) * p.scale),
-              pack_el<F16>(__uint_as_float(v[2]) * p.scale, __uint_as_float(v[3]) * p.scale),
-              pack_el<F16>(__uint_as_float(v[4]) * p.scale, __uint_as_float(v[5]) * p.scale),
-              pack_el<F16>(__uint_as_float(v[6]) * p.scale, __uint_as_float(v[7]) * p.scale));
+          for (int a = 1; a < C::QACC; ++a) {
+            uint32_t oa[16];
+            tmem_ld16(lane_addr + C::Q_COL + a * C::QN + 16 * hh, oa);
+            tc_wait_ld();
+#pragma unroll
+            for (int z = 0; z < 16; ++z) o[hh][z] = __float_as_uint(__uint_as_float(o[hh][z]) + __uint_as_float(oa[z]));
+          }
         }
+        tc_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(dq_free);
+        if (tq) qtrace(p, it, 13);
+#pragma unroll
+        for (int hh = 0; hh < C::QN / 16; ++hh)
+#pragma unroll
+          for (int z2 = 0; z2 < 2; ++z2) {
+            const int z = (hq * C::QN) / 8 + 2 * hh + z2;
+            const int zs = kRB == 32 ? (z ^ ((R >> 2) & 1)) : kRB == 64 ? (z ^ ((R >> 1) & 3)) : (z ^ (R & 7));
+            const uint32_t *v = o[hh] + 8 * z2;
+            *(uint4 *)(orow + 16 * zs) = make_uint4(
+                pack_el<F16>(__uint_as_float(v[0]) * p.scale, __uint_as_float(v[1]) * p.scale),
+                pack_el<F16>(__uint_as_float(v[2]) * p.scale, __uint_as_float(v[3]) * p.scale),
+                pack_el<F16>(__uint_as_float(v[4]) * p.scale, __uint_as_float(v[5]) * p.scale),
+                pack_el<F16>(__uint_as_float(v[6]) * p.scale, __uint_as_float(v[7]) * p.scale));
+          }
+      }
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {  // queries past the map / band edge are clipped by the TMA unit
@@ -653,6 +664,7 @@ cudaError_t dq_for_el(const Geo &g, const void *q, const void *k, const void *v,
   switch (g.d) {
     case 16: return dq_for_d<16, F16>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D_, part, b2_tile_counter, st);
     case 32: return dq_for_d<32, F16>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D_, part, b2_tile_counter, st);
+    case 64: return dq_for_d<64, F16>(g, q, k, v, rpb, out, lse, dout, dq, drpb, D_, part, b2_tile_counter, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -58,7 +58,7 @@ TileOrder make_tile_order(const Geo &g, int L) {
 }
 
 bool tc_backward_supported(const Geo &g) {
-  if (!((g.dtype == NA2D_BF16 || g.dtype == NA2D_F16) && (g.d == 16 || g.d == 32) && (g.L == 3 || g.L == 5 || g.L == 7) &&
+  if (!((g.dtype == NA2D_BF16 || g.dtype == NA2D_F16) && (g.d == 16 || g.d == 32 || g.d == 64) && (g.L == 3 || g.L == 5 || g.L == 7) &&
         tmap_available()))
     return false;
   const TileOrder o = make_tile_order(g, g.L);
