@@ -101,7 +101,10 @@ int na2d_version(void);
 na2d_status na2d_forward(const na2d_problem *p, const void *q, const void *k, const void *v,
                          const float *rpb, void *out, float *lse, void *stream);
 
-/* Device workspace (bytes) na2d_backward needs for this problem (D, dRPB partials). */
+/* Device workspace (bytes) na2d_backward needs for this problem: D (fp32 per query) plus the
+ * tensor-core path's per-CTA dRPB partial tables, or the SIMT path's per-query window-slot dS
+ * (B*heads*H*W*L*L fp32).  Both paths sum dRPB in a fixed order: drpb is bitwise reproducible for a
+ * given problem and device. */
 size_t na2d_backward_workspace_bytes(const na2d_problem *p);
 
 /* Backward pass, steps a6-a10.  out and lse must be the na2d_forward results for the same

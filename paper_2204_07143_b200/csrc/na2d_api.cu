@@ -66,10 +66,10 @@ bool use_tc(const Geo &g, int which) {
   return which == 0 ? tc_forward_supported(g) : tc_backward_supported(g);
 }
 
-// Workspace: [D fp32 per query | tensor-core backward scratch]
+// Workspace: [D fp32 per query | tensor-core backward scratch, or the SIMT path's per-query window-slot dS]
 size_t bwd_ws(const Geo &g) {
   size_t b = align_up(n_query(g) * sizeof(float));
-  if (use_tc(g, 1)) b += align_up(tc_backward_scratch_bytes(g));
+  b += align_up(use_tc(g, 1) ? tc_backward_scratch_bytes(g) : simt_backward_scratch_bytes(g));
   return b;
 }
 
@@ -149,7 +149,8 @@ na2d_status na2d_backward(const na2d_problem *p, const void *q, const void *k, c
     void *scratch = (char *)workspace + align_up(n_query(g) * sizeof(float));
     return cuda_status(tc_backward(g, q, k, v, rpb, out, lse, dout, dq, dk, dv, drpb, D, scratch, st));
   }
-  return cuda_status(simt_backward(g, q, k, v, rpb, out, lse, dout, dq, dk, dv, drpb, D, st));
+  float *ds_slots = (float *)((char *)workspace + align_up(n_query(g) * sizeof(float)));
+  return cuda_status(simt_backward(g, q, k, v, rpb, out, lse, dout, dq, dk, dv, drpb, D, ds_slots, st));
 }
 
 size_t na2d_paper_attn_bytes(const na2d_problem *p) {

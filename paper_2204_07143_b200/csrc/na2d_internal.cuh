@@ -47,9 +47,12 @@ template <> __device__ __forceinline__ __half from_f32<__half>(float x) { return
 // SIMT path (any even dim <= 128, any odd L <= 31, fp32 or bf16): na2d_simt.cu
 cudaError_t simt_forward(const Geo &g, const void *q, const void *k, const void *v, const float *rpb,
                          void *out, float *lse, cudaStream_t st);
+// ds_slots: scratch of simt_backward_scratch_bytes(g) (per-query window-slot dS, summed per dRPB
+// cell in a fixed order: the SIMT dRPB is bitwise reproducible)
 cudaError_t simt_backward(const Geo &g, const void *q, const void *k, const void *v, const float *rpb,
                           const void *out, const float *lse, const void *dout, void *dq, void *dk,
-                          void *dv, float *drpb, float *D, cudaStream_t st);
+                          void *dv, float *drpb, float *D, float *ds_slots, cudaStream_t st);
+size_t simt_backward_scratch_bytes(const Geo &g);
 int simt_launches(const Geo &g, int which);
 // SIMT dK/dV only (uses D and LSE already computed)
 cudaError_t simt_backward_dkdv(const Geo &g, const void *q, const void *k, const void *v, const float *rpb,

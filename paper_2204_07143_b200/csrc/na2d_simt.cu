@@ -87,17 +87,14 @@ __global__ void __launch_bounds__(kThreads) dq_simt(Geo g, const T *__restrict__
                                                     const T *__restrict__ v, const float *__restrict__ rpb,
                                                     const float *__restrict__ lse, const T *__restrict__ dout,
                                                     const float *__restrict__ D, T *__restrict__ dq,
-                                                    float *__restrict__ drpb) {
-  extern __shared__ float sdb[];  // [TT*TT] per-block dB partial (one head per block row)
+                                                    float *__restrict__ ds_slots) {
+  // ds_slots (when the problem has a bias table): scale * dS of query qi, window slot (p - si, q - sj)
+  // at [qi * L * L + slot]; drpb_reduce sums them per cell in a fixed order (no atomics)
   const int TT = 2 * g.L - 1;
   const long nq = (long)g.q_rows * g.W;
   const int li = wlen(g.H, g.L), lj = wlen(g.W, g.L);
   for (int bh = blockIdx.y; bh < g.B * g.heads; bh += gridDim.y) {
     const int h = bh % g.heads;
-    if (rpb) {
-      for (int c = threadIdx.x; c < TT * TT; c += blockDim.x) sdb[c] = 0.f;
-      __syncthreads();
-    }
     const T *kb = k + (size_t)bh * g.kv_rows * g.W * g.d;
     const T *vb = v + (size_t)bh * g.kv_rows * g.W * g.d;
     for (long t = (long)blockIdx.x * blockDim.x + threadIdx.x; t < nq; t += (long)gridDim.x * blockDim.x) {
@@ -129,20 +126,46 @@ __global__ void __launch_bounds__(kThreads) dq_simt(Geo g, const T *__restrict__
 #pragma unroll
           for (int c = 0; c < DMAX; ++c)
             if (c < g.d) acc[c] = fmaf(dS, to_f32(kb[kidx + c]), acc[c]);
-          if (rpb) atomicAdd(&sdb[cell], g.scale * dS);
+          if (rpb) ds_slots[qi * g.L * g.L + (p - si) * g.L + (qq - sj)] = g.scale * dS;
         }
       }
 #pragma unroll
       for (int c = 0; c < DMAX; ++c)
         if (c < g.d) dq[qi * g.d + c] = from_f32<T>(g.scale * acc[c]);
     }
-    if (rpb) {
-      __syncthreads();
-      for (int c = threadIdx.x; c < TT * TT; c += blockDim.x)
-        if (sdb[c] != 0.f) atomicAdd(&drpb[(size_t)h * TT * TT + c], sdb[c]);
-      __syncthreads();
+  }
+}
+
+// a10: dB[h][a][c] = sum over (b, i, j) of scale * dS at the window slot whose key is
+// (i + a - L + 1, j + c - L + 1), one block per (head, cell): strided partial sums in a fixed order,
+// then a fixed shared-memory tree (bitwise reproducible for a given launch configuration)
+__global__ void __launch_bounds__(256) drpb_reduce_simt(Geo g, const float *__restrict__ ds_slots,
+                                                        float *__restrict__ drpb) {
+  __shared__ float red[256];
+  const int TT = 2 * g.L - 1;
+  const int h = blockIdx.x / (TT * TT), cell = blockIdx.x % (TT * TT);
+  const int ro = cell / TT - (g.L - 1), co = cell % TT - (g.L - 1);  // key - query offsets
+  const int li = wlen(g.H, g.L), lj = wlen(g.W, g.L);
+  const long nq = (long)g.q_rows * g.W;
+  float acc = 0.f;
+  for (long t = threadIdx.x; t < (long)g.B * nq; t += 256) {
+    const int b = (int)(t / nq);
+    const long r = t - (long)b * nq;
+    const int i = (int)(r / g.W) + g.q_row0, j = (int)(r % g.W);
+    const int p = i + ro, qq = j + co;
+    const int si = wstart(i, g.H, g.L), sj = wstart(j, g.W, g.L);
+    if (p >= si && p < si + li && qq >= sj && qq < sj + lj) {
+      const size_t qi = ((size_t)b * g.heads + h) * nq + r;
+      acc += ds_slots[qi * g.L * g.L + (p - si) * g.L + (qq - sj)];
     }
   }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) drpb[(size_t)h * TT * TT + cell] = red[0];
 }
 
 // a8: thread per key, looping over the queries whose window contains it (|i - p| <= L - 1).
@@ -226,7 +249,7 @@ cudaError_t fwd_t(const Geo &g, const void *q, const void *k, const void *v, con
 template <typename T, int DMAX>
 cudaError_t bwd_t(const Geo &g, const void *q, const void *k, const void *v, const float *rpb, const void *out,
                   const float *lse, const void *dout, void *dq, void *dk, void *dv, float *drpb, float *D,
-                  cudaStream_t st) {
+                  float *ds_slots, cudaStream_t st) {
   const long nq = (long)g.B * g.heads * g.q_rows * g.W;
   const int TT = 2 * g.L - 1;
   long nb = (nq + 255) / 256;
@@ -236,17 +259,19 @@ cudaError_t bwd_t(const Geo &g, const void *q, const void *k, const void *v, con
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  if (rpb) {
-    e = cudaMemsetAsync(drpb, 0, sizeof(float) * g.heads * TT * TT, st);
-    if (e != cudaSuccess) return e;
-  }
   {
   ProfScope ps("na2d_bwd_dq_simt", st);
-  dq_simt<T, DMAX><<<grid_for((long)g.q_rows * g.W, g.B * g.heads), kThreads, rpb ? sizeof(float) * TT * TT : 0, st>>>(
-      g, (const T *)q, (const T *)k, (const T *)v, rpb, lse, (const T *)dout, D, (T *)dq, drpb);
+  dq_simt<T, DMAX><<<grid_for((long)g.q_rows * g.W, g.B * g.heads), kThreads, 0, st>>>(
+      g, (const T *)q, (const T *)k, (const T *)v, rpb, lse, (const T *)dout, D, (T *)dq, ds_slots);
   }
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  if (rpb) {
+    ProfScope ps("na2d_bwd_drpb_simt", st);
+    drpb_reduce_simt<<<g.heads * TT * TT, 256, 0, st>>>(g, ds_slots, drpb);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
   ProfScope ps("na2d_bwd_dkdv_simt", st);
   dkdv_simt<T, DMAX><<<grid_for((long)g.kv_rows * g.W, g.B * g.heads), kThreads, 0, st>>>(
       g, (const T *)q, (const T *)k, (const T *)v, rpb, lse, (const T *)dout, D, (T *)dk, (T *)dv);
@@ -279,15 +304,19 @@ cudaError_t simt_forward(const Geo &g, const void *q, const void *k, const void 
 
 cudaError_t simt_backward(const Geo &g, const void *q, const void *k, const void *v, const float *rpb,
                           const void *out, const float *lse, const void *dout, void *dq, void *dk, void *dv,
-                          float *drpb, float *D, cudaStream_t st) {
+                          float *drpb, float *D, float *ds_slots, cudaStream_t st) {
   if (g.dtype == NA2D_F32)
-    return NA2D_DISPATCH_D(bwd_t, float, g, q, k, v, rpb, out, lse, dout, dq, dk, dv, drpb, D, st);
+    return NA2D_DISPATCH_D(bwd_t, float, g, q, k, v, rpb, out, lse, dout, dq, dk, dv, drpb, D, ds_slots, st);
   if (g.dtype == NA2D_F16)
-    return NA2D_DISPATCH_D(bwd_t, __half, g, q, k, v, rpb, out, lse, dout, dq, dk, dv, drpb, D, st);
-  return NA2D_DISPATCH_D(bwd_t, __nv_bfloat16, g, q, k, v, rpb, out, lse, dout, dq, dk, dv, drpb, D, st);
+    return NA2D_DISPATCH_D(bwd_t, __half, g, q, k, v, rpb, out, lse, dout, dq, dk, dv, drpb, D, ds_slots, st);
+  return NA2D_DISPATCH_D(bwd_t, __nv_bfloat16, g, q, k, v, rpb, out, lse, dout, dq, dk, dv, drpb, D, ds_slots, st);
 }
 
-int simt_launches(const Geo &, int which) { return which == 0 ? 1 : 3; }
+size_t simt_backward_scratch_bytes(const Geo &g) {
+  return sizeof(float) * (size_t)g.B * g.heads * g.q_rows * g.W * g.L * g.L;
+}
+
+int simt_launches(const Geo &, int which) { return which == 0 ? 1 : 4; }
 
 cudaError_t simt_backward_dkdv(const Geo &g, const void *q, const void *k, const void *v, const float *rpb,
                                const float *lse, const void *dout, const float *D, void *dk, void *dv,

@@ -290,3 +290,20 @@ def test_every_output_element_written(shape, dtype):
                                shape.d ** -0.5)
     compare({n: x.float().cpu().numpy() for n, x in got.items()}, ref, dtype,
             names=["out", "lse", "dq", "dk", "dv", "drpb"])
+
+
+@pytest.mark.parametrize("dtype,d", [("f32", 32), ("bf16", 32), ("bf16", 128)])
+def test_drpb_bitwise_reproducible(dtype, d):
+    """dRPB is summed in a fixed order on both paths (tcgen05: per-CTA tables reduced in CTA order;
+    SIMT: per-query window-slot dS reduced per cell in a fixed order): two runs give identical bits."""
+    import torch
+    import paper_2204_07143_b200 as na2d
+    shape = Shape(f"det_{dtype}_d{d}", 2, 2, 19, 23, d, 7)
+    inp = make_inputs(shape, seed=5, dtype=dtype)
+    el = {"f32": torch.float32, "bf16": torch.bfloat16}[dtype]
+    t = {n: torch.from_numpy(inp[n]).cuda().to(el) for n in ("q", "k", "v", "dout")}
+    rpb = torch.from_numpy(inp["rpb"]).cuda()
+    out, lse = na2d.forward(t["q"], t["k"], t["v"], rpb, 7)
+    a = na2d.backward(t["q"], t["k"], t["v"], rpb, out, lse, t["dout"], 7)[3].clone()
+    b = na2d.backward(t["q"], t["k"], t["v"], rpb, out, lse, t["dout"], 7)[3].clone()
+    assert torch.equal(a, b)
