@@ -17,8 +17,12 @@ cases = [
     (Shape("s5", 1, 2, 13, 21, 32, 5), "bf16"),
     (Shape("s3", 1, 1, 9, 18, 32, 3), "bf16"),
     (Shape("f32", 1, 2, 11, 14, 32, 7), "f32"),
+    (Shape("d16", 2, 2, 19, 37, 16, 7), "bf16"),  # tcgen05, 32-byte swizzled rows
+    (Shape("d64", 2, 2, 19, 37, 64, 7), "bf16"),  # tcgen05, 128-byte rows, single stage, dQ in two passes
+    (Shape("d64k5f16", 1, 2, 13, 21, 64, 5), "f16"),
+    (Shape("d128", 1, 2, 11, 14, 128, 7), "bf16"),  # SIMT (incl. the fixed-order dRPB reduction)
 ]
-only = sys.argv[1:]  # optional case names (s7 s5 s3 f32 paper)
+only = sys.argv[1:]  # optional case names (s7 s5 s3 f32 d16 d64 d64k5f16 d128 paper)
 for s, dt in cases:
     if only and s.name not in only:
         continue
