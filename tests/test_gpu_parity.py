@@ -186,10 +186,11 @@ def test_large_bias_range(L):
         log_errors(f"{shape.name}x{mul:g}", "bf16", compare(got, ref, "bf16"))
 
 
-@pytest.mark.parametrize("dtype", ["bf16", "f32", "f16"])
-def test_row_band(dtype):
-    """Band call (global coordinates) == oracle band call, incl. dk/dv partials."""
-    shape = Shape("band", 2, 2, 40, 27, 32, 7)
+@pytest.mark.parametrize("dtype,d", [("bf16", 32), ("f32", 32), ("f16", 32), ("bf16", 16), ("bf16", 64)])
+def test_row_band(dtype, d):
+    """Band call (global coordinates) == oracle band call, incl. dk/dv partials (d = 16 / 64: the
+    head-dim variants of the tcgen05 kernels in band geometry)."""
+    shape = Shape("band", 2, 2, 40, 27, d, 7)
     inp = make_inputs(shape, seed=77, dtype=dtype)
     import oracle
     for r0, r1 in [(0, 20), (20, 40), (13, 29)]:
@@ -197,8 +198,8 @@ def test_row_band(dtype):
         k1 = oracle.window_start(r1 - 1, 40, 7) + 7
         sub = dict(q=inp["q"][:, :, r0:r1], k=inp["k"][:, :, k0:k1], v=inp["v"][:, :, k0:k1],
                    dout=inp["dout"][:, :, r0:r1], rpb=inp["rpb"])
-        ref = run_oracle(sub, 7, 32 ** -0.5, H=40, q_row0=r0, kv_row0=k0)
-        got = run_cuda(sub, 7, 32 ** -0.5, dtype, H=40, q_row0=r0, kv_row0=k0)
+        ref = run_oracle(sub, 7, d ** -0.5, H=40, q_row0=r0, kv_row0=k0)
+        got = run_cuda(sub, 7, d ** -0.5, dtype, H=40, q_row0=r0, kv_row0=k0)
         compare(got, ref, dtype)
 
 
