@@ -263,7 +263,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t *slot_free = s_full + 8;  // chunk slot x: the dV/dK MMAs reading it have completed
   uint32_t *tmem_slot = (uint32_t *)(bars + 2 * kStages + 10);
 
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // broadcast from lane 0 so the compiler treats the warp index (and the TMEM addresses
+  // derived from it) as warp-uniform: they stay in uniform registers, no R2UR per tcgen05.ld
+  const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x / 32, 0), lane = threadIdx.x % 32;
   const int q_end = p.q_row0 + p.q_rows;
 
   // zero the never-loaded tail rows of the Q / dO halos (read by partial chunks)

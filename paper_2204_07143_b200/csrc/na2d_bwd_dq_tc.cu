@@ -147,7 +147,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t *sp_part = sp_full + 4;  // [kGroups]: S / dP columns of group g's row pairs (NA2D_B1_SPLIT)
   uint32_t *tmem_slot = (uint32_t *)(bars + 2 * kStages + 4 + kGroups);
 
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // broadcast from lane 0 so the compiler treats the warp index (and the TMEM addresses
+  // derived from it) as warp-uniform: they stay in uniform registers, no R2UR per tcgen05.ld
+  const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x / 32, 0), lane = threadIdx.x % 32;
   const int t_begin = (int)((long)p.num_tiles * blockIdx.x / gridDim.x);
   const int t_end = (int)((long)p.num_tiles * (blockIdx.x + 1) / gridDim.x);
   const int q_end = p.q_row0 + p.q_rows;
