@@ -98,7 +98,8 @@ struct CfgQ {
   static_assert(STAGE_BYTES % 1024 == 0, "stages must stay 1 KB aligned (swizzled TMA / UMMA)");
   static constexpr int TT = 2 * L - 1;
   static constexpr int TBL_OFF = NST * STAGE_BYTES;
-  static constexpr int OUT_OFF = (TBL_OFF + BiasTable<L>::FLOATS * 4 + 1023) / 1024 * 1024;  // dQ staging
+  // two parity copies of the masked bias table (8-byte aligned element pairs: LDS.64)
+  static constexpr int OUT_OFF = (TBL_OFF + 2 * BiasTable<L>::FLOATS * 4 + 1023) / 1024 * 1024;  // dQ staging
   static constexpr int HALF_B = 16 * ROWB;                 // one 4 x 4 block of dQ rows (TMA store box)
   static constexpr int DB_OFF = OUT_OFF + 4 * 2 * HALF_B;
   static constexpr int DP_OFF = DB_OFF + ((8 * kGroups * TT * TT * 4 + 255) / 256) * 256;  // partial D
@@ -412,7 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (h != cur_head) {
           if (p.rpb) commit_head(cur_head);
           named_bar_sync(1, kEw);
-          BiasTable<L>::build_elems(tbl, p.rpb, h, Lw, sl2, gtid, kEw);  // (measured fastest here)
+          BiasTable<L>::build_elems2(tbl, p.rpb, h, Lw, sl2, gtid, kEw);  // (measured fastest here)
           named_bar_sync(1, kEw);
           cur_head = h;
         }
@@ -425,7 +426,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const bool qvalid = i < q_end && j < p.W;
       const size_t qi = ((size_t)bh * p.q_rows + (ic - p.q_row0)) * p.W + jc;
-      const float *tcls = tbl + dc * BiasTable<L>::TROWS * kTblStride + kTblOff + bcol0;
+      // parity copy: row starts (and so every element pair z, z + 1 with z even) 8-byte aligned
+      const int cpar = bcol0 & 1;
+      const float *tcls = tbl + cpar * BiasTable<L>::FLOATS + dc * BiasTable<L>::TROWS * kTblStride + kTblOff + cpar + bcol0;
       const bool tq = grp == 0 && quarter == 2 && lane == 0;
       if (tq) qtrace(p, it, 8);
       const float nlse2 = -((const float *)(smem + stage * C::STAGE_BYTES + C::LSE_OFF))[half * 64 + quarter * 16 + r * 4 + c];
@@ -450,23 +453,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float *ta = tcls + (rva ? pr - ic + L - 1 : C::TT) * kTblStride;
         const float *tb = tcls + (rvb ? pr + 1 - ic + L - 1 : C::TT) * kTblStride;
         tc_wait_ld();
-        float2 da = make_float2(0.f, 0.f), db = make_float2(0.f, 0.f);
+        // two accumulators per row (shorter dependent FFMA2 chains behind the exp2 results)
+        float2 da[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)}, db[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
         for (int z = 0; z < C::UCW; z += 2) {
-          const float2 tta = make_float2(ta[z], ta[z + 1]), ttb = make_float2(tb[z], tb[z + 1]);
+          const float2 tta = *reinterpret_cast<const float2 *>(ta + z), ttb = *reinterpret_cast<const float2 *>(tb + z);
           const float2 xa = __fadd2_rn(__ffma2_rn(make_float2(__uint_as_float(sa[z]), __uint_as_float(sa[z + 1])),
                                                   sl2x2, tta), nlse2x2);
           const float2 xb = __fadd2_rn(__ffma2_rn(make_float2(__uint_as_float(sb_[z]), __uint_as_float(sb_[z + 1])),
                                                   sl2x2, ttb), nlse2x2);
           const float2 Pa = make_float2(ex2(xa.x), ex2(xa.y)), Pb = make_float2(ex2(xb.x), ex2(xb.y));
-          da = __ffma2_rn(Pa, make_float2(__uint_as_float(pa_[z]), __uint_as_float(pa_[z + 1])), da);
-          db = __ffma2_rn(Pb, make_float2(__uint_as_float(pb_[z]), __uint_as_float(pb_[z + 1])), db);
+          const int w = (z >> 1) & 1;
+          da[w] = __ffma2_rn(Pa, make_float2(__uint_as_float(pa_[z]), __uint_as_float(pa_[z + 1])), da[w]);
+          db[w] = __ffma2_rn(Pb, make_float2(__uint_as_float(pb_[z]), __uint_as_float(pb_[z + 1])), db[w]);
           sa[z] = __float_as_uint(Pa.x);
           sa[z + 1] = __float_as_uint(Pa.y);
           sb_[z] = __float_as_uint(Pb.x);
           sb_[z + 1] = __float_as_uint(Pb.y);
         }
-        Dq += (da.x + da.y) + (db.x + db.y);
+        Dq += ((da[0].x + da[1].x) + (da[0].y + da[1].y)) + ((db[0].x + db[1].x) + (db[0].y + db[1].y));
         st_row<C::UCW>(ca, sa);
         st_row<C::UCW>(ca + kHCP, sb_);
       }

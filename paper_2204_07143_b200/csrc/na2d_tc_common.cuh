@@ -40,6 +40,19 @@ struct BiasTable {
       tbl[e] = v;
     }
   }
+  // two copies, copy x holding column b at kTblOff + x + b (copy x at tbl + x * FLOATS): a reader
+  // whose first column has parity x uses copy x, so its element pairs are 8-byte aligned (LDS.64)
+  __device__ static void build_elems2(float *tbl, const float *rpb, int h, int Lw, float mul, int tid, int nthreads) {
+    for (int e = tid; e < 2 * FLOATS; e += nthreads) {
+      const int x = e >= FLOATS, ex = e - x * FLOATS;
+      const int dc = ex / (TROWS * kTblStride);
+      const int rr = (ex / kTblStride) % TROWS;
+      const int cb = ex % kTblStride - kTblOff - x;
+      float v = -INFINITY;
+      if (rr < TT && cb >= dc && cb < dc + Lw) v = rpb ? __ldg(&rpb[(h * TT + rr) * TT + cb]) * mul : 0.f;
+      tbl[e] = v;
+    }
+  }
   // one table row per thread: the row's 2L-1 bias values are loaded together (independent loads),
   // then the row's kTblStride entries written
   __device__ static void build_rows(float *tbl, const float *rpb, int h, int Lw, float mul, int tid, int nthreads) {
