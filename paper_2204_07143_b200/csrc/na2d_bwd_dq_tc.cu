@@ -151,8 +151,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // broadcast from lane 0 so the compiler treats the warp index (and the TMEM addresses
   // derived from it) as warp-uniform: they stay in uniform registers, no R2UR per tcgen05.ld
   const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x / 32, 0), lane = threadIdx.x % 32;
-  const int t_begin = (int)((long)p.num_tiles * blockIdx.x / gridDim.x);
-  const int t_end = (int)((long)p.num_tiles * (blockIdx.x + 1) / gridDim.x);
+  const int t_begin = p.ranges.start[blockIdx.x], t_end = p.ranges.start[blockIdx.x + 1];
   const int q_end = p.q_row0 + p.q_rows;
   if (threadIdx.x == 0) qtrace_gt(p, 16);
 
@@ -635,6 +634,7 @@ cudaError_t launch_dq(const Geo &g, const void *q, const void *k, const void *v,
   p.b2_tile_counter = b2_tile_counter;
   p.trace = (long long *)debug_trace_buffer();
   const int grid = dq_grid(g);
+  make_b1_ranges(p.order, g, grid, &p.ranges);
   (void)drpb;  // summed from the partial tables by B2
   {
     ProfScope ps("na2d_bwd_dq_tc", st);
@@ -649,7 +649,8 @@ cudaError_t launch_dq(const Geo &g, const void *q, const void *k, const void *v,
 
 int dq_grid(const Geo &g) {
   const TileOrder o = make_tile_order(g, g.L);
-  return o.num_tiles < tc::num_sms() ? o.num_tiles : tc::num_sms();
+  const int grid = o.num_tiles < tc::num_sms() ? o.num_tiles : tc::num_sms();
+  return grid < kMaxB1Ctas ? grid : kMaxB1Ctas;
 }
 
 namespace {

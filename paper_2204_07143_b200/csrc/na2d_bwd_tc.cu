@@ -57,6 +57,73 @@ TileOrder make_tile_order(const Geo &g, int L) {
   return o;
 }
 
+void make_b1_ranges(const TileOrder &o, const Geo &g, int grid, B1Ranges *r) {
+  // (class, head) segments of the visiting order (TileOrder::decode), as lengths in tiles
+  int seg[2 * TileOrder::kMaxGroups * TileOrder::kMaxGroups * 64];
+  int ns = 0;
+  const int cap = (int)(sizeof(seg) / sizeof(seg[0]));
+  auto per_map = [&](int a, int b) { return o.rg_count[a] * o.cg_count[b]; };
+  auto push = [&](int n) {
+    if (n > 0 && ns < cap) seg[ns++] = n;
+  };
+  bool ok = (long)o.n_rg * o.n_cg * g.heads <= cap;
+  if (ok && o.class_major) {
+    for (int a = 0; a < o.n_rg; ++a)
+      for (int b = 0; b < o.n_cg; ++b)
+        for (int h = 0; h < g.heads; ++h) push(g.B * per_map(a, b));
+  } else if (ok) {
+    if (o.int_rg >= 0 && o.int_cg >= 0)
+      for (int h = 0; h < g.heads; ++h) push(g.B * per_map(o.int_rg, o.int_cg));
+    for (int h = 0; h < g.heads; ++h)
+      for (int a = 0; a < o.n_rg; ++a)
+        for (int b = 0; b < o.n_cg; ++b)
+          if (a != o.int_rg || b != o.int_cg) push(g.B * per_map(a, b));
+  }
+  const int n = o.num_tiles;
+  long total = 0;
+  for (int i = 0; i < ns; ++i) total += seg[i];
+  if (!ok || total != n || grid <= 1) {
+    for (int c = 0; c <= grid; ++c) r->start[c] = (int)((long)n * c / grid);
+    return;
+  }
+  // greedy fill to a cost target T (tiles + kSwitchCost per segment change inside a range), the
+  // smallest T whose ranges cover all tiles with `grid` CTAs (bisection; costs in quarter tiles)
+  constexpr int kSwitchCost = 6;  // 1.5 tiles
+  auto fill = [&](long T, bool write) {
+    int c = 0, si = 0, left = seg[0], t = 0;
+    while (c < grid) {
+      if (write) r->start[c] = t;
+      long cost = 0;
+      bool first = true;
+      while (t < n) {
+        if (left == 0) {
+          ++si;
+          left = seg[si];
+          if (!first) {
+            if (cost + kSwitchCost + 4 > T) break;
+            cost += kSwitchCost;
+          }
+        }
+        if (cost + 4 > T && !first) break;
+        cost += 4;
+        ++t;
+        --left;
+        first = false;
+      }
+      ++c;
+    }
+    if (write) r->start[grid] = n;
+    return t >= n;
+  };
+  long lo = 4, hi = 4L * n + 1;  // hi always feasible
+  while (lo < hi) {
+    const long mid = (lo + hi) / 2;
+    if (fill(mid, false)) hi = mid;
+    else lo = mid + 1;
+  }
+  fill(lo, true);
+}
+
 bool tc_backward_supported(const Geo &g) {
   if (!((g.dtype == NA2D_BF16 || g.dtype == NA2D_F16) && (g.d == 16 || g.d == 32 || g.d == 64) && (g.L == 3 || g.L == 5 || g.L == 7) &&
         tmap_available()))

@@ -86,6 +86,17 @@ struct TileOrder {
 // Build the class-grouped order for query tiles of a (band of a) map.
 TileOrder make_tile_order(const Geo &g, int L);
 
+// B1's contiguous tile ranges: CTA c takes tiles [start[c], start[c + 1]) of the order.  A CTA whose
+// range crosses from one (class, head) segment into the next pays a dRPB flush (and on a head
+// change a partial-table commit and a bias-table rebuild): measured ~1.2-1.6 tiles' time each
+// (profiles/r02_b1_balance.txt).  The ranges are chosen so that tiles + kSwitchCost x switches is
+// balanced across CTAs instead of the tile count alone.
+constexpr int kMaxB1Ctas = 256;
+struct B1Ranges {
+  int start[kMaxB1Ctas + 1];
+};
+void make_b1_ranges(const TileOrder &o, const Geo &g, int grid, B1Ranges *r);
+
 struct BwdQParams {
   int heads, H, W, q_rows, q_row0, kv_row0;
   int num_tiles;
@@ -98,6 +109,7 @@ struct BwdQParams {
   float *D;          // [B*heads*q_rows*W] written
   float *drpb_part;  // [grid][heads][TT*TT] partial tables (null if no rpb)
   int *b2_tile_counter;  // zeroed by this kernel for B2's dynamic tile scheduler
+  B1Ranges ranges;       // per-CTA tile ranges (make_b1_ranges)
   long long *trace;  // debug timeline (na2d_debug_set_trace) or null
 };
 

@@ -4,7 +4,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from na2d_inputs import CONFIGS, make_inputs
 import paper_2204_07143_b200 as na2d
-s = CONFIGS["cfg2_nat_tiny_s1"]
+s = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "cfg2_nat_tiny_s1"]
 inp = make_inputs(s, dtype="bf16", rpb="swin")
 t = {n: torch.from_numpy(inp[n]).cuda().bfloat16() for n in ("q", "k", "v", "dout")}
 rpb = torch.from_numpy(inp["rpb"]).cuda()
@@ -23,6 +23,9 @@ for name, off in (("fwd", 16384), ("B1", 16384 + 512), ("B2", 16384 + 1024)):
     st, en = b[off:off + 296:2], b[off + 1:off + 297:2]
     ok = (st > 0) & (en > 0)
     st, en = st[ok], en[ok]
+    if not ok.any():
+        print(f"{name}: no span recorded")
+        continue
     t0 = st.min()
     dur = (en - st) / 1e3
     print(f"{name}: CTAs {ok.sum()}  kernel span {(en.max() - t0) / 1e3:.1f} us  start spread {(st.max() - t0) / 1e3:.1f} us  "
