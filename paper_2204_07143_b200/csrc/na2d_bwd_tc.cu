@@ -80,48 +80,37 @@ void make_b1_ranges(const TileOrder &o, const Geo &g, int grid, B1Ranges *r) {
           if (a != o.int_rg || b != o.int_cg) push(g.B * per_map(a, b));
   }
   const int n = o.num_tiles;
-  long total = 0;
-  for (int i = 0; i < ns; ++i) total += seg[i];
-  if (!ok || total != n || grid <= 1) {
+  long sum = 0;
+  for (int i = 0; i < ns; ++i) sum += seg[i];
+  if (!ok || sum != n || grid <= 1) {
     for (int c = 0; c <= grid; ++c) r->start[c] = (int)((long)n * c / grid);
     return;
   }
-  // greedy fill to a cost target T (tiles + kSwitchCost per segment change inside a range), the
-  // smallest T whose ranges cover all tiles with `grid` CTAs (bisection; costs in quarter tiles)
-  constexpr int kSwitchCost = 6;  // 1.5 tiles
-  auto fill = [&](long T, bool write) {
-    int c = 0, si = 0, left = seg[0], t = 0;
+  // cost of the order as a line: 4 per tile (quarter-tile units) plus kSwitchCost where a segment
+  // starts; CTA c starts at the first tile whose cumulative cost reaches c / grid of the total (a
+  // target that falls on a switch lands on the segment's first tile, so that CTA pays no switch)
+  constexpr long kSwitchCost = 6;  // 1.5 tiles
+  const long total = 4L * n + kSwitchCost * (ns - 1);
+  r->start[0] = 0;
+  int c = 1;
+  long pre = 0;  // cumulative cost before the current segment's first tile (switch included)
+  int s0 = 0;
+  for (int i = 0; i < ns && c < grid; ++i) {
+    if (i > 0) pre += kSwitchCost;
+    const long hi = pre + 4L * seg[i];
     while (c < grid) {
-      if (write) r->start[c] = t;
-      long cost = 0;
-      bool first = true;
-      while (t < n) {
-        if (left == 0) {
-          ++si;
-          left = seg[si];
-          if (!first) {
-            if (cost + kSwitchCost + 4 > T) break;
-            cost += kSwitchCost;
-          }
-        }
-        if (cost + 4 > T && !first) break;
-        cost += 4;
-        ++t;
-        --left;
-        first = false;
-      }
-      ++c;
+      const long tau = (total * c + grid - 1) / grid;
+      if (tau > hi) break;
+      const long k = tau <= pre ? 0 : (tau - pre + 3) / 4;  // tiles of this segment before CTA c
+      int st = s0 + (int)k;
+      if (st < r->start[c - 1]) st = r->start[c - 1];
+      r->start[c++] = st;
     }
-    if (write) r->start[grid] = n;
-    return t >= n;
-  };
-  long lo = 4, hi = 4L * n + 1;  // hi always feasible
-  while (lo < hi) {
-    const long mid = (lo + hi) / 2;
-    if (fill(mid, false)) hi = mid;
-    else lo = mid + 1;
+    pre = hi;
+    s0 += seg[i];
   }
-  fill(lo, true);
+  while (c < grid) r->start[c++] = n;
+  r->start[grid] = n;
 }
 
 bool tc_backward_supported(const Geo &g) {

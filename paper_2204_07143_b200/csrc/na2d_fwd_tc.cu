@@ -201,6 +201,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
   pdl_trigger();
   pdl_wait();  // the previous kernel on the stream is complete: global memory from here on
+#ifdef NA2D_TRACE
+  if (threadIdx.x == 0 && p.trace) {  // per-CTA wall-clock span (load balance, scripts/trace_balance.py)
+    uint64_t gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    p.trace[16384 + 2 * blockIdx.x] = (long long)gt;
+  }
+#endif
 
   if (warp == kProducerWarp) {
     // ================= producer (whole warp converged; one elected thread writes the tile
@@ -547,6 +554,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
+#ifdef NA2D_TRACE
+  if (threadIdx.x == 0 && p.trace) {
+    uint64_t gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    p.trace[16384 + 2 * blockIdx.x + 1] = (long long)gt;
+  }
+#endif
 }
 
 template <int L, int D, bool F16>
