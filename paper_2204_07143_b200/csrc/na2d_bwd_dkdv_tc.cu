@@ -81,7 +81,8 @@ struct CfgK {
 };
 
 struct BwdKParams {
-  int B, heads, H, W, q_rows, q_row0, kv_rows, kv_row0;
+  int B, heads, H, W, q_rows, q_row0, kv_rows, kv_row0;  // B: maps per head (pair mode: map pairs)
+  int pair;  // tc::pair_mode: a key tile holds maps (b, h), (b + 1, h); Q / dO halos are pair views
   int tiles_h, tiles_w, num_tiles;
   int shift_cols;  // last two key tile columns start at W-L-16 and W-16 (key_col0)
   int tma_lsd;  // LSE / D halos by TMA (W * 4 bytes 16-byte aligned) instead of lane loads
@@ -147,7 +148,7 @@ __device__ __forceinline__ KTile ktile(const BwdKParams &p, int t) {
   const int per = p.tiles_h * p.tiles_w;
   const int u = t / per, rem = t - u * per;
   const int h = u / p.B;
-  g.bh = (u - h * p.B) * p.heads + h;
+  g.bh = (p.pair ? 2 : 1) * (u - h * p.B) * p.heads + h;  // (pair mode: member 0)
   g.kr0 = p.kv_row0 + (rem / p.tiles_w) * kTQH;
   g.kc0 = key_col0(p, rem % p.tiles_w, L);
   const int q_end = p.q_row0 + p.q_rows, kv_end = p.kv_row0 + p.kv_rows;
@@ -357,9 +358,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) ktrace(p, it, 14);
       const KTile g = ktile<L, QP>(p, t);
       if (lane < 4) {  // union origin of lane quarter q = lane (warp-uniform in the consumers)
-        const int ucr = (inv_lo(min(g.kc0 + 4 * lane, p.W - 1), p.W, L, 0, p.W) - g.qc0) & ~1;
+        // (pair mode: member lane >> 1's query columns start at halo column (lane >> 1) * QP / 2)
+        const int ucr = p.pair ? ((lane >> 1) * (QP / 2) + inv_lo(min(4 * (lane & 1), p.W - 1), p.W, L, 0, p.W)) & ~1
+                               : (inv_lo(min(g.kc0 + 4 * lane, p.W - 1), p.W, L, 0, p.W) - g.qc0) & ~1;
         // interior quarters (all union columns of class NS, UCWF wide) take the immediate-offset path
-        const bool fast = L < p.W && g.qc0 + ucr >= C::NS && g.qc0 + ucr + C::UCWF - 1 < p.W - C::NS &&
+        const bool fast = !p.pair && L < p.W && g.qc0 + ucr >= C::NS && g.qc0 + ucr + C::UCWF - 1 < p.W - C::NS &&
                           ucr + C::UCWF <= QP;
         ti->uc[lane] = fast ? ucr : min(ucr, QP - C::UCW);
         ti->fast[lane] = fast;
@@ -382,7 +385,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int e = lane; e < 64; e += 32) {  // class offset of union column z of quarter q
         const int q = e >> 4, z = e & 15;
         const int j = g.qc0 + ti->uc[q] + z;
-        const int dcl = j < p.W ? wstart(j, p.W, L) - j + L - 1 : L;
+        int dcl = j < p.W ? wstart(j, p.W, L) - j + L - 1 : L;
+        if (p.pair) {  // a column of the quarter's own member inside the map, else the all -inf class
+          const int m = j / (QP / 2), jl = j - m * (QP / 2);
+          dcl = m == (q >> 1) && jl < p.W ? wstart(jl, p.W, L) - jl + L - 1 : L;
+        }
         ti->colterm[q][z] = dcl * C::TROWS * kTblStride - j;
       }
       __syncwarp();
@@ -400,11 +407,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int qb = 0; qb < 4; ++qb) {
             const int r0 = (64 * sb + 16 * qb) * kRB;
-            tma_load_4d(kt + r0, &tm_k, &full[s], 0, g.kc0 + 4 * qb, g.kr0 - p.kv_row0 + 4 * sb, g.bh);
-            tma_load_4d(kt + C::KT_BYTES + r0, &tm_v, &full[s], 0, g.kc0 + 4 * qb, g.kr0 - p.kv_row0 + 4 * sb, g.bh);
+            const int kc = p.pair ? 4 * (qb & 1) : g.kc0 + 4 * qb, kbh = p.pair ? g.bh + (qb >> 1) * p.heads : g.bh;
+            tma_load_4d(kt + r0, &tm_k, &full[s], 0, kc, g.kr0 - p.kv_row0 + 4 * sb, kbh);
+            tma_load_4d(kt + C::KT_BYTES + r0, &tm_v, &full[s], 0, kc, g.kr0 - p.kv_row0 + 4 * sb, kbh);
           }
-        tma_load_4d(st, &tm_q, &full[s], 0, g.qc0, g.qr0 - p.q_row0, g.bh);
-        tma_load_4d(st + C::Q_BYTES, &tm_do, &full[s], 0, g.qc0, g.qr0 - p.q_row0, g.bh);
+        if (p.pair) {  // both members' query halos side by side (row pitch QP, member m at m * QP / 2)
+          tma_load_5d(st, &tm_q, &full[s], 0, 0, 0, g.qr0 - p.q_row0, g.bh);
+          tma_load_5d(st + C::Q_BYTES, &tm_do, &full[s], 0, 0, 0, g.qr0 - p.q_row0, g.bh);
+        } else {
+          tma_load_4d(st, &tm_q, &full[s], 0, g.qc0, g.qr0 - p.q_row0, g.bh);
+          tma_load_4d(st + C::Q_BYTES, &tm_do, &full[s], 0, g.qc0, g.qr0 - p.q_row0, g.bh);
+        }
       }
       __syncwarp();
       if (!p.tma_lsd) {
@@ -415,11 +428,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int u = 0; u < PER_LANE; ++u) {
           const int e = lane + 32 * u;
-          const int i = g.qr0 + e / C::LP, j = (g.qc0 & ~3) + e % C::LP;
+          const int i = g.qr0 + e / C::LP;
+          int j = (g.qc0 & ~3) + e % C::LP, jbh = g.bh;
+          if (p.pair) {  // halo column -> (member, column)
+            const int m = j / (QP / 2);
+            j -= m * (QP / 2);
+            jbh = m < 2 ? g.bh + m * p.heads : -1;
+          }
           lv[u] = 0.f;
           dv[u] = 0.f;
-          if (e < C::QRH * C::LP && i < q_end && j < p.W) {
-            const size_t qi = ((size_t)g.bh * p.q_rows + (i - p.q_row0)) * p.W + j;
+          if (e < C::QRH * C::LP && i < q_end && j < p.W && jbh >= 0) {
+            const size_t qi = ((size_t)jbh * p.q_rows + (i - p.q_row0)) * p.W + j;
             lv[u] = __ldg(&p.lse[qi]);
             dv[u] = __ldg(&p.D[qi]);
           }
@@ -545,11 +564,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int b = eit % kNacc;
       mbar_wait(&acc_full[b], (eit / kNacc) & 1);
       tc_fence_after();
+      // pair mode: key columns of member quarter >> 1
+      const int ec0 = p.pair ? 4 * (quarter & 1) : kc0 + 4 * quarter, ebh = p.pair ? bh + (quarter >> 1) * p.heads : bh;
       if constexpr (C::EPI_DIRECT) {
         // straight to global memory, 16 head dims at a time: this thread's key (r, cc) of block `half`
-        const int pk = kr0 + 4 * half + r, qk = kc0 + 4 * quarter + cc;
+        const int pk = kr0 + 4 * half + r, qk = ec0 + cc;
         const bool ok = pk < p.kv_row0 + p.kv_rows && qk < p.W;
-        const size_t row = ((size_t)bh * p.kv_rows + (pk - p.kv_row0)) * p.W + qk;
+        const size_t row = ((size_t)ebh * p.kv_rows + (pk - p.kv_row0)) * p.W + qk;
 #pragma unroll
         for (int z16 = 0; z16 < D / 16; ++z16) {
           uint32_t a0[16], a1[16];
@@ -608,8 +629,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {  // out-of-range keys (map / band edge) are clipped by the TMA unit
 #pragma unroll
           for (int sb = 0; sb < 2; ++sb) {
-            tma_store_4d(&tm_dv, ostage + sb * 16 * kRB, 0, kc0 + 4 * quarter, kr0 - p.kv_row0 + 4 * sb, bh);
-            tma_store_4d(&tm_dk, ostage + (2 + sb) * 16 * kRB, 0, kc0 + 4 * quarter, kr0 - p.kv_row0 + 4 * sb, bh);
+            tma_store_4d(&tm_dv, ostage + sb * 16 * kRB, 0, ec0, kr0 - p.kv_row0 + 4 * sb, ebh);
+            tma_store_4d(&tm_dk, ostage + (2 + sb) * 16 * kRB, 0, ec0, kr0 - p.kv_row0 + 4 * sb, ebh);
           }
           bulk_commit();
         }
@@ -641,7 +662,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         cur_head = h;
       }
       // this thread's key
-      const int pk = kr0 + 4 * half + r, qk = kc0 + 4 * quarter + cc;
+      // this thread's key; pair mode: halo column of member quarter >> 1 (bias columns are key - query
+      // differences inside one member, colterm sends the other member's columns to the -inf class)
+      const int pk = kr0 + 4 * half + r,
+                qk = p.pair ? (quarter >> 1) * (QP / 2) + 4 * (quarter & 1) + cc : kc0 + 4 * quarter + cc;
       const float *lsd = (const float *)(smem + stage * C::STAGE_BYTES + 2 * C::Q_BYTES + 2 * C::KT_BYTES);
       const float *tbl_row0 = tbl + kTblOff + qk + L - 1 + (fast ? C::NS * C::TROWS * kTblStride - (qc0 + uc) : 0);
       if (trq) ktrace(p, c, 17 + 4 * grp);
@@ -658,7 +682,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t lane_addr = lane_q + x * kSlot;
         // a quarter whose keys all lie past the map edge only feeds accumulator rows the TMA store
         // clips, so its P / dS columns may hold anything
-        if (kc0 + 4 * quarter < p.W) {
+        if ((p.pair ? 4 * (quarter & 1) : kc0 + 4 * quarter) < p.W) {
           if (fast)
             chunk_rows<L, QP, true, F16>(lane_addr, uc, tbl_row0, colterm, lrow0, pk, i_base, p.H, rows_here, Lh, sl2,
                                     chunk_rows_even<C::CR>(qn0, qn1, k));
@@ -713,20 +737,24 @@ cudaError_t launch_dkdv_t(const Geo &g, const void *q, const void *k, const void
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap tq, tdo, tk, tv, tdk, tdv;
   const int BH = g.B * g.heads;
-  if (!make_tmap_e16_4d(F16, &tq, q, HD, g.W, g.q_rows, BH, QP, C::QRH) ||
-      !make_tmap_e16_4d(F16, &tdo, dout, HD, g.W, g.q_rows, BH, QP, C::QRH) ||
+  const bool pair = pair_mode(g.B, g.H, g.W, g.q_row0, g.q_rows, g.kv_row0, g.kv_rows);
+  if (!(pair ? make_tmap_e16_pair(F16, &tq, q, HD, g.W, g.q_rows, g.heads, BH, QP / 2, C::QRH)
+             : make_tmap_e16_4d(F16, &tq, q, HD, g.W, g.q_rows, BH, QP, C::QRH)) ||
+      !(pair ? make_tmap_e16_pair(F16, &tdo, dout, HD, g.W, g.q_rows, g.heads, BH, QP / 2, C::QRH)
+             : make_tmap_e16_4d(F16, &tdo, dout, HD, g.W, g.q_rows, BH, QP, C::QRH)) ||
       !make_tmap_e16_4d(F16, &tk, k, HD, g.W, g.kv_rows, BH, 4, 4) ||
       !make_tmap_e16_4d(F16, &tv, v, HD, g.W, g.kv_rows, BH, 4, 4) ||
       !make_tmap_e16_4d(F16, &tdk, dk, HD, g.W, g.kv_rows, BH, 4, 4) ||
       !make_tmap_e16_4d(F16, &tdv, dv, HD, g.W, g.kv_rows, BH, 4, 4))
     return cudaErrorInvalidValue;
   CUtensorMap tl, td;
-  const bool tma_lsd = (g.W * 4) % 16 == 0 && make_tmap_f32_3d(&tl, lse, g.W, g.q_rows, BH, C::LP, C::QRH) &&
+  const bool tma_lsd = !pair && (g.W * 4) % 16 == 0 && make_tmap_f32_3d(&tl, lse, g.W, g.q_rows, BH, C::LP, C::QRH) &&
                        make_tmap_f32_3d(&td, D, g.W, g.q_rows, BH, C::LP, C::QRH);
   if (!tma_lsd) tl = td = tq;  // unused
   BwdKParams p;
   p.tma_lsd = tma_lsd ? 1 : 0;
-  p.B = g.B;
+  p.pair = pair ? 1 : 0;
+  p.B = pair ? g.B / 2 : g.B;
   p.heads = g.heads;
   p.H = g.H;
   p.W = g.W;
@@ -736,7 +764,7 @@ cudaError_t launch_dkdv_t(const Geo &g, const void *q, const void *k, const void
   p.kv_row0 = g.kv_row0;
   p.tiles_h = (g.kv_rows + kTQH - 1) / kTQH;
   p.tiles_w = (g.W + kTQW - 1) / kTQW;
-  p.num_tiles = BH * p.tiles_h * p.tiles_w;
+  p.num_tiles = p.B * g.heads * p.tiles_h * p.tiles_w;
   p.shift_cols = 0;
   if (max_query_halo_width(g, false) > QP) p.shift_cols = 1;
   p.scale = g.scale;

@@ -204,8 +204,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int hr0 = wstart(g.i0, p.H, L), hc0 = wstart(g.j0, p.W, L);
       uint8_t *st = smem + s * C::STAGE_BYTES;
       TileInfoQ *ti = tinfo + s;
+      const bool pair = p.order.pair;  // members at halo columns 0 / kHCP / 2 (tc::pair_mode)
       if (lane < 2) ti->rb[lane] = wstart(min(g.i0 + 4 * lane, q_end - 1), p.H, L) - hr0;
-      if (lane < 4) ti->uc[lane] = (wstart(min(g.j0 + 4 * lane, p.W - 1), p.W, L) - hc0) & ~1;
+      if (lane < 4)
+        ti->uc[lane] = (pair ? (lane >> 1) * (kHCP / 2) + wstart(min(4 * (lane & 1), p.W - 1), p.W, L)
+                             : wstart(min(g.j0 + 4 * lane, p.W - 1), p.W, L) - hc0) & ~1;
       if (lane == 0) {
         ti->bh = g.bh;
         ti->i0 = g.i0;
@@ -222,11 +225,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int qb = 0; qb < 4; ++qb) {
             const int r0 = (64 * sb + 16 * qb) * kRB;
-            tma_load_4d(st + r0, &tm_q, &full[s], 0, g.j0 + 4 * qb, g.i0 - p.q_row0 + 4 * sb, g.bh);
-            tma_load_4d(st + C::Q_BYTES + r0, &tm_do, &full[s], 0, g.j0 + 4 * qb, g.i0 - p.q_row0 + 4 * sb, g.bh);
+            const int qc = pair ? 4 * (qb & 1) : g.j0 + 4 * qb, qbh = pair ? g.bh + (qb >> 1) * p.heads : g.bh;
+            tma_load_4d(st + r0, &tm_q, &full[s], 0, qc, g.i0 - p.q_row0 + 4 * sb, qbh);
+            tma_load_4d(st + C::Q_BYTES + r0, &tm_do, &full[s], 0, qc, g.i0 - p.q_row0 + 4 * sb, qbh);
           }
-        tma_load_4d(st + 2 * C::Q_BYTES, &tm_k, &full[s], 0, hc0, hr0 - p.kv_row0, g.bh);
-        tma_load_4d(st + 2 * C::Q_BYTES + C::KV_BYTES, &tm_v, &full[s], 0, hc0, hr0 - p.kv_row0, g.bh);
+        if (pair) {  // both members' halo rows side by side (pair tensor maps, row pitch kHCP)
+          tma_load_5d(st + 2 * C::Q_BYTES, &tm_k, &full[s], 0, 0, 0, hr0 - p.kv_row0, g.bh);
+          tma_load_5d(st + 2 * C::Q_BYTES + C::KV_BYTES, &tm_v, &full[s], 0, 0, 0, hr0 - p.kv_row0, g.bh);
+        } else {
+          tma_load_4d(st + 2 * C::Q_BYTES, &tm_k, &full[s], 0, hc0, hr0 - p.kv_row0, g.bh);
+          tma_load_4d(st + 2 * C::Q_BYTES + C::KV_BYTES, &tm_v, &full[s], 0, hc0, hr0 - p.kv_row0, g.bh);
+        }
       }
       __syncwarp();
       // LSE of query (half, quarter, r, c) at e = half*64 + quarter*16 + r*4 + c; 0 if outside
@@ -234,10 +243,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       float lv[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int e = lane + 32 * u;
-        const int i = g.i0 + 4 * (e >> 6) + ((e >> 2) & 3), j = g.j0 + 4 * ((e >> 4) & 3) + (e & 3);
+        const int e = lane + 32 * u, qq = (e >> 4) & 3;
+        const int i = g.i0 + 4 * (e >> 6) + ((e >> 2) & 3), j = (pair ? 4 * (qq & 1) : g.j0 + 4 * qq) + (e & 3);
+        const int qbh = pair ? g.bh + (qq >> 1) * p.heads : g.bh;
         lv[u] = (i < q_end && j < p.W)
-                    ? __ldg(&p.lse[((size_t)g.bh * p.q_rows + (i - p.q_row0)) * p.W + j]) * 1.4426950408889634f
+                    ? __ldg(&p.lse[((size_t)qbh * p.q_rows + (i - p.q_row0)) * p.W + j]) * 1.4426950408889634f
                     : 0.f;
       }
 #pragma unroll
@@ -402,11 +412,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int rb = ti.rb[half], uc = ti.uc[quarter];
       const int h = bh % p.heads;
       const int key = ti.cls * p.heads + h;
-      const int i = i0 + 4 * half + r, j = j0 + 4 * quarter + c;
+      // pair mode: j is the column inside member quarter >> 1, whose keys start at halo column jv
+      const bool pair = p.order.pair;
+      const int i = i0 + 4 * half + r, j = pair ? 4 * (quarter & 1) + c : j0 + 4 * quarter + c;
+      const int jv = pair ? (quarter >> 1) * (kHCP / 2) : 0, bhq = pair ? bh + (quarter >> 1) * p.heads : bh;
       const int ic = min(i, q_end - 1), jc = min(j, p.W - 1);
       const int si = wstart(ic, p.H, L), sj = wstart(jc, p.W, L);
       const int dc = sj - jc + L - 1;
-      const int brow0 = hr0 + rb - ic + L - 1, bcol0 = hc0 + uc - jc + L - 1;
+      const int brow0 = hr0 + rb - ic + L - 1, bcol0 = hc0 + uc - jc - jv + L - 1;
       if (key != cur_key) {
         if (p.rpb && cur_key >= 0) flush();
         if (h != cur_head) {
@@ -419,12 +432,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         cur_key = key;
         f_valid = i < q_end && j < p.W;
         f_wr = si - hr0 - rb;
-        f_wc = sj - hc0 - uc;
+        f_wc = sj + jv - hc0 - uc;
         f_brow = brow0;
         f_bcol = bcol0;
       }
       const bool qvalid = i < q_end && j < p.W;
-      const size_t qi = ((size_t)bh * p.q_rows + (ic - p.q_row0)) * p.W + jc;
+      const size_t qi = ((size_t)bhq * p.q_rows + (ic - p.q_row0)) * p.W + jc;
       // parity copy: row starts (and so every element pair z, z + 1 with z even) 8-byte aligned
       const int cpar = bcol0 & 1;
       const float *tcls = tbl + cpar * BiasTable<L>::FLOATS + dc * BiasTable<L>::TROWS * kTblStride + kTblOff + cpar + bcol0;
@@ -571,8 +584,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {  // queries past the map / band edge are clipped by the TMA unit
-        tma_store_4d(&tm_dq, ostage, 0, j0 + 4 * quarter, i0 - p.q_row0, bh);
-        tma_store_4d(&tm_dq, ostage + C::HALF_B, 0, j0 + 4 * quarter, i0 - p.q_row0 + 4, bh);
+        const int oc = pair ? 4 * (quarter & 1) : j0 + 4 * quarter;
+        tma_store_4d(&tm_dq, ostage, 0, oc, i0 - p.q_row0, bhq);
+        tma_store_4d(&tm_dq, ostage + C::HALF_B, 0, oc, i0 - p.q_row0 + 4, bhq);
         bulk_commit();
       }
       if (tq) qtrace(p, it, 14);
@@ -608,10 +622,13 @@ cudaError_t launch_dq(const Geo &g, const void *q, const void *k, const void *v,
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap tq, tdo, tk, tv, tdq;
   const int BH = g.B * g.heads;
+  const bool pair = pair_mode(g.B, g.H, g.W, g.q_row0, g.q_rows, g.kv_row0, g.kv_rows);
   if (!make_tmap_e16_4d(F16, &tq, q, HD, g.W, g.q_rows, BH, 4, 4) ||
       !make_tmap_e16_4d(F16, &tdo, dout, HD, g.W, g.q_rows, BH, 4, 4) ||
-      !make_tmap_e16_4d(F16, &tk, k, HD, g.W, g.kv_rows, BH, kHCP, C::HR) ||
-      !make_tmap_e16_4d(F16, &tv, v, HD, g.W, g.kv_rows, BH, kHCP, C::HR) ||
+      !(pair ? make_tmap_e16_pair(F16, &tk, k, HD, g.W, g.kv_rows, g.heads, BH, kHCP / 2, C::HR)
+             : make_tmap_e16_4d(F16, &tk, k, HD, g.W, g.kv_rows, BH, kHCP, C::HR)) ||
+      !(pair ? make_tmap_e16_pair(F16, &tv, v, HD, g.W, g.kv_rows, g.heads, BH, kHCP / 2, C::HR)
+             : make_tmap_e16_4d(F16, &tv, v, HD, g.W, g.kv_rows, BH, kHCP, C::HR)) ||
       !make_tmap_e16_4d(F16, &tdq, dq, HD, g.W, g.q_rows, BH, 4, 4))
     return cudaErrorInvalidValue;
   BwdQParams p;

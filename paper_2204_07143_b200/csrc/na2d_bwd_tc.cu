@@ -9,7 +9,8 @@ namespace na2d {
 
 TileOrder make_tile_order(const Geo &g, int L) {
   TileOrder o{};
-  o.B = g.B;
+  o.pair = tc::pair_mode(g.B, g.H, g.W, g.q_row0, g.q_rows, g.kv_row0, g.kv_rows);
+  o.B = o.pair ? g.B / 2 : g.B;
   o.heads = g.heads;
   o.q_row0 = g.q_row0;
   const int ns = (L - 1) / 2, q_end = g.q_row0 + g.q_rows;
@@ -43,13 +44,13 @@ TileOrder make_tile_order(const Geo &g, int L) {
   };
   o.n_rg = groups(tiles_h, tc::kTQH, g.q_row0, q_end, g.H, o.rg_start, o.rg_count, &o.int_rg);
   o.n_cg = groups(tiles_w, tc::kTQW, 0, g.W, g.W, o.cg_start, o.cg_count, &o.int_cg);
-  o.num_tiles = g.B * g.heads * tiles_h * tiles_w;
+  o.num_tiles = o.B * g.heads * tiles_h * tiles_w;
   // class-major unless the smallest class holds so few tiles per head that a CTA's contiguous share
   // would cross more than ~4 heads there
   int min_class = 1 << 30;
   for (int a = 0; a < o.n_rg; ++a)
     for (int b = 0; b < o.n_cg; ++b) {
-      const int c = g.B * o.rg_count[a] * o.cg_count[b];
+      const int c = o.B * o.rg_count[a] * o.cg_count[b];
       min_class = c < min_class ? c : min_class;
     }
   const int grid = o.num_tiles < tc::num_sms() ? o.num_tiles : tc::num_sms();
@@ -70,14 +71,14 @@ void make_b1_ranges(const TileOrder &o, const Geo &g, int grid, B1Ranges *r) {
   if (ok && o.class_major) {
     for (int a = 0; a < o.n_rg; ++a)
       for (int b = 0; b < o.n_cg; ++b)
-        for (int h = 0; h < g.heads; ++h) push(g.B * per_map(a, b));
+        for (int h = 0; h < g.heads; ++h) push(o.B * per_map(a, b));
   } else if (ok) {
     if (o.int_rg >= 0 && o.int_cg >= 0)
-      for (int h = 0; h < g.heads; ++h) push(g.B * per_map(o.int_rg, o.int_cg));
+      for (int h = 0; h < g.heads; ++h) push(o.B * per_map(o.int_rg, o.int_cg));
     for (int h = 0; h < g.heads; ++h)
       for (int a = 0; a < o.n_rg; ++a)
         for (int b = 0; b < o.n_cg; ++b)
-          if (a != o.int_rg || b != o.int_cg) push(g.B * per_map(a, b));
+          if (a != o.int_rg || b != o.int_cg) push(o.B * per_map(a, b));
   }
   const int n = o.num_tiles;
   long sum = 0;

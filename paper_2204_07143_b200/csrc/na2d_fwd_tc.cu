@@ -68,6 +68,7 @@ struct Cfg {
   // single-stage at D = 64 (shared memory)
   static constexpr int SQK = D <= 32 ? 2 : 1, SV = D <= 32 ? 2 : 1;
   static constexpr int HP = kTQW + L - 1;       // halo width = row pitch of the K / V sub-tile buffers
+  static constexpr int PW = HP / 2;             // pair mode: key columns of member m start at m * PW
   static constexpr int UR = 4 + L - 1;          // halo rows of a sub-tile (4 query rows)
   static constexpr int UH = UR / 2;             // union rows per elementwise warp (two warps per lane quarter)
   static_assert(UR % 2 == 0, "union rows split evenly between the two warps of a quarter");
@@ -105,6 +106,7 @@ struct Cfg {
 
 struct FwdParams {
   int B, heads, H, W, q_rows, q_row0, kv_row0;
+  int pair;          // small-map pair mode (tc::pair_mode): B counts map pairs, K / V maps are pair views
   int tiles_h, tiles_w, num_tiles;
   float scale_log2;  // scale * log2(e)
   const float *rpb;  // [heads][TT][TT] or null
@@ -222,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // last read (tile it - kTInfo) before that tile's S was loaded, long before
       mbar_wait_sleep(&empty[s], ((it / kStagesQK) & 1) ^ 1, 1024);
       if (lane == 0) trace_ev(p, it, 0);
-      const int bh = b * p.heads + h;
+      const int bh = p.pair ? 2 * b * p.heads + h : b * p.heads + h;  // (pair: member 0)
       const int i0 = p.q_row0 + tr * kTQH, j0 = tcol * kTQW;
       const int hr0 = wstart(i0, p.H, L), hc0 = wstart(j0, p.W, L);
       if (elect_one()) {
@@ -236,7 +238,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         ti->rb[0] = wstart(min(i0, q_end - 1), p.H, L) - hr0;
         ti->rb[1] = wstart(min(i0 + 4, q_end - 1), p.H, L) - hr0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) ti->uc[q] = wstart(min(j0 + 4 * q, p.W - 1), p.W, L) - hc0;
+        for (int q = 0; q < 4; ++q)
+          ti->uc[q] = p.pair ? (q >> 1) * C::PW + wstart(min(4 * (q & 1), p.W - 1), p.W, L)
+                             : wstart(min(j0 + 4 * q, p.W - 1), p.W, L) - hc0;
         mbar_arrive(&ti_full[it % kTInfo]);  // release: the description above is visible to its waiters
         uint8_t *st = smem + s * C::QK_BYTES;
         mbar_expect_tx(&full[s], C::Q_BYTES + 2 * C::BOX_BYTES);
@@ -245,10 +249,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int sb = 0; sb < 2; ++sb)
 #pragma unroll
           for (int qb = 0; qb < 4; ++qb)
-            tma_load_4d(st + (64 * sb + 16 * qb) * kRB, &tm_q, &full[s], 0, j0 + 4 * qb, i0 - p.q_row0 + 4 * sb, bh);
+            tma_load_4d(st + (64 * sb + 16 * qb) * kRB, &tm_q, &full[s], 0, p.pair ? 4 * (qb & 1) : j0 + 4 * qb,
+                        i0 - p.q_row0 + 4 * sb, p.pair ? bh + (qb >> 1) * p.heads : bh);
 #pragma unroll
-        for (int sb = 0; sb < 2; ++sb)
-          tma_load_4d(st + C::Q_BYTES + sb * C::SUB_BYTES, &tm_k, &full[s], 0, hc0, hr0 + ti->rb[sb] - p.kv_row0, bh);
+        for (int sb = 0; sb < 2; ++sb) {
+          if (p.pair)  // both members' halo rows side by side: row pitch 2 * PW = HP
+            tma_load_5d(st + C::Q_BYTES + sb * C::SUB_BYTES, &tm_k, &full[s], 0, 0, 0, hr0 + ti->rb[sb] - p.kv_row0, bh);
+          else
+            tma_load_4d(st + C::Q_BYTES + sb * C::SUB_BYTES, &tm_k, &full[s], 0, hc0, hr0 + ti->rb[sb] - p.kv_row0, bh);
+        }
       }
       __syncwarp();
       if (++tcol == p.tiles_w) {
@@ -271,14 +280,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int it = 0; it < ntile; ++it) {
       const int s = it % kStagesV;
       mbar_wait_sleep(&empty_v[s], ((it / kStagesV) & 1) ^ 1, 1024);
-      const int bh = b * p.heads + h;
+      const int bh = p.pair ? 2 * b * p.heads + h : b * p.heads + h;
       const int i0 = p.q_row0 + tr * kTQH, j0 = tcol * kTQW;
       if (elect_one()) {
         mbar_expect_tx(&full_v[s], 2 * C::BOX_BYTES);
 #pragma unroll
-        for (int sb = 0; sb < 2; ++sb)
-          tma_load_4d(smem + C::V_OFF + s * C::V_BYTES + sb * C::SUB_BYTES, &tm_v, &full_v[s], 0, wstart(j0, p.W, L),
-                      wstart(min(i0 + 4 * sb, q_end - 1), p.H, L) - p.kv_row0, bh);
+        for (int sb = 0; sb < 2; ++sb) {
+          uint8_t *dst = smem + C::V_OFF + s * C::V_BYTES + sb * C::SUB_BYTES;
+          const int row = wstart(min(i0 + 4 * sb, q_end - 1), p.H, L) - p.kv_row0;
+          if (p.pair) tma_load_5d(dst, &tm_v, &full_v[s], 0, 0, 0, row, bh);
+          else tma_load_4d(dst, &tm_v, &full_v[s], 0, wstart(j0, p.W, L), row, bh);
+        }
       }
       __syncwarp();
       if (++tcol == p.tiles_w) {
@@ -409,8 +421,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         named_bar_sync(1 + g, 256);
         cur_head = h;
       }
-      // this thread's query and window geometry
-      const int i = i0 + 4 * sub + r, j = j0 + 4 * quarter + c;
+      // this thread's query and window geometry (pair mode: j is the column inside member
+      // quarter >> 1, whose keys start at halo column (quarter >> 1) * PW)
+      const int i = i0 + 4 * sub + r, j = p.pair ? 4 * (quarter & 1) + c : j0 + 4 * quarter + c;
+      const int jv = p.pair ? (quarter >> 1) * C::PW : 0;  // halo column offset of the member
       const int ic = min(i, q_end - 1), jc = min(j, p.W - 1);
       const int si = wstart(ic, p.H, L), sj = wstart(jc, p.W, L);
       const int dc = sj - jc + L - 1;                                // column-clamp class
@@ -424,7 +438,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         constexpr int ODD = decltype(odd_tag)::value;
         constexpr int NC = C::UW + 2 * ODD, NPK = NC / 2;
         const int uc = ucr - ODD;                                    // first loaded (even) column
-        const int bcol0 = hc0 + uc - jc + L - 1;                     // bias column of loaded col 0
+        const int bcol0 = hc0 + uc - jc - jv + L - 1;                // bias column of loaded col 0
         const int cp = bcol0 & 1;                                    // parity copy: aligned row start
         const float *tcls = tbl + cp * C::TBL_FLOATS + dc * C::TROWS * kTblStride + kTblOff + cp + bcol0;
         auto trow = [&](int u) {  // bias row of union row u0 + u (the -inf row outside the window)
@@ -538,7 +552,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (trc) trace_ev(p, it, 12);
       if (i < q_end && j < p.W) {
         const float inv = 1.f / sum;
-        const size_t qi = ((size_t)bh * p.q_rows + (i - p.q_row0)) * p.W + j;
+        const int bhq = p.pair ? bh + (quarter >> 1) * p.heads : bh;
+        const size_t qi = ((size_t)bhq * p.q_rows + (i - p.q_row0)) * p.W + j;
         uint4 *dst = (uint4 *)(p.out + qi * D + DH * hf);
 #pragma unroll
         for (int z = 0; z < DH; z += 8)
@@ -571,12 +586,16 @@ cudaError_t launch_fwd(const Geo &g, const void *q, const void *k, const void *v
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap tq, tk, tv;
   const int BH = g.B * g.heads;
+  const bool pair = pair_mode(g.B, g.H, g.W, g.q_row0, g.q_rows, g.kv_row0, g.kv_rows);
   if (!make_tmap_e16_4d(F16, &tq, q, D, g.W, g.q_rows, BH, 4, 4) ||
-      !make_tmap_e16_4d(F16, &tk, k, D, g.W, g.kv_rows, BH, C::HP, C::UR) ||
-      !make_tmap_e16_4d(F16, &tv, v, D, g.W, g.kv_rows, BH, C::HP, C::UR))
+      !(pair ? make_tmap_e16_pair(F16, &tk, k, D, g.W, g.kv_rows, g.heads, BH, C::PW, C::UR)
+             : make_tmap_e16_4d(F16, &tk, k, D, g.W, g.kv_rows, BH, C::HP, C::UR)) ||
+      !(pair ? make_tmap_e16_pair(F16, &tv, v, D, g.W, g.kv_rows, g.heads, BH, C::PW, C::UR)
+             : make_tmap_e16_4d(F16, &tv, v, D, g.W, g.kv_rows, BH, C::HP, C::UR)))
     return cudaErrorInvalidValue;
   FwdParams p;
-  p.B = g.B;
+  p.pair = pair;
+  p.B = pair ? g.B / 2 : g.B;
   p.heads = g.heads;
   p.H = g.H;
   p.W = g.W;
@@ -585,7 +604,7 @@ cudaError_t launch_fwd(const Geo &g, const void *q, const void *k, const void *v
   p.kv_row0 = g.kv_row0;
   p.tiles_h = (g.q_rows + kTQH - 1) / kTQH;
   p.tiles_w = (g.W + kTQW - 1) / kTQW;
-  p.num_tiles = BH * p.tiles_h * p.tiles_w;
+  p.num_tiles = p.B * g.heads * p.tiles_h * p.tiles_w;
   p.scale_log2 = g.scale * 1.4426950408889634f;
   p.rpb = rpb;
   p.out = (__nv_bfloat16 *)out;

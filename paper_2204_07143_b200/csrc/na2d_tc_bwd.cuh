@@ -22,7 +22,8 @@ namespace na2d {
 //    interior first 167 / 115 us.
 struct TileOrder {
   static constexpr int kMaxGroups = 16;
-  int B, heads, q_row0, num_tiles;
+  int B, heads, q_row0, num_tiles;  // B: maps per head (pair mode: map pairs per head)
+  int pair;                         // tc::pair_mode: tile = maps (b, h) and (b + 1, h), b even
   int n_rg, n_cg;
   int int_rg, int_cg;  // the interior row / column group (-1: none)
   int class_major;     // plain class-major order (class, head, batch, row, column)
@@ -32,7 +33,7 @@ struct TileOrder {
   };
   __device__ __forceinline__ Tile make(int a, int b, int h, int bb, int rem) const {
     Tile x;
-    x.bh = bb * heads + h;
+    x.bh = pair ? 2 * bb * heads + h : bb * heads + h;  // (pair mode: member 0)
     x.i0 = q_row0 + (rg_start[a] + rem / cg_count[b]) * tc::kTQH;
     x.j0 = (cg_start[b] + rem % cg_count[b]) * tc::kTQW;
     x.cls = a * n_cg + b;

@@ -1,4 +1,6 @@
 // na2d_tc_common.cu -- host helpers shared by the tcgen05 kernels.
+#include <stdlib.h>
+
 #include <mutex>
 #include <set>
 #include <utility>
@@ -40,6 +42,15 @@ cudaError_t ensure_smem_attr(const void *func, int smem_bytes) {
   const cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
   if (e == cudaSuccess) g_attr_done.insert({func, dev});
   return e;
+}
+
+bool pair_mode(int B, int H, int W, int q_row0, int q_rows, int kv_row0, int kv_rows) {
+  static const bool off = [] {
+    const char *e = getenv("NA2D_NO_PAIR");
+    return e && e[0] == '1';
+  }();
+  return !off && B >= 2 && B % 2 == 0 && H <= kTQH && W <= kTQW / 2 && q_row0 == 0 && q_rows == H && kv_row0 == 0 &&
+         kv_rows == H;
 }
 
 }  // namespace tc

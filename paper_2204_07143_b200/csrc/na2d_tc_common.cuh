@@ -197,6 +197,13 @@ __device__ __forceinline__ float tree_sum(const float (&x)[N]) {
 
 
 int num_sms();  // of the current device
+
+// Small-map pair mode: maps of at most one tile (H, W <= 8, whole map, no row band) and an even
+// batch run two maps per 8 x 16 tile -- map (b, h) in tile columns 0-7 (TMEM lane quarters 0, 1)
+// and map (b + 1, h) in columns 8-15 (quarters 2, 3) -- instead of one map in 49 of 128 query slots
+// (NAT stage 4, 7 x 7).  K / V / Q halos come from make_tmap_e16_pair views; each map keeps its own
+// clamped windows and bias cells.  NA2D_NO_PAIR=1 disables it (tests, A/B).
+bool pair_mode(int B, int H, int W, int q_row0, int q_rows, int kv_row0, int kv_rows);
 // raise kernel `func`'s dynamic shared-memory limit on the current device (once per device)
 cudaError_t ensure_smem_attr(const void *func, int smem_bytes);
 

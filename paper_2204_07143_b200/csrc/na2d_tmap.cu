@@ -61,6 +61,28 @@ bool make_tmap_e16_4d(bool f16, CUtensorMap *m, const void *base, int dim, int W
   return r == CUDA_SUCCESS;
 }
 
+bool make_tmap_e16_pair(bool f16, CUtensorMap *m, const void *base, int dim, int W, int rows, int heads, int outer,
+                        int box_w, int box_h) {
+  EncodeFn fn = encode_fn();
+  if (!fn || (dim != 16 && dim != 32 && dim != 64)) return false;
+  const CUtensorMapSwizzle sw = dim == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : dim == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                                      : CU_TENSOR_MAP_SWIZZLE_128B;
+  const cuuint64_t map = (cuuint64_t)rows * W * dim * 2;  // bytes per (b, h) map
+  // dims {dim, col, member, row, bh}: member 1 of the pair at bh is the map bh + heads
+  const cuuint64_t gdim[5] = {(cuuint64_t)dim, (cuuint64_t)W, 2, (cuuint64_t)rows, (cuuint64_t)outer};
+  const cuuint64_t gstride[4] = {(cuuint64_t)dim * 2, map * heads, (cuuint64_t)W * dim * 2, map};
+  const cuuint32_t box[5] = {(cuuint32_t)dim, (cuuint32_t)box_w, 2, (cuuint32_t)box_h, 1};
+  const cuuint32_t estride[5] = {1, 1, 1, 1, 1};
+  auto encode = [&] {
+    return fn(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void *>(base),
+              gdim, gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  };
+  CUresult r = encode();
+  if (r == CUDA_ERROR_INVALID_CONTEXT && bind_context()) r = encode();
+  return r == CUDA_SUCCESS;
+}
+
 bool make_tmap_f32_3d(CUtensorMap *m, const void *base, int W, int rows, int outer, int box_w, int box_h) {
   EncodeFn fn = encode_fn();
   if (!fn || (box_w * 4) % 16 != 0 || ((size_t)W * 4) % 16 != 0) return false;

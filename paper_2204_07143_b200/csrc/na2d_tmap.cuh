@@ -18,6 +18,13 @@ bool make_tmap_bf16_4d(CUtensorMap *m, const void *base, int dim, int W, int row
 bool make_tmap_e16_4d(bool f16, CUtensorMap *m, const void *base, int dim, int W, int rows, int outer, int box_w,
                       int box_h);
 
+// Pair layout for small maps (tc::pair_mode): the maps bh and bh + heads side by side.  5-D view
+// {dim, col, member, row, bh} with a box of {dim, box_w, 2, box_h, 1}: shared memory receives
+// [row][member][col] rows, i.e. a halo of pitch 2 * box_w keys with member m at column m * box_w
+// (columns >= W zero-filled).  The caller must only address pairs whose member 1 exists.
+bool make_tmap_e16_pair(bool f16, CUtensorMap *m, const void *base, int dim, int W, int rows, int heads, int outer,
+                        int box_w, int box_h);
+
 }  // namespace na2d
 
 namespace na2d {

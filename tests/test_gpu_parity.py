@@ -308,3 +308,34 @@ def test_drpb_bitwise_reproducible(dtype, d):
     a = na2d.backward(t["q"], t["k"], t["v"], rpb, out, lse, t["dout"], 7)[3].clone()
     b = na2d.backward(t["q"], t["k"], t["v"], rpb, out, lse, t["dout"], 7)[3].clone()
     assert torch.equal(a, b)
+
+
+# Small-map pair mode (tc::pair_mode: H, W <= 8, even B, whole map): two maps per 8 x 16 tile,
+# each with its own clamped windows and bias cells.  Shapes cover W <= 4 (quarters 1 and 3 empty),
+# L > map, L < map (clamped windows inside each member), odd and even widths.
+PAIR = [
+    Shape("pair7x7k7", 4, 3, 7, 7, 32, 7),     # NAT-Tiny stage 4 geometry
+    Shape("pair8x8k3", 2, 2, 8, 8, 32, 3),
+    Shape("pair6x8k5", 6, 1, 6, 8, 32, 5),
+    Shape("pair8x5k7", 2, 2, 8, 5, 32, 7),
+    Shape("pair3x4k3", 4, 2, 3, 4, 32, 3),
+    Shape("pair7x7k5", 2, 2, 7, 7, 32, 5),
+    Shape("pair2x7k3", 8, 1, 2, 7, 32, 3),
+]
+
+
+@pytest.mark.parametrize("shape", PAIR, ids=lambda s: s.name)
+@pytest.mark.parametrize("dtype", ["bf16", "f16"])
+def test_pair_mode_small_maps(shape, dtype):
+    assert family(shape, dtype) == ("tcgen05", "tcgen05")
+    check(shape, dtype)
+
+
+@pytest.mark.parametrize("d", [16, 64])
+@pytest.mark.parametrize("L", [3, 7])
+def test_pair_mode_head_dims(d, L):
+    check(Shape(f"pair7x6d{d}k{L}", 4, 2, 7, 6, d, L), "bf16")
+
+
+def test_pair_mode_outputs_all_written():
+    test_every_output_element_written(Shape("nanpair", 4, 2, 7, 7, 32, 7), "bf16")
