@@ -169,9 +169,11 @@ const char *na2d_last_cuda_error(void);
 na2d_status na2d_profile_enable(int on);
 int na2d_profile_read(char *names_out, size_t name_cap, float *total_ms, int *counts, int max_entries);
 
-/* Development aid: device buffer of >= 8192 int64 that the tensor-core kernels fill with
- * clock64() timestamps of their pipeline events (first 32 tiles / chunks of CTAs 0-3: forward and
- * B2 in slots [0, 4096), B1 in [4096, 8192)); NULL disables. */
+/* Development aid, effective only in builds with -DNA2D_TRACE: device buffer of >= 24000 int64
+ * that the tensor-core kernels fill with clock64() timestamps of their pipeline events (first 32
+ * tiles / chunks of CTAs 0-3: forward and B2 in slots [0, 4096), B1 in [4096, 8192)) and
+ * %globaltimer wall-clock points (per-CTA spans from 16384, forward / B2 prologue and epilogue
+ * points from 18000 / 19200; scripts/trace_balance.py, scripts/trace_fixed.py); NULL disables. */
 na2d_status na2d_debug_set_trace(void *device_buffer);
 
 #ifdef __cplusplus

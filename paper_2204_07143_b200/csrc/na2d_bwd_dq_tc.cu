@@ -103,7 +103,8 @@ struct CfgQ {
   static constexpr int HALF_B = 16 * ROWB;                 // one 4 x 4 block of dQ rows (TMA store box)
   static constexpr int DB_OFF = OUT_OFF + 4 * 2 * HALF_B;
   static constexpr int DP_OFF = DB_OFF + ((8 * kGroups * TT * TT * 4 + 255) / 256) * 256;  // partial D
-  static constexpr int TI_OFF = DP_OFF + kGroups * 128 * 4;
+  static constexpr int RS_OFF = DP_OFF + kGroups * 128 * 4;  // the head's bias values (table build)
+  static constexpr int TI_OFF = RS_OFF + (TT * TT * 4 + 15) / 16 * 16;
   static constexpr int BAR_OFF = TI_OFF + NST * 64;
   static_assert(sizeof(TileInfoQ) <= 64, "TileInfoQ");
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
@@ -187,6 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
   pdl_trigger();
   pdl_wait();  // the previous kernel (forward / last step's B2) is complete: global memory from here on
+  if (threadIdx.x == 0) qtrace_gt(p, 19);
   if (blockIdx.x == 0 && threadIdx.x == 0 && p.b2_tile_counter) *p.b2_tile_counter = 0;  // for B2 (next)
   if (p.drpb_part) {  // this CTA's partial tables (only this CTA writes them; B2 reads them after B1)
     for (int c = threadIdx.x; c < p.heads * C::TT * C::TT; c += kThreads)
@@ -385,9 +387,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int z = 0; z < C::UCW / 2; ++z) acc[u][z] = make_float2(0.f, 0.f);
     };
+    uint64_t committed = 0;  // heads (< 64) whose partial table this CTA has written already
     auto commit_head = [&](int head) {  // sum of the private tables -> partials[cta][head]; clear
       named_bar_sync(1, kEw);
-      if (head >= 0 && p.drpb_part)
+      if (head >= 0 && p.drpb_part) {
+        // first commit of a head: plain store (no dependent global load); the table was zeroed at entry
+        const bool again = head >= 64 || ((committed >> head) & 1);
         for (int e = gtid; e < C::TT * C::TT; e += kEw) {
           float v = 0.f;
 #pragma unroll
@@ -396,10 +401,28 @@ __global__ void __launch_bounds__(kThreads, 1)
             s_db[w * C::TT * C::TT + e] = 0.f;
           }
           float *dst = &p.drpb_part[((size_t)blockIdx.x * p.heads + head) * C::TT * C::TT + e];
-          *dst += p.scale * v;
+          *dst = again ? *dst + p.scale * v : p.scale * v;
         }
+        if (head < 64) committed |= 1ull << head;
+      }
       named_bar_sync(1, kEw);
     };
+    // the masked bias table of head h: the head's bias values staged in shared memory (one global
+    // load per thread), then the two parity copies built from there
+    auto build_table = [&](int h) {
+      named_bar_sync(1, kEw);
+      float *rs = (float *)(smem + C::RS_OFF);
+      for (int e = gtid; e < C::TT * C::TT; e += kEw) rs[e] = p.rpb ? __ldg(&p.rpb[h * C::TT * C::TT + e]) * sl2 : 0.f;
+      named_bar_sync(1, kEw);
+      BiasTable<L>::build_rows_smem(tbl, p.rpb ? rs : nullptr, Lw, 2, 0, gtid, kEw);
+      named_bar_sync(1, kEw);
+    };
+    // the first tile's table is built while its Q / K / V / dO loads are in flight
+    if (t_begin < t_end) {
+      cur_head = decode(p, t_begin).bh % p.heads;
+      build_table(cur_head);
+      if (gtid == 0) qtrace_gt(p, 20);
+    }
     int it = 0;
     for (int t = t_begin; t < t_end; ++t, ++it) {
       const uint32_t ph = it & 1;
@@ -424,9 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (p.rpb && cur_key >= 0) flush();
         if (h != cur_head) {
           if (p.rpb) commit_head(cur_head);
-          named_bar_sync(1, kEw);
-          BiasTable<L>::build_elems2(tbl, p.rpb, h, Lw, sl2, gtid, kEw);  // (measured fastest here)
-          named_bar_sync(1, kEw);
+          build_table(h);
           cur_head = h;
         }
         cur_key = key;
@@ -447,6 +468,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float2 nlse2x2 = make_float2(nlse2, nlse2);
       mbar_wait(NA2D_B1_SPLIT ? &sp_part[grp] : sp_full, ph);
       if (tq) qtrace(p, it, 9);
+      if (gtid == 0 && it == 0) qtrace_gt(p, 21);
       tc_fence_after();
       // ---- pass 1: P = exp2(s*scale*log2e + B' - LSE*log2e) (fp32, written over S in place) and
       // D = dO.O = sum_window P dP (exact in fp32: O = sum P V, so dO.O = sum P (dO.v)); element
@@ -592,10 +614,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (tq) qtrace(p, it, 14);
     }
     if (threadIdx.x == 64 + 64) qtrace_gt(p, 17);
+    if (gtid == 0) qtrace_gt(p, 22);
     if (p.rpb) {
       if (cur_key >= 0) flush();
       commit_head(cur_head);
     }
+    if (gtid == 0) qtrace_gt(p, 23);
     if (lane == 0) bulk_wait0();
   }
   __syncthreads();

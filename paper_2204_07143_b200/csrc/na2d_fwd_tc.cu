@@ -96,8 +96,8 @@ struct Cfg {
   static constexpr int TBL_OFF = V_OFF + SV * V_BYTES;             // 2 groups x 2 parity copies
   static constexpr int EX_OFF = TBL_OFF + 4 * TBL_FLOATS * 4;      // row max / sum exchange [2][2][4][2][32]
   static constexpr int RB_OFF = EX_OFF + 2 * 2 * 4 * 2 * 32 * 4;   // per group: scaled RPB + window max
-  static constexpr int RB_FLOATS = 256;
-  static_assert(TT * TT + L * L <= RB_FLOATS, "RPB staging");
+  static constexpr int RB_FLOATS = 320;  // scaled RPB, window maxima, row-wise sliding maxima
+  static_assert(TT * TT + L * L + TT * L <= RB_FLOATS, "RPB staging");
   static constexpr int TI_OFF = RB_OFF + 2 * RB_FLOATS * 4;
   static constexpr int BAR_OFF = TI_OFF + kTInfo * 64;
   static constexpr int SMEM = BAR_OFF + 320 + 1024;
@@ -122,8 +122,17 @@ __device__ __forceinline__ void trace_ev(const FwdParams &p, int it, int ev) {
   if (p.trace && blockIdx.x < 4 && it < kTraceTiles)
     p.trace[((size_t)blockIdx.x * kTraceTiles + it) * kTraceEv + ev] = clock64();
 }
+// wall clock of prologue / epilogue points: trace[18000 + 8 * cta + k] (scripts/trace_fixed.py)
+__device__ __forceinline__ void trace_gt(const FwdParams &p, int k) {
+  if (p.trace) {
+    uint64_t gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    p.trace[18000 + 8 * blockIdx.x + k] = (long long)gt;
+  }
+}
 #else
 __device__ __forceinline__ void trace_ev(const FwdParams &, int, int) {}
+__device__ __forceinline__ void trace_gt(const FwdParams &, int) {}
 #endif
 
 // Tile description (ring of kTInfo), written by the Q/K producer before it arms full_qk.
@@ -163,6 +172,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int t_end = (int)((long)p.num_tiles * (blockIdx.x + 1) / gridDim.x);
   const int ntile = t_end - t_begin;
   const int q_end = p.q_row0 + p.q_rows;
+  if (threadIdx.x == 0) trace_gt(p, 0);
 
   if (warp == kProducerWarp && lane == 0) {
     for (int s = 0; s < kStagesQK; ++s) {
@@ -203,6 +213,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
   pdl_trigger();
   pdl_wait();  // the previous kernel on the stream is complete: global memory from here on
+  if (threadIdx.x == 0) trace_gt(p, 1);
 #ifdef NA2D_TRACE
   if (threadIdx.x == 0 && p.trace) {  // per-CTA wall-clock span (load balance, scripts/trace_balance.py)
     uint64_t gt;
@@ -411,15 +422,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             dst[e] = (rv && cb >= dc && cb < dc + Lw) ? src[cb] : -INFINITY;
           }
         }
-        for (int e = stid; e < L * L; e += 256) {
-          const int dr = e / L, dc = e % L;
+        // window maxima, separably: row-wise sliding maxima m1[a][dc] over [dc, dc + Lw), then
+        // tmx[dr][dc] = max over rows [dr, dr + Lh) of m1 (7 + 7 dependent loads instead of 49)
+        float *m1 = tmx + L * L;
+        for (int e = stid; e < C::TT * L; e += 256) {
+          const int a = e / L, dc = e - a * L;
           float m = -INFINITY;
-          for (int a = dr; a < dr + Lh; ++a)
-            for (int b2 = dc; b2 < dc + Lw; ++b2) m = fmaxf(m, rbs[a * C::TT + b2]);
+          for (int b2 = dc; b2 < dc + Lw; ++b2) m = fmaxf(m, rbs[a * C::TT + b2]);
+          m1[e] = m;
+        }
+        named_bar_sync(1 + g, 256);
+        for (int e = stid; e < L * L; e += 256) {
+          const int dr = e / L, dc = e - dr * L;
+          float m = -INFINITY;
+          for (int a = dr; a < dr + Lh; ++a) m = fmaxf(m, m1[a * L + dc]);
           tmx[e] = m;
         }
         named_bar_sync(1 + g, 256);
         cur_head = h;
+        if (stid == 0 && it < 2) trace_gt(p, 2);
       }
       // this thread's query and window geometry (pair mode: j is the column inside member
       // quarter >> 1, whose keys start at halo column (quarter >> 1) * PW)
@@ -448,6 +469,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (trc) trace_ev(p, it, 5);
         wait_bar(&s_full[g], ph);
         if (trc) trace_ev(p, it, 6);
+        if (trc && it == 0) trace_gt(p, 3);
         tc_fence_after();
         uint32_t sv[C::UH][NC];
 #pragma unroll
@@ -563,12 +585,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (trc) trace_ev(p, it, 13);
     }
+    if (threadIdx.x == 0) trace_gt(p, 4);
   }
   __syncthreads();
   if (warp == kProducerWarp) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
+  if (threadIdx.x == 0) trace_gt(p, 5);
 #ifdef NA2D_TRACE
   if (threadIdx.x == 0 && p.trace) {
     uint64_t gt;

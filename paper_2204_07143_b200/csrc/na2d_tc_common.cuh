@@ -40,17 +40,26 @@ struct BiasTable {
       tbl[e] = v;
     }
   }
-  // two copies, copy x holding column b at kTblOff + x + b (copy x at tbl + x * FLOATS): a reader
-  // whose first column has parity x uses copy x, so its element pairs are 8-byte aligned (LDS.64)
-  __device__ static void build_elems2(float *tbl, const float *rpb, int h, int Lw, float mul, int tid, int nthreads) {
-    for (int e = tid; e < 2 * FLOATS; e += nthreads) {
-      const int x = e >= FLOATS, ex = e - x * FLOATS;
-      const int dc = ex / (TROWS * kTblStride);
-      const int rr = (ex / kTblStride) % TROWS;
-      const int cb = ex % kTblStride - kTblOff - x;
-      float v = -INFINITY;
-      if (rr < TT && cb >= dc && cb < dc + Lw) v = rpb ? __ldg(&rpb[(h * TT + rr) * TT + cb]) * mul : 0.f;
-      tbl[e] = v;
+  // `copies` (1 or 2) parity copies of the table (copy x holds column b at kTblOff + x + b: a reader
+  // whose first column has parity x uses copy x, so its element pairs are 8-byte aligned), plus `extra` all -inf classes after the L real
+  // ones (copy x at tbl + x * (L + extra) * TROWS * kTblStride), from a staged, pre-scaled copy of the
+  // head's (2L-1)^2 bias values in shared memory (rs, or null for no bias).  One table row per
+  // thread: no global load latency and no per-element index arithmetic inside the build (an
+  // element-parallel build straight from global memory took ~3.8 us per head in B1,
+  // scripts/trace_fixed.py).
+  __device__ static void build_rows_smem(float *tbl, const float *rs, int Lw, int copies, int extra, int tid,
+                                         int nthreads) {
+    const int per_copy = (L + extra) * TROWS;
+    for (int row = tid; row < copies * per_copy; row += nthreads) {
+      const int x = row / per_copy, rc = row - x * per_copy;
+      const int dc = rc / TROWS, rr = rc - dc * TROWS;
+      float *dst = tbl + row * kTblStride;
+      const bool live = dc < L && rr < TT;
+      const float *src = rs + (live ? rr * TT : 0);
+      const int lo = kTblOff + x + dc, hi = lo + Lw;  // entries holding columns [dc, dc + Lw)
+#pragma unroll 8
+      for (int e = 0; e < kTblStride; ++e)
+        dst[e] = live && e >= lo && e < hi ? (rs ? src[e - kTblOff - x] : 0.f) : -INFINITY;
     }
   }
   // one table row per thread: the row's 2L-1 bias values are loaded together (independent loads),

@@ -11,7 +11,7 @@ rpb = torch.from_numpy(inp["rpb"]).cuda()
 for _ in range(2):
     out, lse = na2d.forward(t["q"], t["k"], t["v"], rpb, 7)
     na2d.backward(t["q"], t["k"], t["v"], rpb, out, lse, t["dout"], 7)
-buf = torch.zeros(20000, dtype=torch.int64, device="cuda")
+buf = torch.zeros(24000, dtype=torch.int64, device="cuda")
 lib = na2d.load_library()
 lib.na2d_debug_set_trace(buf.data_ptr())
 out, lse = na2d.forward(t["q"], t["k"], t["v"], rpb, 7)
