@@ -187,6 +187,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_trigger();
+  // the masked bias table of head h (elementwise warps, named barrier 1): the head's bias values
+  // staged in shared memory (one global load per thread), then the two parity copies built from there
+  constexpr int kEw = kGroups * 128;  // elementwise threads
+  const int Lw = wlen(p.W, L);
+  const float sl2 = p.scale * 1.4426950408889634f;
+  auto build_table = [&](int h) {
+    named_bar_sync(1, kEw);
+    float *rs = (float *)(smem + C::RS_OFF);
+    for (int e = threadIdx.x; e < C::TT * C::TT; e += kEw) rs[e] = p.rpb ? __ldg(&p.rpb[h * C::TT * C::TT + e]) * sl2 : 0.f;
+    named_bar_sync(1, kEw);
+    BiasTable<L>::build_rows_smem(tbl, p.rpb ? rs : nullptr, Lw, 2, 0, threadIdx.x, kEw);
+    named_bar_sync(1, kEw);
+  };
+  // the first tile's table is built before griddepcontrol.wait: the RPB is an input, not an output of
+  // the previous kernel, so this overlaps that kernel's tail
+  const int first_head = t_begin < t_end ? decode(p, t_begin).bh % p.heads : -1;
+  if (warp < 4 * kGroups && first_head >= 0) build_table(first_head);
   pdl_wait();  // the previous kernel (forward / last step's B2) is complete: global memory from here on
   if (threadIdx.x == 0) qtrace_gt(p, 19);
   if (blockIdx.x == 0 && threadIdx.x == 0 && p.b2_tile_counter) *p.b2_tile_counter = 0;  // for B2 (next)
@@ -349,15 +366,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int half = lane >> 4, r = (lane >> 2) & 3, c = lane & 3;
     const int gtid = threadIdx.x;
     float *s_dpart = (float *)(smem + C::DP_OFF);
-    const int Lh = wlen(p.H, L), Lw = wlen(p.W, L);
+    const int Lh = wlen(p.H, L);
     const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
-    const float sl2 = p.scale * 1.4426950408889634f;
     const float2 sl2x2 = make_float2(sl2, sl2);
     // this (warp, half)'s private dRPB table: within one instruction the 16 lanes of a half touch
     // distinct cells (no intra-instruction address conflicts, no other warp contending), but
     // different (u, z) of different lanes do meet, so the adds stay atomic (RED to shared)
     float *my_db = s_db + ((grp * 4 + quarter) * 2 + half) * C::TT * C::TT;
-    constexpr int kEw = kGroups * 128;  // elementwise threads
     uint8_t *ostage = smem + C::OUT_OFF + quarter * 2 * C::HALF_B;
     // dRPB accumulator in union coordinates for the current (class, head) and its geometry
     float2 acc[2 * C::PA][C::UCW / 2];  // local rows: union row 2 * pr0 + u
@@ -407,22 +422,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       named_bar_sync(1, kEw);
     };
-    // the masked bias table of head h: the head's bias values staged in shared memory (one global
-    // load per thread), then the two parity copies built from there
-    auto build_table = [&](int h) {
-      named_bar_sync(1, kEw);
-      float *rs = (float *)(smem + C::RS_OFF);
-      for (int e = gtid; e < C::TT * C::TT; e += kEw) rs[e] = p.rpb ? __ldg(&p.rpb[h * C::TT * C::TT + e]) * sl2 : 0.f;
-      named_bar_sync(1, kEw);
-      BiasTable<L>::build_rows_smem(tbl, p.rpb ? rs : nullptr, Lw, 2, 0, gtid, kEw);
-      named_bar_sync(1, kEw);
-    };
-    // the first tile's table is built while its Q / K / V / dO loads are in flight
-    if (t_begin < t_end) {
-      cur_head = decode(p, t_begin).bh % p.heads;
-      build_table(cur_head);
-      if (gtid == 0) qtrace_gt(p, 20);
-    }
+    cur_head = first_head;  // its table was built before griddepcontrol.wait
+    if (gtid == 0) qtrace_gt(p, 20);
     int it = 0;
     for (int t = t_begin; t < t_end; ++t, ++it) {
       const uint32_t ph = it & 1;
