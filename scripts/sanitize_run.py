@@ -21,8 +21,10 @@ cases = [
     (Shape("d64", 2, 2, 19, 37, 64, 7), "bf16"),  # tcgen05, 128-byte rows, single stage, dQ in two passes
     (Shape("d64k5f16", 1, 2, 13, 21, 64, 5), "f16"),
     (Shape("d128", 1, 2, 11, 14, 128, 7), "bf16"),  # SIMT (incl. the fixed-order dRPB reduction)
+    (Shape("pair7", 4, 3, 7, 7, 32, 7), "bf16"),  # small-map pair mode (two maps per tile, 5-D TMA views)
+    (Shape("pair3", 4, 2, 3, 4, 32, 3), "f16"),
 ]
-only = sys.argv[1:]  # optional case names (s7 s5 s3 f32 d16 d64 d64k5f16 d128 paper)
+only = sys.argv[1:]  # optional case names (s7 s5 s3 f32 d16 d64 d64k5f16 d128 pair7 pair3 paper)
 for s, dt in cases:
     if only and s.name not in only:
         continue
