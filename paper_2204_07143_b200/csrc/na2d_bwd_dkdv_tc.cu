@@ -69,7 +69,9 @@ struct CfgK {
   static_assert(STAGE_BYTES % 1024 == 0 && Q_BYTES % 1024 == 0, "1 KB alignment");
   static constexpr int TT = 2 * L - 1;
   static constexpr int TROWS = TT + 1;
-  static constexpr int TBL_FLOATS = (L + 1) * TROWS * kTblStride;  // + all -inf class (OOB columns)
+  // the masked table's L column-clamp classes, an all -inf class (index L) and an unmasked class
+  // (index L + 1: B[a][b] for every b, the border path masks per column instead)
+  static constexpr int TBL_FLOATS = (L + 2) * TROWS * kTblStride;
   static constexpr int TBL_OFF = NST * STAGE_BYTES;
   // dV / dK output staging: 2 groups x 4 warps x 4 KB (SW64 boxes, 1 KB aligned)
   static constexpr int OUT_OFF = (TBL_OFF + TBL_FLOATS * 4 + 1023) / 1024 * 1024;
@@ -170,11 +172,13 @@ __device__ __forceinline__ KTile ktile(const BwdKParams &p, int t) {
 
 // Elementwise rows of one chunk for one lane (one key): for each chunk row u and union column z
 //   P = exp2(s*scale*log2e + B'[row][col] - LSE*log2e),  dS = P (dP - D)  -> bf16 pairs over S / dP.
-// FAST: every union column of the quarter is an interior column (column-clamp class NS), so the
-// bias address is trow - z (immediate offsets); otherwise per-column class offsets (colterm).
+// FAST: every union column of the quarter is an interior column (column-clamp class NS): the masked
+// table of class NS at trow - z (immediate offsets).  Otherwise the unmasked class at trow - z plus a
+// per-column mask (0 / -inf: is this lane's key column inside the query column's window), so the
+// border path also uses immediate offsets instead of per-column class offsets.
 template <int L, int QP, bool FAST, bool F16>
 __device__ __forceinline__ void chunk_rows(uint32_t lane_addr, int uc, const float *tbl_row0,
-                                           const int (&colterm)[CfgK<L, QP>::UCW], const float *lrow0,
+                                           const float2 (&mcol)[CfgK<L, QP>::UCW / 2], const float *lrow0,
                                            int pk, int i_base, int H, int rows_here, int Lh, float sl2,
                                            int rows_even) {
   using C = CfgK<L, QP>;
@@ -214,7 +218,7 @@ __device__ __forceinline__ void chunk_rows(uint32_t lane_addr, int uc, const flo
         const float2 lz = *reinterpret_cast<const float2 *>(lrow[y] + z);
         const float2 dz = *reinterpret_cast<const float2 *>(lrow[y] + C::LD_FLOATS + z);
         const float2 tb = FAST ? make_float2(trow[y][-z], trow[y][-(z + 1)])
-                               : make_float2(trow[y][colterm[z]], trow[y][colterm[z + 1]]);
+                               : __fadd2_rn(make_float2(trow[y][-z], trow[y][-(z + 1)]), mcol[z / 2]);
         const float2 sz = make_float2(__uint_as_float(sv[y][z]), __uint_as_float(sv[y][z + 1]));
         const float2 xv = __ffma2_rn(sz, make_float2(sl2, sl2), tb);
         const float2 ar = __ffma2_rn(lz, make_float2(-log2e, -log2e), xv);
@@ -241,7 +245,6 @@ struct TileInfo {
   int bh, kr0, kc0, qr0, qc0, nchunks, head, pad;
   int qs_lo[2], qs_n[2];
   int uc[4], fast[4];
-  int colterm[4][16];  // per union column: bias-table class offset (slow path)
 };
 static_assert(sizeof(TileInfo) <= kTileInfoBytes, "TileInfo size");
 
@@ -379,18 +382,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         ti->qs_lo[1] = g.qs_lo[1];
         ti->qs_n[0] = g.qs_n[0];
         ti->qs_n[1] = g.qs_n[1];
-      }
-      __syncwarp();
-#pragma unroll
-      for (int e = lane; e < 64; e += 32) {  // class offset of union column z of quarter q
-        const int q = e >> 4, z = e & 15;
-        const int j = g.qc0 + ti->uc[q] + z;
-        int dcl = j < p.W ? wstart(j, p.W, L) - j + L - 1 : L;
-        if (p.pair) {  // a column of the quarter's own member inside the map, else the all -inf class
-          const int m = j / (QP / 2), jl = j - m * (QP / 2);
-          dcl = m == (q >> 1) && jl < p.W ? wstart(jl, p.W, L) - jl + L - 1 : L;
-        }
-        ti->colterm[q][z] = dcl * C::TROWS * kTblStride - j;
       }
       __syncwarp();
       uint8_t *st = smem + s * C::STAGE_BYTES;
@@ -650,24 +641,61 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int qn0 = ti.qs_n[0], qn1 = ti.qs_n[1];
       const int uc = ti.uc[quarter];
       const bool fast = ti.fast[quarter];
-      int colterm[C::UCW];
-#pragma unroll
-      for (int z = 0; z < C::UCW; ++z) colterm[z] = ti.colterm[quarter][z];
+      float2 mcol[C::UCW / 2];  // border path: 0 if this lane's key column is in union column z's window
       if (h != cur_head) {  // both groups rebuild the shared table: sync all 256 threads
         named_bar_sync(1, 256);
         const int tid256 = threadIdx.x;
         BiasTable<L>::build_rows(tbl, p.rpb, h, Lw, sl2, tid256, 256);  // (measured fastest here)
-        for (int e = BiasTable<L>::FLOATS + tid256; e < C::TBL_FLOATS; e += 256) tbl[e] = -INFINITY;
+        // the all -inf class L and the unmasked class L + 1: one row per thread past the L classes
+        for (int row = tid256; row < (L + 2) * C::TROWS; row += 256) {
+          if (row < L * C::TROWS) continue;  // a masked class row: built by build_rows
+          const int rr = row % C::TROWS;
+          const bool live = row >= (L + 1) * C::TROWS && rr < C::TT;
+          float b[C::TT];
+#pragma unroll
+          for (int k2 = 0; k2 < C::TT; ++k2) b[k2] = (p.rpb && live) ? __ldg(&p.rpb[(h * C::TT + rr) * C::TT + k2]) * sl2 : 0.f;
+          float *dst = tbl + row * kTblStride;
+#pragma unroll
+          for (int e = 0; e < kTblStride; ++e) {
+            const int cb = e - kTblOff;
+            float v = -INFINITY;
+#pragma unroll
+            for (int k2 = 0; k2 < C::TT; ++k2)
+              if (cb == k2 && live) v = b[k2];
+            dst[e] = v;
+          }
+        }
         named_bar_sync(1, 256);
         cur_head = h;
       }
       // this thread's key
       // this thread's key; pair mode: halo column of member quarter >> 1 (bias columns are key - query
-      // differences inside one member, colterm sends the other member's columns to the -inf class)
+      // differences inside one member; mcol masks the other member's columns)
       const int pk = kr0 + 4 * half + r,
                 qk = p.pair ? (quarter >> 1) * (QP / 2) + 4 * (quarter & 1) + cc : kc0 + 4 * quarter + cc;
       const float *lsd = (const float *)(smem + stage * C::STAGE_BYTES + 2 * C::Q_BYTES + 2 * C::KT_BYTES);
-      const float *tbl_row0 = tbl + kTblOff + qk + L - 1 + (fast ? C::NS * C::TROWS * kTblStride - (qc0 + uc) : 0);
+      const float *tbl_row0 = tbl + kTblOff + qk + L - 1 - (qc0 + uc) + (fast ? C::NS : L + 1) * C::TROWS * kTblStride;
+      if (!fast) {
+        const int kl = p.pair ? 4 * (quarter & 1) + cc : qk;  // key column inside its map
+#pragma unroll
+        for (int z = 0; z < C::UCW; z += 2) {
+          float mv[2];
+#pragma unroll
+          for (int o = 0; o < 2; ++o) {
+            int j = qc0 + uc + z + o;  // query column (pair mode: inside the quarter's own member)
+            bool ok = true;
+            if (p.pair) {
+              const int m = j / (QP / 2);
+              j -= m * (QP / 2);
+              ok = m == (quarter >> 1);
+            }
+            const int ws = wstart(min(j, p.W - 1), p.W, L);
+            ok = ok && j < p.W && kl >= ws && kl < ws + Lw;
+            mv[o] = ok ? 0.f : -INFINITY;
+          }
+          mcol[z / 2] = make_float2(mv[0], mv[1]);
+        }
+      }
       if (trq) ktrace(p, c, 17 + 4 * grp);
       for (int k = 0; k < nch; ++k, ++c) {
         if ((c & 1) != grp) continue;
@@ -684,10 +712,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         // clips, so its P / dS columns may hold anything
         if ((p.pair ? 4 * (quarter & 1) : kc0 + 4 * quarter) < p.W) {
           if (fast)
-            chunk_rows<L, QP, true, F16>(lane_addr, uc, tbl_row0, colterm, lrow0, pk, i_base, p.H, rows_here, Lh, sl2,
+            chunk_rows<L, QP, true, F16>(lane_addr, uc, tbl_row0, mcol, lrow0, pk, i_base, p.H, rows_here, Lh, sl2,
                                     chunk_rows_even<C::CR>(qn0, qn1, k));
           else
-            chunk_rows<L, QP, false, F16>(lane_addr, uc, tbl_row0, colterm, lrow0, pk, i_base, p.H, rows_here, Lh, sl2,
+            chunk_rows<L, QP, false, F16>(lane_addr, uc, tbl_row0, mcol, lrow0, pk, i_base, p.H, rows_here, Lh, sl2,
                                      chunk_rows_even<C::CR>(qn0, qn1, k));
         }
         tc_wait_st();
