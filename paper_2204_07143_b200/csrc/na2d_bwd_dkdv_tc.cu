@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int it = 0;
     for (int t = blockIdx.x;; ++it) {
       const int s = it % kStages;
-      mbar_wait_sleep(&empty[s], ((it / kStages) & 1) ^ 1, 1024);
+      mbar_wait_producer(&empty[s], ((it / kStages) & 1) ^ 1);
       TileInfo *ti = tinfo + s;
       if (t >= p.num_tiles) {  // end of work: sentinel, released like a loaded stage
         if (lane == 0) {

@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int it = 0;
     for (int t = t_begin; t < t_end; ++t, ++it) {
       const int s = it % kStages;
-      mbar_wait_sleep(&empty[s], ((it / kStages) & 1) ^ 1, 1024);
+      mbar_wait_producer(&empty[s], ((it / kStages) & 1) ^ 1);
       const TileOrder::Tile g = decode(p, t);
       const int hr0 = wstart(g.i0, p.H, L), hc0 = wstart(g.j0, p.W, L);
       uint8_t *st = smem + s * C::STAGE_BYTES;

@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int s = it % kStagesQK;
       // full[s] re-arms once QK(it - kStagesQK) has completed; the description slot it % kTInfo was
       // last read (tile it - kTInfo) before that tile's S was loaded, long before
-      mbar_wait_sleep(&empty[s], ((it / kStagesQK) & 1) ^ 1, 1024);
+      mbar_wait_producer(&empty[s], ((it / kStagesQK) & 1) ^ 1);
       if (lane == 0) trace_ev(p, it, 0);
       const int bh = p.pair ? 2 * b * p.heads + h : b * p.heads + h;  // (pair: member 0)
       const int i0 = p.q_row0 + tr * kTQH, j0 = tcol * kTQW;
@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int h = u0 / p.B, b = u0 - h * p.B, tr = rem0 / p.tiles_w, tcol = rem0 - tr * p.tiles_w;
     for (int it = 0; it < ntile; ++it) {
       const int s = it % kStagesV;
-      mbar_wait_sleep(&empty_v[s], ((it / kStagesV) & 1) ^ 1, 1024);
+      mbar_wait_producer(&empty_v[s], ((it / kStagesV) & 1) ^ 1);
       const int bh = p.pair ? 2 * b * p.heads + h : b * p.heads + h;
       const int i0 = p.q_row0 + tr * kTQH, j0 = tcol * kTQW;
       if (elect_one()) {

@@ -62,9 +62,25 @@ __device__ __forceinline__ void mbar_wait_hint(uint64_t *bar, uint32_t parity) {
   while (!mbar_try_wait_hint(bar, parity, 0x100000u)) {
   }
 }
+// Producer warps' wait for a free stage (NA2D_PROD_WAIT: 0 = exponential back-off sleeps up to
+// max_ns, 1 = try_wait with a suspend-time hint, i.e. a hardware sleep that ends when the phase
+// completes, 2 = spin)
+#ifndef NA2D_PROD_WAIT
+#define NA2D_PROD_WAIT 0
+#endif
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity, uint32_t max_ns = 256);
+__device__ __forceinline__ void mbar_wait_producer(uint64_t *bar, uint32_t parity) {
+#if NA2D_PROD_WAIT == 1
+  mbar_wait_hint(bar, parity);
+#elif NA2D_PROD_WAIT == 2
+  mbar_wait(bar, parity);
+#else
+  mbar_wait_sleep(bar, parity, 1024);
+#endif
+}
 // Wait with exponential back-off sleeps: for producer/issuer warps whose spinning would steal
 // issue slots from the compute warps sharing their SM sub-partition.
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity, uint32_t max_ns = 256) {
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity, uint32_t max_ns) {
   uint32_t ns = 16;
   while (!mbar_try_wait(bar, parity)) {
     __nanosleep(ns);
