@@ -353,3 +353,22 @@ def test_many_heads_class_switches():
     heads >= 64 by read-modify-write.  Swin-scale RPB: with the parity RPB this input reaches
     |dV| = 4.5, where bf16 output rounding alone costs up to 0.0156 of the 2e-2 bound (DESIGN R7)."""
     check(Shape("h72", 1, 72, 20, 20, 32, 5), "bf16", rpb="swin")
+
+
+FUZZ = []
+_rng = np.random.default_rng(20441)
+for _n in range(24):
+    _L = int(_rng.choice([3, 5, 7]))
+    _H, _W = int(_rng.integers(1, 41)), int(_rng.integers(1, 41))
+    _B = int(_rng.choice([1, 2, 3, 4, 6]))
+    _heads = int(_rng.integers(1, 5))
+    _d = int(_rng.choice([16, 32, 64]))
+    FUZZ.append((Shape(f"fuzz{_n}_{_B}x{_heads}x{_H}x{_W}d{_d}k{_L}", _B, _heads, _H, _W, _d, _L),
+                 "f16" if _n % 3 == 2 else "bf16"))
+
+
+@pytest.mark.parametrize("shape,dtype", FUZZ, ids=lambda x: x.name if isinstance(x, Shape) else x)
+def test_fuzz_shapes(shape, dtype):
+    """Seeded random geometry (maps 1..40 per axis incl. pair-mode sizes, batch / heads, d, L, bf16 /
+    fp16) against the oracle: catches tile-order, range-balancing, pair-mode and border-path slips."""
+    check(shape, dtype)
