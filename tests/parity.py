@@ -8,6 +8,9 @@ BASELINE.json's north_star:
   1e-3 * max(1, ||drpb_oracle||_inf) (a sum over up to B*H*W fp32 terms; dS is fp32 on every
   path, so the observed error is ~1e-6 relative);
 * fp32 path: ||gpu - oracle||_inf <= 1e-4 * max(1, ||oracle||_inf) per tensor.
+Reading R7b: an element whose oracle value has |x| >= 4 is stored in bf16 with a
+half-ULP of >= 0.0156, most of the 2e-2 budget by itself, so for those elements (only) the bound
+is 2e-2 plus the output type's half-ULP at |x|; the report keeps the plain max-abs error.
 Peripheral dRPB cells (one term per map) are pinned separately by the GPU cell probe
 (tests/test_gpu_parity.py::test_drpb_cell_probe).
 """
@@ -19,6 +22,14 @@ import os
 import numpy as np
 
 BF16_ATOL = 2e-2
+LARGE = 4.0  # |oracle| from which the output type's own rounding is added to the bound (R7b)
+
+
+def half_ulp(x: np.ndarray, dtype: str) -> np.ndarray:
+    """Half a unit in the last place of |x| in the 16-bit output type (bf16: 8, fp16: 11 significant bits)."""
+    _, e = np.frexp(np.abs(x))  # |x| = m 2^e, m in [0.5, 1)
+    bits = 8 if dtype == "bf16" else 11
+    return np.ldexp(1.0, e - 1 - bits)
 F32_RTOL = 1e-4
 DRPB_LONG_RTOL = 1e-3
 DRPB_SHORT = 4096
@@ -61,9 +72,17 @@ def compare(got: dict, ref: dict, dtype: str, names=None, terms: int | None = No
         r = np.asarray(r, np.float64)
         assert g.shape == r.shape, (n, g.shape, r.shape)
         assert np.all(np.isfinite(g)), f"{n}: non-finite values"
-        err = float(np.abs(g - r).max()) if g.size else 0.0
+        diff = np.abs(g - r)
+        err = float(diff.max()) if g.size else 0.0
         tol = tolerance(n, r, dtype, terms)
         report[n] = (err, tol)
+        if dtype != "f32" and tol == BF16_ATOL and err > tol:  # R7b: elements with |oracle| >= 4
+            big = np.abs(r) >= LARGE
+            bound = np.where(big, BF16_ATOL + half_ulp(r, dtype), BF16_ATOL)
+            worst = int(np.argmax(diff - bound))
+            assert np.all(diff <= bound), (f"{n}: err {diff.flat[worst]:.3e} > bound {bound.flat[worst]:.3e} "
+                                           f"at |x| = {abs(r.flat[worst]):.3f}")
+            continue
         assert err <= tol, f"{n}: max abs err {err:.3e} > tol {tol:.3e}"
     return report
 
