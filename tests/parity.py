@@ -8,7 +8,7 @@ BASELINE.json's north_star:
   1e-3 * max(1, ||drpb_oracle||_inf) (a sum over up to B*H*W fp32 terms; dS is fp32 on every
   path, so the observed error is ~1e-6 relative);
 * fp32 path: ||gpu - oracle||_inf <= 1e-4 * max(1, ||oracle||_inf) per tensor.
-Reading R7b: an element whose oracle value has |x| >= 4 is stored in bf16 with a
+Reading R7b: an element of out / dq / dk / dv whose oracle value has |x| >= 4 is stored in bf16 with a
 half-ULP of >= 0.0156, most of the 2e-2 budget by itself, so for those elements (only) the bound
 is 2e-2 plus the output type's half-ULP at |x|; the report keeps the plain max-abs error.
 Peripheral dRPB cells (one term per map) are pinned separately by the GPU cell probe
@@ -76,7 +76,8 @@ def compare(got: dict, ref: dict, dtype: str, names=None, terms: int | None = No
         err = float(diff.max()) if g.size else 0.0
         tol = tolerance(n, r, dtype, terms)
         report[n] = (err, tol)
-        if dtype != "f32" and tol == BF16_ATOL and err > tol:  # R7b: elements with |oracle| >= 4
+        # R7b: elements with |oracle| >= 4 of the 16-bit outputs (lse and drpb are fp32 outputs)
+        if dtype != "f32" and n in ("out", "dq", "dk", "dv") and tol == BF16_ATOL and err > tol:
             big = np.abs(r) >= LARGE
             bound = np.where(big, BF16_ATOL + half_ulp(r, dtype), BF16_ATOL)
             worst = int(np.argmax(diff - bound))

@@ -40,3 +40,10 @@ def test_other_elements_keep_the_strict_bound():
     got["out"][1, 0, 0, 0, 0] += 0.021  # an ordinary element just over 2e-2
     with pytest.raises(AssertionError):
         compare(got, ref, dt)
+
+
+def test_fp32_outputs_get_no_allowance():
+    r = {"out": np.zeros((1, 1, 8, 8, 1)), "lse": np.full((1, 1, 8, 8), 5.0)}
+    g = {"out": r["out"], "lse": r["lse"] + 0.03}
+    with pytest.raises(AssertionError, match="lse"):
+        compare(g, r, "bf16")
