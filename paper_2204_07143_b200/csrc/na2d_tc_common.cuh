@@ -29,24 +29,14 @@ struct BiasTable {
   static constexpr int TT = 2 * L - 1;
   static constexpr int TROWS = TT + 1;
   static constexpr int FLOATS = L * TROWS * kTblStride;
-  // element-parallel build (one global load per entry)
-  __device__ static void build_elems(float *tbl, const float *rpb, int h, int Lw, float mul, int tid, int nthreads) {
-    for (int e = tid; e < FLOATS; e += nthreads) {
-      const int dc = e / (TROWS * kTblStride);
-      const int rr = (e / kTblStride) % TROWS;
-      const int cb = e % kTblStride - kTblOff;
-      float v = -INFINITY;
-      if (rr < TT && cb >= dc && cb < dc + Lw) v = rpb ? __ldg(&rpb[(h * TT + rr) * TT + cb]) * mul : 0.f;
-      tbl[e] = v;
-    }
-  }
-  // `copies` (1 or 2) parity copies of the table (copy x holds column b at kTblOff + x + b: a reader
-  // whose first column has parity x uses copy x, so its element pairs are 8-byte aligned), plus `extra` all -inf classes after the L real
-  // ones (copy x at tbl + x * (L + extra) * TROWS * kTblStride), from a staged, pre-scaled copy of the
-  // head's (2L-1)^2 bias values in shared memory (rs, or null for no bias).  One table row per
-  // thread: no global load latency and no per-element index arithmetic inside the build (an
-  // element-parallel build straight from global memory took ~3.8 us per head in B1,
-  // scripts/trace_fixed.py).
+  // `copies` (1 or 2) parity copies of the table (copy x holds column b at kTblOff + x + b: a
+  // reader whose first column has parity x uses copy x, so its element pairs are 8-byte aligned),
+  // each with `extra` all -inf classes after the L real ones (copy x at
+  // tbl + x * (L + extra) * TROWS * kTblStride), built from a staged, pre-scaled copy of the head's
+  // (2L-1)^2 bias values in shared memory (rs, or null for no bias).  One table row per thread: no
+  // global load latency and no per-element index arithmetic inside the build (the element-parallel
+  // build straight from global memory it replaces took ~5.4 us per head in B1,
+  // scripts/trace_fixed.py).  B1 uses it; B2 keeps build_rows (measured faster there).
   __device__ static void build_rows_smem(float *tbl, const float *rs, int Lw, int copies, int extra, int tid,
                                          int nthreads) {
     const int per_copy = (L + extra) * TROWS;
