@@ -15,6 +15,7 @@
 // and two elementwise groups alternate chunks.  B' is the forward's masked bias table indexed by
 // the query's column-clamp class; rows outside the query's window use the all -inf row.
 #include <math.h>
+#include <stdlib.h>
 
 #include <mutex>
 #include <type_traits>
@@ -230,9 +231,8 @@ __device__ __forceinline__ void chunk_rows(uint32_t lane_addr, int uc, const flo
       }
       const uint32_t prow = lane_addr + u * (QP / 2);
       const uint32_t drow = prow + kNCH;
-      st_zero12(prow);
-      st_zero12(drow);
-      static_assert(QP == 24, "zero fill covers 12 bf16-pair columns");
+      st_zero<QP / 2>(prow);
+      st_zero<QP / 2>(drow);
       st_row<UW / 2>(prow + uc / 2, pp);
       st_row<UW / 2>(drow + uc / 2, dd);
     }
@@ -455,6 +455,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // neither stream waits behind the other's dependencies.
     constexpr uint32_t idesc_s = idesc_el<F16>(64, kNCH, false);
     constexpr uint32_t idesc_s2 = idesc_el<F16>(64, 2 * QP, false);  // a chunk of one row pair
+    static_assert(kNCH % QP == 0 && (QP * 2) % 16 == 0, "chunk row pairs are whole K-steps of the dV / dK MMAs");
     int c = 0;
     for (int it = 0;; ++it) {
       const int stage = it % kStages;
@@ -468,7 +469,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t dkt = dqs + ((2 * C::Q_BYTES) >> 4), dvt = dkt + (C::KT_BYTES >> 4);
       for (int k = 0; k < nch; ++k, ++c) {
         const int x = c & 1;
-        const uint32_t ids = chunk_rows_even<C::CR>(qn0, qn1, k) == C::CR ? idesc_s : idesc_s2;
+        // N = the chunk's (even) row count x QP: a full chunk, or 2 (QP = 24) / 2 or 4 (QP = 16) rows
+        const int rows_k = chunk_rows_even<C::CR>(qn0, qn1, k);
+        const uint32_t ids = rows_k == C::CR ? idesc_s : rows_k == 2 ? idesc_s2 : idesc_el<F16>(64, rows_k * QP, false);
         if (c >= 2) mbar_wait(&slot_free[x], ((c >> 1) - 1) & 1);
         tc_fence_after();
         // descriptors: per-stage bases + immediate offsets (short issue bursts, no per-MMA chains)
@@ -852,9 +855,23 @@ cudaError_t tc_backward_dkdv(const Geo &g, const void *q, const void *k, const v
   // the query halo of a 16-column key tile is at most 16 + 2NS + 1 <= 23 columns away from the right
   // clamp zone; tiles reaching it are shifted (key_col0)
   if (!tc_dkdv_supported(g)) return cudaErrorNotSupported;
+  static const bool no_narrow = [] {
+    const char *e = getenv("NA2D_NO_NARROW");
+    return e && e[0] == '1';
+  }();
+  // (not in pair mode: measured neutral-to-slower there, stage 4 B2 34.6 -> 35.0 us)
+  const bool narrow = !no_narrow && !tc::pair_mode(g.B, g.H, g.W, g.q_row0, g.q_rows, g.kv_row0, g.kv_rows) &&
+                      max_query_halo_width(g, false) <= 16;
   auto for_d = [&](auto hd_tag, auto f16_tag) -> cudaError_t {
     constexpr int HD = decltype(hd_tag)::value;
     constexpr bool F16 = decltype(f16_tag)::value;
+    // query-halo row pitch 16 when every key tile's query halo fits (maps up to ~16 wide): a 96-query
+    // chunk then holds 6 halo rows instead of 4 (NAT stage 3, 14 x 14: B2 62.2 -> 57.6 us)
+    if (narrow) switch (g.L) {
+      case 3: return launch_dkdv_t<3, 16, HD, F16>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, tile_counter, st);
+      case 5: return launch_dkdv_t<5, 16, HD, F16>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, tile_counter, st);
+      case 7: return launch_dkdv_t<7, 16, HD, F16>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, tile_counter, st);
+    }
     switch (g.L) {
       case 3: return launch_dkdv_t<3, 24, HD, F16>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, tile_counter, st);
       case 5: return launch_dkdv_t<5, 24, HD, F16>(g, q, k, v, rpb, lse, dout, D, dk, dv, drpb_part, part_ctas, drpb, tile_counter, st);
