@@ -265,7 +265,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t *full = bars, *empty = bars + kStages;
   uint64_t *s_full = bars + 2 * kStages, *ds_full = s_full + 2, *acc_full = s_full + 4, *acc_free = s_full + 6;
   uint64_t *slot_free = s_full + 8;  // chunk slot x: the dV/dK MMAs reading it have completed
-  uint32_t *tmem_slot = (uint32_t *)(bars + 2 * kStages + 10);
+  // stage s's MMA operands (K / V blocks, Q / dO halos) and tile description: what the MMA warps
+  // wait for; full[s] adds the LSE / D the elementwise warps need, so the MMAs never wait for those
+  uint64_t *full_mma = bars + 2 * kStages + 10;
+  uint32_t *tmem_slot = (uint32_t *)(full_mma + kStages);
 
   // broadcast from lane 0 so the compiler treats the warp index (and the TMEM addresses
   // derived from it) as warp-uniform: they stay in uniform registers, no R2UR per tcgen05.ld
@@ -290,6 +293,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == kProducerWarp && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], p.tma_lsd ? 1 : 1 + 32);  // expect_tx arrive (+ 32 lanes staging LSE / D)
+      mbar_init(&full_mma[s], 1);
       mbar_init(&empty[s], 1 + 8);                  // MMA commit + the 8 elementwise warps
     }
     for (int s = 0; s < 2; ++s) {
@@ -350,6 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (t >= p.num_tiles) {  // end of work: sentinel, released like a loaded stage
         if (lane == 0) {
           ti->bh = -1;
+          mbar_arrive(&full_mma[s]);
           mbar_arrive(&full[s]);
         }
         if (!p.tma_lsd) {
@@ -387,7 +392,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint8_t *st = smem + s * C::STAGE_BYTES;
       float *lsd = (float *)(st + 2 * C::Q_BYTES + 2 * C::KT_BYTES);
       if (elect_one()) {
-        mbar_expect_tx(&full[s], C::TX_BYTES + (p.tma_lsd ? 2 * C::QRH * C::LP * 4 : 0));
+        mbar_expect_tx(&full_mma[s], C::TX_BYTES);
+        mbar_expect_tx(&full[s], p.tma_lsd ? 2 * C::QRH * C::LP * 4 : 0);
         uint8_t *kt = st + 2 * C::Q_BYTES;
 #pragma unroll
         for (int sb = 0; sb < 2; ++sb)
@@ -395,15 +401,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int qb = 0; qb < 4; ++qb) {
             const int r0 = (64 * sb + 16 * qb) * kRB;
             const int kc = p.pair ? 4 * (qb & 1) : g.kc0 + 4 * qb, kbh = p.pair ? g.bh + (qb >> 1) * p.heads : g.bh;
-            tma_load_4d(kt + r0, &tm_k, &full[s], 0, kc, g.kr0 - p.kv_row0 + 4 * sb, kbh);
-            tma_load_4d(kt + C::KT_BYTES + r0, &tm_v, &full[s], 0, kc, g.kr0 - p.kv_row0 + 4 * sb, kbh);
+            tma_load_4d(kt + r0, &tm_k, &full_mma[s], 0, kc, g.kr0 - p.kv_row0 + 4 * sb, kbh);
+            tma_load_4d(kt + C::KT_BYTES + r0, &tm_v, &full_mma[s], 0, kc, g.kr0 - p.kv_row0 + 4 * sb, kbh);
           }
         if (p.pair) {  // both members' query halos side by side (row pitch QP, member m at m * QP / 2)
-          tma_load_5d(st, &tm_q, &full[s], 0, 0, 0, g.qr0 - p.q_row0, g.bh);
-          tma_load_5d(st + C::Q_BYTES, &tm_do, &full[s], 0, 0, 0, g.qr0 - p.q_row0, g.bh);
+          tma_load_5d(st, &tm_q, &full_mma[s], 0, 0, 0, g.qr0 - p.q_row0, g.bh);
+          tma_load_5d(st + C::Q_BYTES, &tm_do, &full_mma[s], 0, 0, 0, g.qr0 - p.q_row0, g.bh);
         } else {
-          tma_load_4d(st, &tm_q, &full[s], 0, g.qc0, g.qr0 - p.q_row0, g.bh);
-          tma_load_4d(st + C::Q_BYTES, &tm_do, &full[s], 0, g.qc0, g.qr0 - p.q_row0, g.bh);
+          tma_load_4d(st, &tm_q, &full_mma[s], 0, g.qc0, g.qr0 - p.q_row0, g.bh);
+          tma_load_4d(st + C::Q_BYTES, &tm_do, &full_mma[s], 0, g.qc0, g.qr0 - p.q_row0, g.bh);
         }
         // LSE / D last: the MMA operands first (B2 127.3 -> 125.6 us at cfg2; the query halos before
         // the key blocks measured 132.3)
@@ -461,7 +467,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int c = 0;
     for (int it = 0;; ++it) {
       const int stage = it % kStages;
-      mbar_wait(&full[stage], (it / kStages) & 1);
+      mbar_wait(&full_mma[stage], (it / kStages) & 1);
       if (lane == 0) ktrace(p, c, 3);
       const TileInfo &ti = tinfo[stage];
       if (ti.bh < 0) break;
@@ -503,7 +509,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int it = 0;; ++it) {
       const int stage = it % kStages, b = it % kNacc;
       // the stage cannot advance past this tile before this warp commits its empty[] below
-      mbar_wait(&full[stage], (it / kStages) & 1);
+      mbar_wait(&full_mma[stage], (it / kStages) & 1);
       const TileInfo &ti = tinfo[stage];
       if (ti.bh < 0) break;
       const int nch = ti.nchunks, row0a = ti.qs_lo[0] - ti.qr0, row0b = ti.qs_lo[1] - ti.qr0;
