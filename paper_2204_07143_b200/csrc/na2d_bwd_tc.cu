@@ -90,7 +90,10 @@ void make_b1_ranges(const TileOrder &o, const Geo &g, int grid, B1Ranges *r) {
   // cost of the order as a line: 4 per tile (quarter-tile units) plus kSwitchCost where a segment
   // starts; CTA c starts at the first tile whose cumulative cost reaches c / grid of the total (a
   // target that falls on a switch lands on the segment's first tile, so that CTA pays no switch)
-  constexpr long kSwitchCost = 6;  // 1.5 tiles
+#ifndef NA2D_B1_SWITCH_COST
+#define NA2D_B1_SWITCH_COST 12
+#endif
+  constexpr long kSwitchCost = NA2D_B1_SWITCH_COST;  // quarter tiles: 3 tiles (1.5 measured 2 us slower at cfg2)
   const long total = 4L * n + kSwitchCost * (ns - 1);
   r->start[0] = 0;
   int c = 1;

@@ -89,9 +89,10 @@ TileOrder make_tile_order(const Geo &g, int L);
 
 // B1's contiguous tile ranges: CTA c takes tiles [start[c], start[c + 1]) of the order.  A CTA whose
 // range crosses from one (class, head) segment into the next pays a dRPB flush (and on a head
-// change a partial-table commit and a bias-table rebuild): measured ~1.2-1.6 tiles' time each
-// (profiles/r02_b1_balance.txt).  The ranges are chosen so that tiles + kSwitchCost x switches is
-// balanced across CTAs instead of the tile count alone.
+// change a partial-table commit and a bias-table rebuild): traced at ~1.2-1.6 tiles' time each,
+// and border-class tiles run slower too (profiles/r02_b1_balance.txt).  The ranges are chosen so
+// that tiles + kSwitchCost x switches is balanced across CTAs instead of the tile count alone;
+// kSwitchCost = 3 tiles measured best (1.5: B1 cfg2 126.3 us, 3: 124.1 us, 5: 124.2 us).
 constexpr int kMaxB1Ctas = 256;
 struct B1Ranges {
   int start[kMaxB1Ctas + 1];
